@@ -1,0 +1,520 @@
+// The extern "C" boundary of libhelmb200.so (include/helmb200.h): plan and
+// workspace lifetime, the operator entry points, and the native GMRES driver
+// (gmres.py:65-177) that strings the kernels together with one scalar
+// read-back per iteration.
+#include <chrono>
+#include <cmath>
+#include <cstring>
+
+#include "ops.cuh"
+
+namespace helm {
+
+static thread_local std::string g_last_error;
+void set_last_error(const std::string& msg) { g_last_error = msg; }
+
+template <typename F>
+static int guarded(F&& f) {
+  try {
+    f();
+    return 0;
+  } catch (const std::exception& e) {
+    set_last_error(e.what());
+  } catch (...) {
+    set_last_error("unknown error");
+  }
+  return 1;
+}
+
+template <typename T>
+static T* upload(const void* host, size_t count) {
+  if (count == 0) return nullptr;
+  HELM_CHECK(host != nullptr, "missing setup array in helm_desc");
+  T* d = nullptr;
+  HELM_CUDA(cudaMalloc(&d, count * sizeof(T)));
+  HELM_CUDA(cudaMemcpy(d, host, count * sizeof(T), cudaMemcpyHostToDevice));
+  return d;
+}
+static void* upload_bytes(const void* host, size_t bytes) {
+  if (bytes == 0) return nullptr;
+  HELM_CHECK(host != nullptr, "missing setup array in helm_desc");
+  void* d = nullptr;
+  HELM_CUDA(cudaMalloc(&d, bytes));
+  HELM_CUDA(cudaMemcpy(d, host, bytes, cudaMemcpyHostToDevice));
+  return d;
+}
+
+// ---------------------------------------------------------------------------
+// composite operators
+// ---------------------------------------------------------------------------
+template <typename S> void op_apply_A(const helm_plan* P, const S* x, S* y, int batch, cudaStream_t st) {
+  launch_stencil<S>(P->geo, x, nullptr, y, batch, st);
+}
+
+template <typename S>
+static void op_coarse_correct(const helm_plan* P, helm_workspace* ws, const S* x, S* z, int batch, cudaStream_t st) {
+  S* c = (S*)ws->c;
+  launch_restrict<S>(P->geo, x, c, batch, st);
+  launch_coarse_solve<S>(P, ws, c, c, batch, st);
+  launch_prolong<S>(P->geo, c, z, batch, st);
+}
+
+// SchwarzPreconditioner.apply (schwarz.py:76-103): z = C x shared by every kind
+template <typename S>
+void op_apply_M(const helm_plan* P, helm_workspace* ws, const S* x, S* y, int batch, cudaStream_t st) {
+  HELM_CHECK((const void*)x != (const void*)y, "apply_M: input and output must not alias");
+  S* z = (S*)ws->z;
+  op_coarse_correct<S>(P, ws, x, z, batch, st);
+  const int kind = P->desc.kind;
+  if (kind == HELM_SHS2) {
+    S* d = (S*)ws->d;
+    launch_stencil<S>(P->geo, x, z, d, batch, st);  // d = x - A z (schwarz.py:88)
+    launch_local_sum<S>(P, d, z, y, (S*)ws->ovl, 1, batch, P->dev.band_node, st);
+  } else {
+    launch_local_sum<S>(P, x, z, y, (S*)ws->ovl, kind == HELM_SAS2 ? 1 : 0, batch, P->dev.band_node, st);
+  }
+}
+
+template void op_apply_A<double>(const helm_plan*, const double*, double*, int, cudaStream_t);
+template void op_apply_A<double2>(const helm_plan*, const double2*, double2*, int, cudaStream_t);
+template void op_apply_M<double>(const helm_plan*, helm_workspace*, const double*, double*, int, cudaStream_t);
+template void op_apply_M<double2>(const helm_plan*, helm_workspace*, const double2*, double2*, int, cudaStream_t);
+
+// ---------------------------------------------------------------------------
+// GMRES driver (gmres.py:65-177), statement-level mirror on device buffers
+// ---------------------------------------------------------------------------
+template <typename S> struct DevBuf {
+  S* p = nullptr;
+  cudaStream_t st;
+  DevBuf(size_t n, cudaStream_t s) : st(s) { HELM_CUDA(cudaMallocAsync((void**)&p, n * sizeof(S), s)); }
+  ~DevBuf() {
+    if (p) cudaFreeAsync(p, st);
+  }
+};
+
+template <typename S>
+static void gmres_impl(const helm_plan* P, helm_workspace* ws, const S* b, S* x, double rtol, int mi, int side,
+                       int use_precond, double* history, helm_gmres_report* rep, cudaStream_t st) {
+  const auto t0 = std::chrono::steady_clock::now();
+  HELM_CHECK(rtol > 0.0, "relative tolerance must be positive");
+  HELM_CHECK(mi >= 1, "iteration cap must be at least 1");
+  HELM_CHECK(side == 0 || side == 1, "side must be 0 (right) or 1 (left)");
+  const size_t N = (size_t)P->N;
+  const bool left = side == 1;
+  DevBuf<S> V((size_t)(mi + 1) * N, st), H((size_t)(mi + 1) * mi, st), cs(mi, st), sn(mi, st), g(mi + 1, st),
+      y(mi + 1, st), u(N, st), r(N, st);
+  DevBuf<char> scratch(krylov_scratch_bytes(mi + 1), st);
+  DevBuf<double> scal(16, st);
+  HELM_CUDA(cudaMemsetAsync(H.p, 0, (size_t)(mi + 1) * mi * sizeof(S), st));
+  HELM_CUDA(cudaMemsetAsync(cs.p, 0, mi * sizeof(S), st));
+  HELM_CUDA(cudaMemsetAsync(sn.p, 0, mi * sizeof(S), st));
+  HELM_CUDA(cudaMemsetAsync(g.p, 0, (mi + 1) * sizeof(S), st));
+  double* hp = (double*)ws->pinned;
+
+  auto applyM = [&](const S* in, S* out) {
+    if (use_precond)
+      op_apply_M<S>(P, ws, in, out, 1, st);
+    else
+      HELM_CUDA(cudaMemcpyAsync(out, in, N * sizeof(S), cudaMemcpyDeviceToDevice, st));
+  };
+  auto applyOp = [&](const S* in, S* out) {  // right: A M in ; left: M A in
+    if (left) {
+      op_apply_A<S>(P, in, u.p, 1, st);
+      applyM(u.p, out);
+    } else {
+      applyM(in, u.p);
+      op_apply_A<S>(P, u.p, out, 1, st);
+    }
+  };
+  auto read_scalars = [&](const double* dev, int n) {
+    HELM_CUDA(cudaMemcpyAsync(hp, dev, n * sizeof(double), cudaMemcpyDeviceToHost, st));
+    HELM_CUDA(cudaStreamSynchronize(st));
+  };
+
+  // ||b||, r0 (gmres.py:77-86)
+  krylov_norm2<S>(b, N, scal.p, scratch.p, st);
+  if (left)
+    applyM(b, V.p);
+  else
+    HELM_CUDA(cudaMemcpyAsync(V.p, b, N * sizeof(S), cudaMemcpyDeviceToDevice, st));
+  krylov_norm2<S>(V.p, N, scal.p + 1, scratch.p, st);
+  read_scalars(scal.p, 2);
+  const double bnorm = std::sqrt(hp[0]), beta = std::sqrt(hp[1]);
+  HELM_CHECK(bnorm != 0.0, "right-hand side must be nonzero");
+  // V[0] = r0 / beta ; g[0] = beta
+  double sc[2] = {1.0 / beta, beta};
+  HELM_CUDA(cudaMemcpyAsync(scal.p + 6, sc, 2 * sizeof(double), cudaMemcpyHostToDevice, st));
+  krylov_scale<S>(V.p, V.p, scal.p + 6, 0, N, st);
+  S g0 = Sc<S>::from_real(beta);
+  HELM_CUDA(cudaMemcpyAsync(g.p, &g0, sizeof(S), cudaMemcpyHostToDevice, st));
+  if (history) history[0] = 1.0;
+
+  auto form_solution = [&](int j) {  // gmres.py:98-105
+    krylov_backsolve<S>(H.p, mi, j, g.p, y.p, st);
+    if (left) {
+      krylov_combine<S>(x, V.p, j + 1, N, y.p, N, st);
+    } else {
+      krylov_combine<S>(r.p, V.p, j + 1, N, y.p, N, st);
+      applyM(r.p, x);
+    }
+  };
+  auto true_residual = [&]() {  // ||b - A x|| / ||b||  (gmres.py:153)
+    launch_stencil<S>(P->geo, b, x, r.p, 1, st);
+    krylov_norm2<S>(r.p, N, scal.p + 8, scratch.p, st);
+    read_scalars(scal.p + 8, 1);
+    return std::sqrt(hp[0]) / bnorm;
+  };
+
+  bool done = false;
+  for (int j = 0; j < mi && !done; ++j) {
+    S* vj = V.p + (size_t)j * N;
+    applyOp(vj, vj + N);
+    krylov_cgs2_impl<S>(V.p, j, N, N, H.p + j, (size_t)mi, scal.p + 2, scratch.p, st);
+    krylov_givens<S>(H.p, mi, j, cs.p, sn.p, g.p, beta, scal.p + 4, st);
+    HELM_CUDA(cudaMemcpyAsync(hp, scal.p + 2, 3 * sizeof(double), cudaMemcpyDeviceToHost, st));
+    HELM_CUDA(cudaStreamSynchronize(st));
+    const bool brk = hp[1] != 0.0;
+    const double est = hp[2];
+    if (history) history[j + 1] = est;
+    if (est <= rtol || brk) {
+      form_solution(j);
+      const double true_rel = true_residual();
+      const bool conv = left ? est <= rtol : true_rel <= rtol;
+      if (conv || brk) {
+        rep->iterations = j + 1;
+        rep->converged = conv;
+        rep->breakdown = brk && !conv;
+        rep->final_residual = true_rel;
+        done = true;
+      }
+    }
+  }
+  if (!done) {
+    form_solution(mi - 1);
+    rep->iterations = mi;
+    rep->converged = 0;
+    rep->breakdown = 0;
+    rep->final_residual = true_residual();
+  }
+  HELM_CUDA(cudaStreamSynchronize(st));
+  rep->wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
+// ---------------------------------------------------------------------------
+// plan construction
+// ---------------------------------------------------------------------------
+static void build_plan(const helm_desc* d, helm_plan* P) {
+  HELM_CHECK(d != nullptr, "null descriptor");
+  HELM_CHECK(d->n >= 5 && (d->n % 2) == 1, "n must be odd and >= 5");
+  HELM_CHECK(d->bc == HELM_DIRICHLET || d->bc == HELM_SOMMERFELD, "unknown boundary condition");
+  HELM_CHECK(d->is_complex == (d->bc == HELM_SOMMERFELD ? 1 : 0),
+             "MP-1 (Dirichlet) plans are fp64, MP-2 (Sommerfeld) plans complex128");
+  HELM_CHECK(d->kind >= HELM_AS2 && d->kind <= HELM_SHS2, "unknown preconditioner kind");
+  HELM_CHECK(d->ratio == 2, "only the HOCS coarse ratio 2 (H = 2h) is implemented");
+  // p == 0 (no boxes) and coarse_V == NULL (no coarse solver) give an operator-only plan
+  HELM_CHECK(d->p == 0 || (d->p >= 1 && (d->n - 1) % d->p == 0), "p must divide the cell count n-1");
+  HELM_CHECK(d->refine_steps >= 0 && d->refine_steps <= 8, "refine_steps out of range");
+  P->desc = *d;
+  P->elem = d->is_complex ? sizeof(double2) : sizeof(double);
+  Geo& g = P->geo;
+  const double h = 1.0 / (d->n - 1);
+  g.nu = d->bc == HELM_DIRICHLET ? d->n - 2 : d->n;
+  g.m0 = d->bc == HELM_DIRICHLET ? (d->n - 3) / 2 : (d->n + 1) / 2;
+  HELM_CHECK(d->m0 == g.m0, "descriptor m0 does not match the grid");
+  g.off = d->bc == HELM_DIRICHLET ? 1 : 0;
+  g.sommerfeld = d->bc == HELM_SOMMERFELD;
+  g.inv_h2 = 1.0 / (h * h);
+  g.k2 = d->k * d->k;
+  g.tb = mk(1.0 / (h * h), -d->k / h);
+  P->N = (int64_t)g.nu * g.nu;
+  P->N0 = (int64_t)g.m0 * g.m0;
+  const int nu = g.nu, p = d->p;
+
+  // boxes and per-node overlap maps (decomposition.py:111-134 weights = 1/multiplicity)
+  PlanDev& dv = P->dev;
+  std::memset(&dv, 0, sizeof(dv));
+  const size_t m0 = g.m0;
+  if (d->coarse_V) {
+    dv.coarse_V = upload_bytes(d->coarse_V, m0 * m0 * P->elem);
+    dv.coarse_lambda = upload_bytes(d->coarse_lambda, m0 * P->elem);
+    dv.t0_band = upload_bytes(d->t0_band, m0 * 5 * P->elem);
+    dv.m0_band = upload_bytes(d->m0_band, m0 * 5 * P->elem);
+    dv.band_piv = (uint8_t*)upload_bytes(d->band_piv, m0 * m0);
+    dv.band_l = upload_bytes(d->band_l, m0 * m0 * 2 * P->elem);
+    dv.band_u = upload_bytes(d->band_u, m0 * m0 * 5 * P->elem);
+  }
+  if (p == 0) return;
+  P->h_box_start.assign(d->box_start, d->box_start + p);
+  P->h_box_len.assign(d->box_len, d->box_len + p);
+  P->h_box_class.assign(d->box_class, d->box_class + p);
+  HELM_CHECK(d->n_classes >= 1, "need at least one local class");
+  P->h_class_len.assign(d->class_len, d->class_len + d->n_classes);
+  std::vector<int> first(nu, -1), mult(nu, 0), band(nu, -1), band_node;
+  int max_len = 0;
+  for (int a = 0; a < p; ++a) {
+    const int s = P->h_box_start[a], L = P->h_box_len[a], c = P->h_box_class[a];
+    HELM_CHECK(s >= 0 && L >= 1 && s + L <= nu, "box outside the unknown range");
+    HELM_CHECK(c >= 0 && c < d->n_classes && P->h_class_len[c] == L, "box class length mismatch");
+    max_len = std::max(max_len, L);
+    for (int i = s; i < s + L; ++i) {
+      if (first[i] < 0) first[i] = a;
+      mult[i] += 1;
+    }
+  }
+  for (int i = 0; i < nu; ++i) {
+    HELM_CHECK(mult[i] >= 1, "an unknown is covered by no subdomain");
+    HELM_CHECK(mult[i] <= 2, "more than two subdomains overlap along one dimension");
+    if (mult[i] == 2) {
+      band[i] = (int)band_node.size();
+      band_node.push_back(i);
+    }
+  }
+  const size_t smem = (size_t)(4 * max_len * max_len + 2 * max_len) * P->elem;
+  HELM_CHECK(smem <= 200 * 1024, "subdomain too large for the shared-memory FDM kernel");
+  dv.p = p;
+  dv.max_len = max_len;
+  dv.n_classes = d->n_classes;
+  dv.nbands = (int)band_node.size();
+  dv.box_start = upload<int>(d->box_start, p);
+  dv.box_len = upload<int>(d->box_len, p);
+  dv.box_class = upload<int>(d->box_class, p);
+  dv.class_len = upload<int>(d->class_len, d->n_classes);
+  std::vector<int> offV(d->n_classes), offL(d->n_classes);
+  size_t totV = 0, totL = 0;
+  for (int c = 0; c < d->n_classes; ++c) {
+    offV[c] = (int)totV;
+    offL[c] = (int)totL;
+    totV += (size_t)P->h_class_len[c] * P->h_class_len[c];
+    totL += P->h_class_len[c];
+  }
+  dv.class_off_V = upload<int>(offV.data(), offV.size());
+  dv.class_off_lam = upload<int>(offL.data(), offL.size());
+  dv.class_V = upload_bytes(d->class_V, totV * P->elem);
+  dv.class_lambda = upload_bytes(d->class_lambda, totL * P->elem);
+  dv.node_first_box = upload<int>(first.data(), nu);
+  dv.node_mult = upload<int>(mult.data(), nu);
+  dv.node_band = upload<int>(band.data(), nu);
+  dv.band_node = band_node.empty() ? nullptr : upload<int>(band_node.data(), band_node.size());
+}
+
+static void finish_desc(helm_plan* P) {
+  // pointer members of the stored descriptor are not owned: clear them
+  P->desc.box_start = P->desc.box_len = P->desc.box_class = P->desc.class_len = nullptr;
+  P->desc.class_V = P->desc.class_lambda = P->desc.coarse_V = P->desc.coarse_lambda = nullptr;
+  P->desc.t0_band = P->desc.m0_band = P->desc.band_l = P->desc.band_u = nullptr;
+  P->desc.band_piv = nullptr;
+}
+
+static void free_plan(helm_plan* P) {
+  PlanDev& dv = P->dev;
+  void* ptrs[] = {dv.box_start, dv.box_len, dv.box_class, dv.class_len, dv.class_off_V, dv.class_off_lam,
+                  dv.class_V, dv.class_lambda, dv.node_first_box, dv.node_mult, dv.node_band, dv.band_node,
+                  dv.coarse_V, dv.coarse_lambda, dv.t0_band, dv.m0_band, dv.band_piv, dv.band_l, dv.band_u};
+  for (void* q : ptrs)
+    if (q) cudaFree(q);
+}
+
+template <typename F>
+static void dispatch(const helm_plan* P, F&& f) {
+  if (P->desc.is_complex)
+    f(double2{});
+  else
+    f(double{});
+}
+
+}  // namespace helm
+
+using namespace helm;
+
+extern "C" {
+
+int32_t helm_abi_version(void) { return HELM_ABI_VERSION; }
+const char* helm_last_error(void) { return g_last_error.c_str(); }
+
+int helm_plan_create(const helm_desc* desc, helm_plan** out) {
+  return guarded([&] {
+    HELM_CHECK(out != nullptr, "null output pointer");
+    helm_plan* P = new helm_plan();
+    try {
+      build_plan(desc, P);
+      finish_desc(P);
+    } catch (...) {
+      free_plan(P);
+      delete P;
+      throw;
+    }
+    *out = P;
+  });
+}
+
+int helm_plan_destroy(helm_plan* plan) {
+  return guarded([&] {
+    if (!plan) return;
+    free_plan(plan);
+    delete plan;
+  });
+}
+
+int64_t helm_plan_num_unknowns(const helm_plan* plan) { return plan ? plan->N : -1; }
+int64_t helm_plan_num_coarse(const helm_plan* plan) { return plan ? plan->N0 : -1; }
+
+int helm_workspace_create(const helm_plan* P, int32_t max_batch, helm_workspace** out) {
+  return guarded([&] {
+    HELM_CHECK(P && out && max_batch >= 1, "bad workspace arguments");
+    helm_workspace* w = new helm_workspace();
+    std::memset(w, 0, sizeof(*w));
+    w->plan = P;
+    w->max_batch = max_batch;
+    const size_t B = max_batch, e = P->elem;
+    HELM_CUBLAS(cublasCreate(&w->cublas));
+    HELM_CUDA(cudaMalloc(&w->z, B * P->N * e));
+    HELM_CUDA(cudaMalloc(&w->d, B * P->N * e));
+    void** coarse[] = {&w->c, &w->g, &w->y0, &w->r0, &w->e0};
+    for (void** q : coarse) HELM_CUDA(cudaMalloc(q, B * P->N0 * e));
+    const size_t novl = std::max<size_t>(1, B * 6 * (size_t)P->dev.nbands * P->geo.nu);
+    HELM_CUDA(cudaMalloc(&w->ovl, novl * e));
+    w->red_bytes = krylov_scratch_bytes(4096);
+    HELM_CUDA(cudaMalloc(&w->red, w->red_bytes));
+    HELM_CUDA(cudaMallocHost(&w->pinned, 64 * sizeof(double)));
+    *out = w;
+  });
+}
+
+int helm_workspace_destroy(helm_workspace* w) {
+  return guarded([&] {
+    if (!w) return;
+    void* ptrs[] = {w->z, w->d, w->c, w->g, w->y0, w->r0, w->e0, w->ovl, w->red};
+    for (void* q : ptrs)
+      if (q) cudaFree(q);
+    if (w->pinned) cudaFreeHost(w->pinned);
+    if (w->cublas) cublasDestroy(w->cublas);
+    delete w;
+  });
+}
+
+#define HELM_BATCH_CHECK(ws, batch) \
+  HELM_CHECK((batch) >= 1 && (!(ws) || (batch) <= (ws)->max_batch), "batch exceeds the workspace capacity")
+
+int helm_apply_A(const helm_plan* P, const void* x, void* y, int32_t batch, void* stream) {
+  return guarded([&] {
+    HELM_CHECK(P && x && y && batch >= 1, "bad arguments");
+    dispatch(P, [&](auto t) {
+      using S = decltype(t);
+      op_apply_A<S>(P, (const S*)x, (S*)y, batch, (cudaStream_t)stream);
+    });
+  });
+}
+
+int helm_deflate(const helm_plan* P, const void* x, const void* z, void* y, int32_t batch, void* stream) {
+  return guarded([&] {
+    HELM_CHECK(P && x && z && y && batch >= 1, "bad arguments");
+    dispatch(P, [&](auto t) {
+      using S = decltype(t);
+      launch_stencil<S>(P->geo, (const S*)x, (const S*)z, (S*)y, batch, (cudaStream_t)stream);
+    });
+  });
+}
+
+int helm_restrict(const helm_plan* P, const void* x, void* c, int32_t batch, void* stream) {
+  return guarded([&] {
+    HELM_CHECK(P && x && c && batch >= 1, "bad arguments");
+    dispatch(P, [&](auto t) {
+      using S = decltype(t);
+      launch_restrict<S>(P->geo, (const S*)x, (S*)c, batch, (cudaStream_t)stream);
+    });
+  });
+}
+
+int helm_prolong(const helm_plan* P, const void* c, void* z, int32_t batch, void* stream) {
+  return guarded([&] {
+    HELM_CHECK(P && c && z && batch >= 1, "bad arguments");
+    dispatch(P, [&](auto t) {
+      using S = decltype(t);
+      launch_prolong<S>(P->geo, (const S*)c, (S*)z, batch, (cudaStream_t)stream);
+    });
+  });
+}
+
+int helm_coarse_solve(const helm_plan* P, helm_workspace* ws, const void* c, void* y, int32_t batch, void* stream) {
+  return guarded([&] {
+    HELM_CHECK(P && ws && c && y, "bad arguments");
+    HELM_BATCH_CHECK(ws, batch);
+    dispatch(P, [&](auto t) {
+      using S = decltype(t);
+      launch_coarse_solve<S>(P, ws, (const S*)c, (S*)y, batch, (cudaStream_t)stream);
+    });
+  });
+}
+
+int helm_coarse_correct(const helm_plan* P, helm_workspace* ws, const void* x, void* z, int32_t batch, void* stream) {
+  return guarded([&] {
+    HELM_CHECK(P && ws && x && z, "bad arguments");
+    HELM_BATCH_CHECK(ws, batch);
+    dispatch(P, [&](auto t) {
+      using S = decltype(t);
+      op_coarse_correct<S>(P, ws, (const S*)x, (S*)z, batch, (cudaStream_t)stream);
+    });
+  });
+}
+
+int helm_local_sum(const helm_plan* P, helm_workspace* ws, const void* x, const void* base, void* y,
+                   int32_t weighted, int32_t batch, void* stream) {
+  return guarded([&] {
+    HELM_CHECK(P && ws && x && y, "bad arguments");
+    HELM_CHECK(x != y, "local_sum: input and output must not alias");
+    HELM_BATCH_CHECK(ws, batch);
+    dispatch(P, [&](auto t) {
+      using S = decltype(t);
+      launch_local_sum<S>(P, (const S*)x, (const S*)base, (S*)y, (S*)ws->ovl, weighted ? 1 : 0, batch,
+                          P->dev.band_node, (cudaStream_t)stream);
+    });
+  });
+}
+
+int helm_apply_M(const helm_plan* P, helm_workspace* ws, const void* x, void* y, int32_t batch, void* stream) {
+  return guarded([&] {
+    HELM_CHECK(P && ws && x && y, "bad arguments");
+    HELM_BATCH_CHECK(ws, batch);
+    dispatch(P, [&](auto t) {
+      using S = decltype(t);
+      op_apply_M<S>(P, ws, (const S*)x, (S*)y, batch, (cudaStream_t)stream);
+    });
+  });
+}
+
+int helm_cgs2(const helm_plan* P, helm_workspace* ws, void* V, int32_t j, void* hcol, void* stream) {
+  return guarded([&] {
+    HELM_CHECK(P && ws && V && hcol && j >= 0, "bad arguments");
+    HELM_CHECK(krylov_scratch_bytes(j + 1) <= ws->red_bytes, "basis too large for the workspace scratch");
+    dispatch(P, [&](auto t) {
+      using S = decltype(t);
+      krylov_cgs2<S>((S*)V, j, (size_t)P->N, (size_t)P->N, (S*)hcol, ws->red, (cudaStream_t)stream);
+    });
+  });
+}
+
+int helm_givens(const helm_plan* P, void* H, int32_t ldh, int32_t j, void* cs, void* sn, void* g, double beta,
+                double* est_out, void* stream) {
+  return guarded([&] {
+    HELM_CHECK(P && H && cs && sn && g && est_out && j >= 0 && ldh > j, "bad arguments");
+    dispatch(P, [&](auto t) {
+      using S = decltype(t);
+      krylov_givens<S>((S*)H, ldh, j, (S*)cs, (S*)sn, (S*)g, beta, est_out, (cudaStream_t)stream);
+    });
+  });
+}
+
+int helm_gmres(const helm_plan* P, helm_workspace* ws, const void* b, void* x, double rtol, int32_t max_iter,
+               int32_t side, int32_t use_precond, double* history, helm_gmres_report* report, void* stream) {
+  return guarded([&] {
+    HELM_CHECK(P && ws && b && x && report, "bad arguments");
+    HELM_CHECK(b != x, "gmres: b and x must not alias");
+    dispatch(P, [&](auto t) {
+      using S = decltype(t);
+      gmres_impl<S>(P, ws, (const S*)b, (S*)x, rtol, max_iter, side, use_precond, history, report,
+                    (cudaStream_t)stream);
+    });
+  });
+}
+
+}  // extern "C"

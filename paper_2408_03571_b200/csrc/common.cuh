@@ -1,0 +1,178 @@
+// Shared device helpers for libhelmb200: the scalar algebra used by every
+// kernel (fp64 for MP-1, interleaved complex128 = double2 for MP-2), error
+// plumbing, and the internal plan/workspace structs.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cublas_v2.h>
+#include <cstdint>
+#include <cstdio>
+#include <string>
+#include <stdexcept>
+#include <vector>
+
+#include "../../include/helmb200.h"
+
+namespace helm {
+
+// ----------------------------------------------------------------------------
+// scalar algebra: the same kernel source serves fp64 and complex128
+// ----------------------------------------------------------------------------
+__host__ __device__ __forceinline__ double2 mk(double r, double i) { return make_double2(r, i); }
+
+template <typename S> struct Sc;
+template <> struct Sc<double> {
+  static constexpr bool cplx = false;
+  __host__ __device__ __forceinline__ static double zero() { return 0.0; }
+  __host__ __device__ __forceinline__ static double from_real(double r) { return r; }
+};
+template <> struct Sc<double2> {
+  static constexpr bool cplx = true;
+  __host__ __device__ __forceinline__ static double2 zero() { return mk(0.0, 0.0); }
+  __host__ __device__ __forceinline__ static double2 from_real(double r) { return mk(r, 0.0); }
+};
+
+__host__ __device__ __forceinline__ double add(double a, double b) { return a + b; }
+__host__ __device__ __forceinline__ double2 add(double2 a, double2 b) { return mk(a.x + b.x, a.y + b.y); }
+__host__ __device__ __forceinline__ double sub(double a, double b) { return a - b; }
+__host__ __device__ __forceinline__ double2 sub(double2 a, double2 b) { return mk(a.x - b.x, a.y - b.y); }
+__host__ __device__ __forceinline__ double mul(double a, double b) { return a * b; }
+__host__ __device__ __forceinline__ double2 mul(double2 a, double2 b) {
+  return mk(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+__host__ __device__ __forceinline__ double2 mul(double a, double2 b) { return mk(a * b.x, a * b.y); }
+__host__ __device__ __forceinline__ double2 mul(double2 a, double b) { return mk(a.x * b, a.y * b); }
+// a + b*c
+__host__ __device__ __forceinline__ double fma_(double b, double c, double a) { return fma(b, c, a); }
+__host__ __device__ __forceinline__ double2 fma_(double2 b, double2 c, double2 a) {
+  return mk(fma(b.x, c.x, fma(-b.y, c.y, a.x)), fma(b.x, c.y, fma(b.y, c.x, a.y)));
+}
+__host__ __device__ __forceinline__ double2 fma_(double b, double2 c, double2 a) {
+  return mk(fma(b, c.x, a.x), fma(b, c.y, a.y));
+}
+// a - b*c
+__host__ __device__ __forceinline__ double fms_(double b, double c, double a) { return fma(-b, c, a); }
+__host__ __device__ __forceinline__ double2 fms_(double2 b, double2 c, double2 a) {
+  return mk(fma(-b.x, c.x, fma(b.y, c.y, a.x)), fma(-b.x, c.y, fma(-b.y, c.x, a.y)));
+}
+__host__ __device__ __forceinline__ double conj_(double a) { return a; }
+__host__ __device__ __forceinline__ double2 conj_(double2 a) { return mk(a.x, -a.y); }
+// conj(a) * b
+__host__ __device__ __forceinline__ double cmul(double a, double b) { return a * b; }
+__host__ __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  return mk(a.x * b.x + a.y * b.y, a.x * b.y - a.y * b.x);
+}
+__host__ __device__ __forceinline__ double abs2(double a) { return a * a; }
+__host__ __device__ __forceinline__ double abs2(double2 a) { return a.x * a.x + a.y * a.y; }
+__host__ __device__ __forceinline__ double scale(double a, double s) { return a * s; }
+__host__ __device__ __forceinline__ double2 scale(double2 a, double s) { return mk(a.x * s, a.y * s); }
+// a / b  (Smith-free: the denominators here are O(1/h^2), far from overflow)
+__host__ __device__ __forceinline__ double div_(double a, double b) { return a / b; }
+__host__ __device__ __forceinline__ double2 div_(double2 a, double2 b) {
+  double d = b.x * b.x + b.y * b.y;
+  return mk((a.x * b.x + a.y * b.y) / d, (a.y * b.x - a.x * b.y) / d);
+}
+__host__ __device__ __forceinline__ double recip(double b) { return 1.0 / b; }
+__host__ __device__ __forceinline__ double2 recip(double2 b) {
+  double d = b.x * b.x + b.y * b.y;
+  return mk(b.x / d, -b.y / d);
+}
+
+// ----------------------------------------------------------------------------
+// error plumbing
+// ----------------------------------------------------------------------------
+struct Error : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+void set_last_error(const std::string& msg);
+
+#define HELM_CUDA(call)                                                                   \
+  do {                                                                                    \
+    cudaError_t e_ = (call);                                                              \
+    if (e_ != cudaSuccess)                                                                \
+      throw ::helm::Error(std::string(#call) + ": " + cudaGetErrorString(e_) + " @" +      \
+                          __FILE__ + ":" + std::to_string(__LINE__));                     \
+  } while (0)
+#define HELM_CUBLAS(call)                                                                 \
+  do {                                                                                    \
+    cublasStatus_t s_ = (call);                                                           \
+    if (s_ != CUBLAS_STATUS_SUCCESS)                                                      \
+      throw ::helm::Error(std::string(#call) + ": cublas status " + std::to_string((int)s_)); \
+  } while (0)
+#define HELM_CHECK(cond, msg)                                                             \
+  do {                                                                                    \
+    if (!(cond)) throw ::helm::Error(msg);                                                \
+  } while (0)
+#define HELM_LAUNCH_CHECK() HELM_CUDA(cudaGetLastError())
+
+// ----------------------------------------------------------------------------
+// grid geometry shared by the stencil, transfer and local kernels
+// ----------------------------------------------------------------------------
+struct Geo {
+  int nu;        // unknowns per dimension
+  int m0;        // coarse unknowns per dimension
+  int off;       // fine unknown u of coarse unknown U is 2U + off + d (0 Sommerfeld, 1 Dirichlet)
+  int sommerfeld;
+  double inv_h2; // 1/h^2
+  double k2;     // k^2
+  double2 tb;    // Sommerfeld 1-D end diagonal 1/h^2 - i k/h (discretization.py:136-148)
+};
+
+// Device-side constants of a plan (device pointers).
+struct PlanDev {
+  // 1-D boxes
+  int p;
+  int* box_start;
+  int* box_len;
+  int* box_class;
+  int n_classes;
+  int max_len;
+  int* class_len;
+  int* class_off_V;    // element offset of class c in class_V
+  int* class_off_lam;  // element offset of class c in class_lambda
+  void* class_V;
+  void* class_lambda;
+  // per-unknown 1-D overlap bookkeeping
+  int* node_first_box; // first box containing unknown i
+  int* node_mult;      // 1 or 2
+  int* node_band;      // compact overlap-band index or -1
+  int* band_node;      // inverse of node_band
+  int nbands;          // number of 1-D unknowns with multiplicity 2
+  // coarse
+  void* coarse_V;
+  void* coarse_lambda;
+  void* t0_band;
+  void* m0_band;
+  uint8_t* band_piv;
+  void* band_l;
+  void* band_u;
+};
+
+}  // namespace helm
+
+struct helm_plan {
+  helm_desc desc;  // scalars only (pointer members cleared)
+  helm::Geo geo;
+  helm::PlanDev dev;
+  int64_t N;
+  int64_t N0;
+  size_t elem;     // bytes per scalar
+  std::vector<int> h_box_start, h_box_len, h_box_class, h_class_len;
+};
+
+struct helm_workspace {
+  const helm_plan* plan;
+  int max_batch;
+  cublasHandle_t cublas;
+  void* z;        // [B][N]
+  void* d;        // [B][N]
+  void* c;        // [B][N0]
+  void* g;        // [B][N0]
+  void* y0;       // [B][N0]
+  void* r0;       // [B][N0]
+  void* e0;       // [B][N0]
+  void* ovl;      // overlap scratch [B][6][nbands][nu]
+  void* red;      // reduction scratch (doubles)
+  size_t red_bytes;
+  void* pinned;   // small pinned host buffer for scalar read-back
+};

@@ -1,0 +1,42 @@
+// Internal launcher declarations shared between the kernel translation units.
+#pragma once
+#include "common.cuh"
+
+namespace helm {
+
+template <typename S> void launch_stencil(const Geo& g, const S* x, const S* z, S* y, int batch, cudaStream_t st);
+template <typename S> void launch_restrict(const Geo& g, const S* x, S* c, int batch, cudaStream_t st);
+template <typename S> void launch_prolong(const Geo& g, const S* c, S* z, int batch, cudaStream_t st);
+template <typename S>
+void launch_local_sum(const helm_plan* P, const S* x, const S* base, S* y, S* ovl, int weighted, int batch,
+                      const int* band_node, cudaStream_t st);
+template <typename S>
+void launch_coarse_solve(const helm_plan* P, helm_workspace* ws, const S* c, S* y, int batch, cudaStream_t st);
+
+// composite operators (capi.cu)
+template <typename S> void op_apply_A(const helm_plan* P, const S* x, S* y, int batch, cudaStream_t st);
+template <typename S>
+void op_apply_M(const helm_plan* P, helm_workspace* ws, const S* x, S* y, int batch, cudaStream_t st);
+
+// Krylov kernels (krylov.cu)
+template <typename S>
+void krylov_dots(const S* V, int nvec, size_t ldv, const S* w, size_t N, S* out, void* scratch, cudaStream_t st);
+template <typename S>
+void krylov_update(S* w, const S* V, int nvec, size_t ldv, const S* h, double sign, size_t N, double* norm2_out,
+                   void* scratch, cudaStream_t st);
+template <typename S> void krylov_norm2(const S* x, size_t N, double* out, void* scratch, cudaStream_t st);
+template <typename S>
+void krylov_combine(S* x, const S* V, int nvec, size_t ldv, const S* h, size_t N, cudaStream_t st);
+template <typename S>
+void krylov_cgs2_impl(S* V, int j, size_t ldv, size_t N, S* hcol, size_t hstride, double* inv_out, void* scratch,
+                      cudaStream_t st);
+template <typename S>
+void krylov_cgs2(S* V, int j, size_t ldv, size_t N, S* hcol, void* scratch, cudaStream_t st);
+template <typename S>
+void krylov_givens(S* H, int ldh, int j, S* cs, S* sn, S* g, double beta, double* est, cudaStream_t st);
+template <typename S> void krylov_backsolve(const S* H, int ldh, int j, const S* g, S* y, cudaStream_t st);
+template <typename S> void krylov_scale(S* x, const S* src, const double* s, int invert, size_t N, cudaStream_t st);
+
+size_t krylov_scratch_bytes(int max_vec);
+
+}  // namespace helm

@@ -1,0 +1,94 @@
+"""Device GMRES — drop-in for helmdd ``gmres(A, M_inv, b, cfg) -> SolveReport`` (gmres.py:29-177).
+
+The whole loop runs in ``helm_gmres`` (libhelmb200.so): Krylov basis, Hessenberg
+matrix, Givens rotations and residual estimates live in HBM; the host reads one
+estimate per iteration to decide termination, exactly where the reference's
+Python loop tests ``estimate <= rtol`` (gmres.py:151).  Stopping semantics are
+the reference's: right preconditioning confirms on the true residual
+``||b - A x|| / ||b||`` before declaring convergence; left stops on the
+estimate; breakdown ``h_{j+1,j} <= 1e-14 max(max|H[:j+2,j]|, 1)`` terminates.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib
+from .operators import HelmholtzOperator, SchwarzPreconditioner, _as_operator, _ptr, _stream, _Vec
+
+__all__ = ["GmresConfig", "SolveReport", "gmres"]
+
+
+@dataclass(frozen=True)
+class GmresConfig:
+    """helmdd gmres.py:29-41 (defaults rtol 1e-7, max_iter 100, side 'right')."""
+
+    rtol: float = 1e-7
+    max_iter: int = 100
+    side: str = "right"
+
+    def __post_init__(self):
+        if self.rtol <= 0:
+            raise ValueError(f"relative tolerance must be positive, got {self.rtol}")
+        if self.max_iter < 1:
+            raise ValueError(f"iteration cap must be at least 1, got {self.max_iter}")
+        if self.side not in ("left", "right"):
+            raise ValueError(f"preconditioning side must be 'left' or 'right', got {self.side!r}")
+
+
+@dataclass
+class SolveReport:
+    """helmdd gmres.py:44-54."""
+
+    iterations: int
+    converged: bool
+    residual_history: np.ndarray
+    final_residual: float
+    breakdown: bool = False
+    wall_seconds: float = field(default=0.0)
+    x: object = None
+
+
+def gmres(A, M_inv, b, cfg: GmresConfig = GmresConfig()) -> SolveReport:
+    """Solve A x = b with the B200 preconditioner ``M_inv`` (a SchwarzPreconditioner or None)."""
+    if M_inv is not None and not isinstance(M_inv, SchwarzPreconditioner):
+        raise TypeError("device GMRES needs M_inv to be a SchwarzPreconditioner of this package (or None)")
+    if M_inv is not None:
+        plan, use_precond = M_inv.plan, 1
+        op = M_inv.A
+    else:
+        if isinstance(A, HelmholtzOperator):
+            op = A
+        else:
+            raise TypeError("with M_inv=None, A must be a HelmholtzOperator")
+        plan, use_precond = op._stencil_plan(), 0
+    v = _Vec(b, op.N, op.torch_dtype)
+    if v.batch != 1 or v.t.dim() != 1:
+        raise ValueError("gmres solves one right-hand side")
+    x = torch.empty_like(v.t)
+    hist = np.zeros(cfg.max_iter + 1)
+    rep = _lib.HelmGmresReport()
+    with plan.lock:
+        status = plan.lib.helm_gmres(
+            plan.handle, plan.ws, _ptr(v.t), _ptr(x), float(cfg.rtol), int(cfg.max_iter),
+            1 if cfg.side == "left" else 0, use_precond,
+            hist.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), ctypes.byref(rep), _stream(),
+        )
+    if status != 0:
+        msg = plan.lib.helm_last_error().decode(errors="replace")
+        if "nonzero" in msg:
+            raise ValueError(msg)
+        raise _lib.HelmError(msg)
+    return SolveReport(
+        iterations=rep.iterations,
+        converged=bool(rep.converged),
+        residual_history=hist[: rep.iterations + 1].copy(),
+        final_residual=float(rep.final_residual),
+        breakdown=bool(rep.breakdown),
+        wall_seconds=float(rep.wall_seconds),
+        x=v.out(x),
+    )

@@ -1,0 +1,349 @@
+"""Drop-in operators: the B200 replacements of ``A @ x`` and ``SchwarzPreconditioner.apply``.
+
+Mirrors helmdd's public operator surface (``assemble(...).A``,
+``SchwarzPreconditioner(kind, A, decomposition, coarse_space, ...)``,
+``coarse_correct``) so the reference's own ``gmres`` — or this package's device
+GMRES — can drive them.  Every application runs the sm_100a kernels of
+``libhelmb200.so`` through its C ABI; there is no CPU compute path.
+
+Vectors may be numpy arrays (copied host->device->host, so the unmodified
+reference ``gmres`` can call us) or CUDA torch tensors (zero copy).  Both 1-D
+``[N]`` and batched ``[batch, N]`` inputs are accepted.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import threading
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from .discretization import CoarseSpace, Decomposition, Grid, PROBLEMS, build_hocs, extend, partition
+from .fdm_setup import SingularMatrixError, coarse_fdm, local_classes
+
+__all__ = [
+    "HelmholtzOperator",
+    "HelmholtzProblem",
+    "assemble",
+    "galerkin",
+    "coarse_correct",
+    "SchwarzPreconditioner",
+    "SingularMatrixError",
+]
+
+
+def _stream():
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _ptr(t: torch.Tensor):
+    return ctypes.c_void_p(t.data_ptr())
+
+
+class _Vec:
+    """Normalise an input vector to a contiguous CUDA tensor of the plan dtype."""
+
+    def __init__(self, x, N: int, dtype: torch.dtype):
+        self.numpy = isinstance(x, np.ndarray) or not isinstance(x, torch.Tensor)
+        if self.numpy:
+            arr = np.asarray(x)
+            self.np_dtype = np.result_type(arr.dtype, np.complex128 if dtype == torch.complex128 else np.float64)
+            if np.iscomplexobj(arr) and dtype == torch.float64:
+                raise TypeError("complex input to a real (MP-1) operator is not supported on the device path")
+            t = torch.from_numpy(np.ascontiguousarray(arr)).to(dtype)
+            t = t.pin_memory().to("cuda", non_blocking=True) if t.numel() else t.to("cuda")
+        else:
+            if not x.is_cuda:
+                raise ValueError("torch inputs must live on a CUDA device")
+            if x.is_complex() and dtype == torch.float64:
+                raise TypeError("complex input to a real (MP-1) operator is not supported on the device path")
+            t = x.to(dtype).contiguous()
+        if t.shape[-1] != N:
+            raise ValueError(f"operator has dimension {N}, vector {t.shape[-1]}")
+        if t.dim() not in (1, 2):
+            raise ValueError("expected a vector [N] or a batch [batch, N]")
+        self.t = t
+        self.batch = 1 if t.dim() == 1 else t.shape[0]
+
+    def empty_like(self, n=None):
+        shape = self.t.shape if n is None else (*self.t.shape[:-1], n)
+        return torch.empty(shape, dtype=self.t.dtype, device=self.t.device)
+
+    def out(self, y: torch.Tensor):
+        if self.numpy:
+            return y.cpu().numpy()
+        return y
+
+
+def _real_split(fn, x, N):
+    """Apply a real-coefficient operator to a complex numpy vector by linearity (re, im)."""
+    return fn(np.real(x)) + 1j * fn(np.imag(x))
+
+
+class HelmholtzOperator:
+    """Matrix-free 5-point Helmholtz operator A (helmdd discretization.py:157-191).
+
+    ``A @ x`` launches K1.  It is immutable; ``plan`` is shared with the
+    preconditioners built on it.
+    """
+
+    def __init__(self, grid: Grid, k: float, problem: str):
+        self.grid, self.k, self.problem = grid, float(k), problem
+        self.N = grid.num_unknowns
+        self.dtype = np.complex128 if problem == "MP2" else np.float64
+        self.torch_dtype = torch.complex128 if problem == "MP2" else torch.float64
+        self.shape = (self.N, self.N)
+        self._plan = None
+        self._lock = threading.Lock()
+
+    # the stencil only needs the grid part of a plan; it is created lazily so
+    # that setting up an operator does not run the coarse eigen-solves
+    def _stencil_plan(self):
+        with self._lock:
+            if self._plan is None:
+                self._plan = _Plan.create(self.grid, self.k, "SHS2", None, None)
+            return self._plan
+
+    def matvec(self, x):
+        if isinstance(x, np.ndarray) and np.iscomplexobj(x) and self.dtype == np.float64:
+            return _real_split(self.matvec, x, self.N)
+        v = _Vec(x, self.N, self.torch_dtype)
+        y = v.empty_like()
+        plan = self._stencil_plan()
+        _lib.check(plan.lib.helm_apply_A(plan.handle, _ptr(v.t), _ptr(y), v.batch, _stream()))
+        return v.out(y)
+
+    def __matmul__(self, x):
+        if isinstance(x, np.ndarray) and x.ndim == 2 and x.shape[0] == self.N and x.shape[1] != self.N:
+            return self.matvec(x.T).T  # scipy-style (N, k) columns
+        return self.matvec(x)
+
+    __call__ = matvec
+
+    def tocsr(self):
+        """Explicit CSR on the host (interop / tests only; never on the hot path)."""
+        import scipy.sparse as sp
+
+        from .discretization import pencil_1d
+
+        T, w = pencil_1d(self.grid, self.k)
+        T = sp.csr_matrix(T)
+        W = sp.diags(w)
+        A = sp.kron(T, W) + sp.kron(W, T) - self.k**2 * sp.kron(W, W)
+        A = sp.csr_matrix(A)
+        A.sort_indices()
+        return A
+
+
+@dataclass(frozen=True)
+class HelmholtzProblem:
+    grid: Grid
+    k: float
+    problem: str
+    A: HelmholtzOperator
+    f: np.ndarray
+
+
+def assemble(grid: Grid, k: float, problem: str) -> HelmholtzProblem:
+    """Problem setup (helmdd discretization.py:157-191): matrix-free A and the point load."""
+    if problem not in PROBLEMS:
+        raise ValueError(f"unknown problem {problem!r}, expected one of {PROBLEMS}")
+    if k < 0:
+        raise ValueError(f"wavenumber must be nonnegative, got {k}")
+    expected = "dirichlet" if problem == "MP1" else "sommerfeld"
+    if grid.bc != expected:
+        raise ValueError(f"{problem} requires a {expected} grid, got {grid.bc!r}")
+    if grid.n % 2 == 0:
+        raise ValueError("the GPU path needs odd n (H = 2h coarse grid, centre node source)")
+    A = HelmholtzOperator(grid, k, problem)
+    f = np.zeros(grid.num_unknowns, dtype=A.dtype)
+    c = (grid.n - 1) // 2
+    f[grid.unknown_index(c, c)] = 1.0 / grid.h**2
+    return HelmholtzProblem(grid, float(k), problem, A, f)
+
+
+def galerkin(cs: CoarseSpace, A) -> CoarseSpace:
+    """Attach the partial-FDM coarse solver (replaces SuperLU of A0, helmdd coarse.py:154-167)."""
+    op = _as_operator(A, cs.grid)
+    from dataclasses import replace
+
+    return replace(cs, fdm=coarse_fdm(cs.grid, op.k))
+
+
+class _Plan:
+    """Owns a helm_plan + helm_workspace pair (C ABI handles)."""
+
+    def __init__(self, lib, handle, ws, N, N0, keep):
+        self.lib, self.handle, self.ws, self.N, self.N0 = lib, handle, ws, N, N0
+        self._keep = keep
+        self.lock = threading.Lock()
+
+    @staticmethod
+    def create(grid: Grid, k: float, kind: str, dec: Decomposition, cf, weights_before_solve=False,
+               max_batch: int = 1, refine_steps: int = 1):
+        lib = _lib.load()
+        cplx = grid.bc == "sommerfeld"
+        dt = np.complex128 if cplx else np.float64
+        i32 = lambda a: a.ctypes.data_as(_lib.c_int32_p)  # noqa: E731
+        vp = lambda a: ctypes.c_void_p(a.ctypes.data)  # noqa: E731
+        d = _lib.HelmDesc()
+        d.n, d.bc, d.is_complex = grid.n, (_lib.HELM_SOMMERFELD if cplx else _lib.HELM_DIRICHLET), int(cplx)
+        d.kind, d.weights_before_solve = _lib.KINDS[kind], int(bool(weights_before_solve))
+        d.ratio, d.k = 2, float(k)
+        d.m0 = (grid.n - 3) // 2 if grid.bc == "dirichlet" else (grid.n + 1) // 2
+        keep = {}
+        if dec is not None:  # subdomain FDM classes
+            lc = local_classes(grid, k, dec.boxes)
+            keep["classV"] = np.ascontiguousarray(np.concatenate([v.astype(dt).ravel() for v in lc.V]))
+            keep["classL"] = np.ascontiguousarray(np.concatenate([l.astype(dt).ravel() for l in lc.lam]))
+            for name in ("box_start", "box_len", "box_class", "class_len"):
+                keep[name] = np.ascontiguousarray(getattr(lc, name), dtype=np.int32)
+            d.p, d.overlap_layers = dec.p, dec.overlap_layers
+            d.box_start, d.box_len = i32(keep["box_start"]), i32(keep["box_len"])
+            d.box_class, d.class_len = i32(keep["box_class"]), i32(keep["class_len"])
+            d.n_classes = len(lc.V)
+            d.class_V, d.class_lambda = vp(keep["classV"]), vp(keep["classL"])
+        if cf is not None:  # partial-FDM coarse solver
+            arrays = dict(V=cf.V, lam=cf.lam, t0b=cf.t0b, m0b=cf.m0b, piv=cf.piv, L=cf.L, U=cf.U)
+            for key, v in arrays.items():
+                keep[key] = np.ascontiguousarray(v, dtype=(np.uint8 if key == "piv" else dt))
+            d.coarse_V, d.coarse_lambda = vp(keep["V"]), vp(keep["lam"])
+            d.t0_band, d.m0_band = vp(keep["t0b"]), vp(keep["m0b"])
+            d.band_piv = keep["piv"].ctypes.data_as(ctypes.POINTER(ctypes.c_uint8))
+            d.band_l, d.band_u = vp(keep["L"]), vp(keep["U"])
+        d.refine_steps = int(refine_steps)
+        h = ctypes.c_void_p()
+        _lib.check(lib.helm_plan_create(ctypes.byref(d), ctypes.byref(h)))
+        ws = ctypes.c_void_p()
+        try:
+            _lib.check(lib.helm_workspace_create(h, int(max_batch), ctypes.byref(ws)))
+        except Exception:
+            lib.helm_plan_destroy(h)
+            raise
+        return _Plan(lib, h, ws, lib.helm_plan_num_unknowns(h), lib.helm_plan_num_coarse(h), None)
+
+    def __del__(self):
+        try:
+            if self.ws:
+                self.lib.helm_workspace_destroy(self.ws)
+            if self.handle:
+                self.lib.helm_plan_destroy(self.handle)
+        except Exception:
+            pass
+
+
+def _as_operator(A, grid: Grid) -> HelmholtzOperator:
+    """Accept our operator, or a reference CSR matrix after a structure guard."""
+    if isinstance(A, HelmholtzOperator):
+        return A
+    import scipy.sparse as sp
+
+    if sp.issparse(A):
+        problem = "MP1" if grid.bc == "dirichlet" else "MP2"
+        if A.shape != (grid.num_unknowns, grid.num_unknowns):
+            raise ValueError("matrix size does not match the decomposition's grid")
+        # recover k from an interior diagonal entry: 4/h^2 - k^2
+        c = (grid.unknowns_per_dim // 2) * (grid.unknowns_per_dim + 1)
+        k2 = 4.0 / grid.h**2 - float(np.real(A[c, c]))
+        op = HelmholtzOperator(grid, float(np.sqrt(max(k2, 0.0))), problem)
+        ref = op.tocsr()
+        if abs(ref - A).max() > 1e-12 * abs(A).max():
+            raise ValueError("A is not the constant-k 5-point Helmholtz operator of this grid")
+        return op
+    raise TypeError("A must be a HelmholtzOperator or the reference's assembled CSR matrix")
+
+
+def _grid_of(obj) -> Grid:
+    g = obj.grid
+    return g if isinstance(g, Grid) else Grid(g.n, g.bc)
+
+
+class SchwarzPreconditioner:
+    """Two-level Schwarz M^{-1} (AS2 / SAS2 / SHS2) on the B200 — helmdd schwarz.py:31-103.
+
+    Immutable after construction; ``apply`` serialises on an internal lock
+    because the device workspace is shared (the reference's concurrent-read
+    contract holds for callers).  ``decomposition`` / ``coarse_space`` may be
+    this package's descriptors or the reference's objects (duck-typed).
+    """
+
+    KINDS = ("AS2", "SAS2", "SHS2")
+
+    def __init__(self, kind, A, decomposition, coarse_space, weights_before_solve=False,
+                 local_factorizations=None, max_batch: int = 1, refine_steps: int = 1):
+        if kind not in self.KINDS:
+            raise ValueError(f"unknown preconditioner {kind!r}, expected one of {self.KINDS}")
+        grid = _grid_of(decomposition)
+        if A.shape[0] != grid.num_unknowns:
+            raise ValueError("matrix size does not match the decomposition's grid")
+        self.kind = kind
+        self.A = _as_operator(A, grid)
+        self.decomposition = Decomposition(grid, decomposition.p, decomposition.overlap_layers)
+        if getattr(coarse_space, "kind", "HOCS") != "HOCS" or getattr(coarse_space, "ratio", 2) != 2:
+            raise NotImplementedError("the GPU path implements the HOCS coarse space at ratio 2")
+        cf = getattr(coarse_space, "fdm", None)
+        if cf is None:
+            cf = coarse_fdm(grid, self.A.k)
+        self.coarse_space = CoarseSpace("HOCS", grid, 2, cf)
+        self.weights_before_solve = bool(weights_before_solve)
+        self.max_batch = int(max_batch)
+        self.plan = _Plan.create(grid, self.A.k, kind, self.decomposition, cf, weights_before_solve,
+                                 max_batch=max_batch, refine_steps=refine_steps)
+        self.N = self.plan.N
+        self.N0 = self.plan.N0
+
+    # -- the individual operators (for parity tests and benchmarks) ---------
+    def _run(self, fn, x, out_len=None, in_len=None, *extra):
+        v = _Vec(x, in_len or self.N, self.A.torch_dtype)
+        if v.batch > self.max_batch:
+            raise ValueError(f"batch {v.batch} exceeds max_batch {self.max_batch}")
+        y = v.empty_like(out_len or self.N)
+        with self.plan.lock:
+            _lib.check(fn(v.t, y, v.batch, *extra))
+        return v.out(y)
+
+    def apply(self, x):
+        if isinstance(x, np.ndarray) and np.iscomplexobj(x) and self.A.dtype == np.float64:
+            return _real_split(self.apply, x, self.N)
+        p = self.plan
+        return self._run(lambda a, b, n: p.lib.helm_apply_M(p.handle, p.ws, _ptr(a), _ptr(b), n, _stream()), x)
+
+    __call__ = apply
+
+    def restrict(self, x):
+        p = self.plan
+        return self._run(lambda a, b, n: p.lib.helm_restrict(p.handle, _ptr(a), _ptr(b), n, _stream()), x,
+                         self.N0)
+
+    def prolong(self, c):
+        p = self.plan
+        return self._run(lambda a, b, n: p.lib.helm_prolong(p.handle, _ptr(a), _ptr(b), n, _stream()), c,
+                         self.N, self.N0)
+
+    def coarse_solve(self, c):
+        p = self.plan
+        return self._run(lambda a, b, n: p.lib.helm_coarse_solve(p.handle, p.ws, _ptr(a), _ptr(b), n, _stream()),
+                         c, self.N0, self.N0)
+
+    def coarse_correct(self, x):
+        p = self.plan
+        return self._run(lambda a, b, n: p.lib.helm_coarse_correct(p.handle, p.ws, _ptr(a), _ptr(b), n, _stream()),
+                         x)
+
+    def local_sum(self, x, weighted=True, base=None):
+        """y = base + sum_i R_i^T [D_i] A_i^{-1} [D_i] R_i x  (helmdd schwarz.py:64-74)."""
+        p = self.plan
+        bt = None
+        if base is not None:
+            bt = _Vec(base, self.N, self.A.torch_dtype).t
+        return self._run(
+            lambda a, b, n: p.lib.helm_local_sum(p.handle, p.ws, _ptr(a), _ptr(bt) if bt is not None else None,
+                                                 _ptr(b), int(weighted), n, _stream()), x)
+
+
+def coarse_correct(M: SchwarzPreconditioner, r):
+    """R0^T A0^{-1} R0 r (helmdd coarse.py:170-174) on the preconditioner's plan."""
+    return M.coarse_correct(r)

@@ -1,0 +1,121 @@
+"""Generate golden fixtures by running the UNMODIFIED reference ``helmdd`` (build container only).
+
+Usage (from the repo root, with the read-only reference mounted):
+    PYTHONPATH=/root/reference/pkg/src python tests/golden/make_golden.py small
+    PYTHONPATH=/root/reference/pkg/src python tests/golden/make_golden.py cfg3 cfg4a cfg4b
+
+Inputs are never stored: every test regenerates them from the seeds below
+(numpy PCG64, as SURVEY §8(d) prescribes).  Outputs are written to
+``tests/golden/<case>.npz``.  The reference is driven through its library API
+exactly as SURVEY §3 (S1) describes: Grid → assemble → extend(partition(grid, p), m)
+→ galerkin(build_hocs(grid, ratio)) → SchwarzPreconditioner → gmres.
+"""
+
+from __future__ import annotations
+
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+# name: (n, k, problem, p, m, ratio, gmres_rhs, store_vectors)
+# m = overlap layers passed to extend(); "max" = extend_max (decomposition.py:137-139)
+CASES = {
+    # tiny instances (dense-oracle sized, test_schwarz.py:45-51 style) at HOCS ratio 2
+    "tiny_mp1_n9_p4": (9, 2.0, "MP1", 4, "max", 2, "point", True),
+    "tiny_mp1_n17_p2": (17, 3.0, "MP1", 2, 2, 2, "point", True),
+    "tiny_mp2_n17_p2": (17, 3.0, "MP2", 2, 2, 2, "point", True),
+    "tiny_mp2_n17_p4": (17, 5.0, "MP2", 4, 2, 2, "point", True),
+    "small_mp2_n33_p4": (33, 7.0, "MP2", 4, 2, 2, "point", True),
+    "small_mp1_n33_p4_m3": (33, 9.0, "MP1", 4, 3, 2, "point", True),
+    "small_mp2_n65_p8": (65, 10.0, "MP2", 8, 2, 2, "random", True),
+    # BASELINE.json configs 1 and 2 (full operator set)
+    "cfg1": (65, 20.0, "MP1", 4, 2, 2, "point", True),
+    "cfg2": (257, 50.0, "MP2", 8, 2, 2, "point", "lite"),
+    # BASELINE.json configs 3 and 4: iteration counts, histories, subsampled solutions
+    "cfg3": (513, 100.0, "MP1", 16, 2, 2, "point", False),
+    "cfg4a": (1025, 200.0, "MP2", 32, 2, 2, "point", False),
+    "cfg4b": (1025, 200.0, "MP2", 32, 2, 2, "random", False),
+}
+
+GMRES_RTOL = 1e-6
+GMRES_CAP = 1000
+SUBSAMPLE = 61  # stride of the stored solution sample for the large configs
+
+
+def operator_input(N: int, complex_: bool) -> np.ndarray:
+    """Seed-1 operator input: real block drawn before the imaginary block."""
+    r = np.random.default_rng(1)
+    x = r.standard_normal(N)
+    return x + 1j * r.standard_normal(N) if complex_ else x
+
+
+def random_rhs(N: int) -> np.ndarray:
+    """Config 4(b) right-hand side: default_rng(0), re then im."""
+    r = np.random.default_rng(0)
+    return r.standard_normal(N) + 1j * r.standard_normal(N)
+
+
+def run_case(name: str):
+    import helmdd as H
+
+    n, k, problem, p, m, ratio, rhs_kind, store = CASES[name]
+    t0 = time.time()
+    grid = H.Grid(n, "dirichlet" if problem == "MP1" else "sommerfeld")
+    prob = H.assemble(grid, k, problem)
+    part = H.partition(grid, p)
+    dec = H.extend_max(part) if m == "max" else H.extend(part, m)
+    cs = H.galerkin(H.build_hocs(grid, ratio), prob.A)
+    M = H.SchwarzPreconditioner("SHS2", prob.A, dec, cs)
+    setup_s = time.time() - t0
+    N = prob.A.shape[0]
+    out = dict(n=n, k=k, problem=problem, p=p, m=(-1 if m == "max" else m), ratio=ratio,
+               overlap_layers=dec.overlap_layers, setup_s=setup_s)
+    if store:
+        x = operator_input(N, problem == "MP2")
+        c = cs.r0 @ x
+        out["R0x"] = c
+        out["coarse_solve"] = H.solve(cs.a0_factorization, c)
+        out["M_shs2"] = M(x)
+        if store == "lite":  # keep the large-config fixture small: skip the per-kernel vectors
+            kinds = ()
+        else:
+            kinds = ("AS2", "SAS2")
+            out["Ax"] = prob.A @ x
+            out["R0T_c"] = cs.r0.T @ c
+            out["coarse_correct"] = H.coarse_correct(cs, x)
+            y = np.zeros(N, dtype=np.result_type(x.dtype, prob.A.dtype))
+            M._local_sum(x.astype(y.dtype), y, weighted=True)
+            out["local_sum"] = y
+        for kind in kinds:
+            Mk = H.SchwarzPreconditioner(kind, prob.A, dec, cs, local_factorizations=M.local_factorizations)
+            out["M_" + kind.lower()] = Mk(x)
+    b = prob.f if rhs_kind == "point" else random_rhs(N)
+    rep = H.gmres(prob.A, M, b, H.GmresConfig(rtol=GMRES_RTOL, max_iter=GMRES_CAP, side="right"))
+    out["gmres_rhs"] = rhs_kind
+    out["gmres_iterations"] = rep.iterations
+    out["gmres_converged"] = rep.converged
+    out["gmres_history"] = rep.residual_history
+    out["gmres_final_residual"] = rep.final_residual
+    out["gmres_wall_s"] = rep.wall_seconds
+    out["gmres_x_norm"] = np.linalg.norm(rep.x)
+    if store:
+        out["gmres_x"] = rep.x
+    else:
+        out["gmres_x_sample"] = rep.x[::SUBSAMPLE]
+        out["gmres_x_sample_stride"] = SUBSAMPLE
+    np.savez_compressed(os.path.join(HERE, name + ".npz"), **out)
+    print(json.dumps(dict(case=name, N=N, setup_s=round(setup_s, 2), iterations=rep.iterations,
+                          converged=bool(rep.converged), wall=round(rep.wall_seconds, 2))), flush=True)
+
+
+if __name__ == "__main__":
+    names = sys.argv[1:] or ["small"]
+    if names == ["small"]:
+        names = [c for c in CASES if CASES[c][-1]]
+    for nm in names:
+        run_case(nm)
