@@ -1,0 +1,423 @@
+"""Benchmark of the B200 hot path at BASELINE.json config 5 (MP-2, n=2049, k=300, 64x64 subdomains,
+overlap 2h, HOCS H=2h, SHS2; a batch of 32 seed-1 random complex vectors).
+
+One step = one two-level M^{-1} apply (SHS2) on the 32-vector batch, inputs resident in HBM.
+Prints ONE JSON line (rank 0).  `--impl reference` times the CPU oracle port of the reference
+(oracle/helmdd_oracle.py — the reference is pure Python/scipy and cannot travel to the GPU box)
+on the host cores instead.
+
+Usage:  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "preconditioned GMRES iter/s and M^-1 applies/s at n=2049; HBM GB/s vs peak"
+UNIT = "M^-1 applies/s"
+CFG = dict(problem="MP2", n=2049, k=300.0, p=64, overlap_layers=2, ratio=2, kind="SHS2", batch=32)
+FP64_PEAK_TFLOPS = 37.1  # measured DMMA/DFMA peak on this pool's B200 (profiles/fp64_peak_r01.txt)
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def rng_batch(N, B, seed=1):
+    """default_rng(1), standard_normal((32,N)) + 1j*standard_normal((32,N))."""
+    r = np.random.default_rng(seed)
+    re = r.standard_normal((B, N))
+    im = r.standard_normal((B, N))
+    return re + 1j * im
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region (B200_PROFILING.md)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.idx = str(gpu_index)
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                          "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 7 and parts[0] == self.idx:
+                self.rows.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[3 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# --------------------------------------------------------------------------------------------
+# algorithmic work per vector
+# --------------------------------------------------------------------------------------------
+def work_model(N, N0, m0, s, boxes_1d):
+    """Bytes / flops per vector for each phase.  boxes_1d: list of 1-D box lengths."""
+    f = 8 if s == 16 else 2  # real flops per complex/real MAC
+    sa, sa2 = sum(boxes_1d), sum(L * L for L in boxes_1d)
+    # local FDM: 4 one-sided products per subdomain, L^3 MACs each (complex V)
+    F_loc = 4 * sa2 * sa * f
+    # coarse: partial FDM = 2 m0^3 MAC GEMMs per solve, x (1 + refine) solves
+    F_c = 2 * 2 * m0**3 * f
+    return {
+        "A x": {"bytes": 2 * N * s, "flops": 0},
+        "R0 x": {"bytes": (N + N0) * s, "flops": 0},
+        "R0^T c": {"bytes": (N + N0) * s, "flops": 0},
+        "local sum": {"bytes": 2 * N * s, "flops": F_loc},
+        "coarse solve": {"bytes": 4 * N0 * s + 14 * m0 * m0 * s, "flops": F_c},
+    }
+
+
+def composite_roof(model, bw_gbs, p64_tf):
+    """T_roof = sum_phase max(B/BW, F/P64) for the minimal fused SHS2 apply."""
+    N_s = model["A x"]["bytes"] / 2
+    N0_s = model["R0 x"]["bytes"] - N_s
+    t = 0.0
+    t += (N_s + N0_s) / (bw_gbs * 1e9)  # R0 phase
+    c = model["coarse solve"]
+    t += max(c["bytes"] / (bw_gbs * 1e9), c["flops"] / (p64_tf * 1e12))
+    loc = model["local sum"]
+    t += max((2 * N_s + N0_s) / (bw_gbs * 1e9), loc["flops"] / (p64_tf * 1e12))
+    return t
+
+
+# --------------------------------------------------------------------------------------------
+def run_ours(a, rank, world, local_rank):
+    import torch
+
+    import paper_2408_03571_b200 as hb
+    from paper_2408_03571_b200 import _lib
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    B = a.batch
+    t0 = time.time()
+    grid = hb.Grid(a.n, "sommerfeld")
+    prob = hb.assemble(grid, a.k, "MP2")
+    dec = hb.extend(hb.partition(grid, a.p), CFG["overlap_layers"])
+    cs = hb.galerkin(hb.build_hocs(grid, 2), prob.A)
+    M = hb.SchwarzPreconditioner("SHS2", prob.A, dec, cs, max_batch=B)
+    setup_s = time.time() - t0
+    N, N0 = M.N, M.N0
+    m0 = cs.coarse_unknowns_per_dim
+    lib = _lib.load()
+    Xh = torch.from_numpy(rng_batch(N, B)).pin_memory()
+    X = Xh.to(dev)
+    Y = torch.empty_like(X)
+    st = torch.cuda.current_stream()
+
+    def step():
+        M.apply(X, out=Y)
+
+    for _ in range(a.warmup):
+        step()
+    torch.cuda.synchronize()
+    bw, peak_kind = peaks()
+    dist = world > 1
+    if dist:
+        import torch.distributed as tdist
+
+        tdist.barrier()
+    torch.cuda.synchronize()
+    l0 = lib.helm_kernel_launches()
+    with ClockSampler(local_rank) as clk:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        for _ in range(a.steps):
+            step()
+        e1.record(st)
+        torch.cuda.synchronize()
+    launches = lib.helm_kernel_launches() - l0
+    ms = e0.elapsed_time(e1) / a.steps
+    if dist:
+        t = torch.tensor([ms], device=dev)
+        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+        ms = float(t.item())
+        tdist.barrier()
+    value = world * B / (ms / 1e3)
+
+    # ---- per-phase timings on the same batch (CUDA events on the launching stream) ----
+    p = M.plan
+    C = torch.empty(B, N0, dtype=X.dtype, device=dev)
+    C2 = torch.empty_like(C)
+    M.restrict(X[:1])  # warm
+    phases = {
+        "A x": lambda: lib.helm_apply_A(p.handle, X.data_ptr(), Y.data_ptr(), B, st.cuda_stream),
+        "R0 x": lambda: lib.helm_restrict(p.handle, X.data_ptr(), C.data_ptr(), B, st.cuda_stream),
+        "R0^T c": lambda: lib.helm_prolong(p.handle, C.data_ptr(), Y.data_ptr(), B, st.cuda_stream),
+        "coarse solve": lambda: lib.helm_coarse_solve(p.handle, p.ws, C.data_ptr(), C2.data_ptr(), B,
+                                                      st.cuda_stream),
+        "local sum": lambda: lib.helm_local_sum(p.handle, p.ws, X.data_ptr(), None, Y.data_ptr(), 1, B,
+                                                st.cuda_stream),
+    }
+    s = 16
+    model = work_model(N, N0, m0, s, [L for _, L in dec.boxes])
+    comp = {}
+    for name, fn in phases.items():
+        for _ in range(2):
+            fn()
+        torch.cuda.synchronize()
+        e0.record(st)
+        reps = 3
+        for _ in range(reps):
+            fn()
+        e1.record(st)
+        torch.cuda.synchronize()
+        pms = e0.elapsed_time(e1) / reps
+        mdl = model[name]
+        comp[name] = {
+            "ms_per_batch": round(pms, 4),
+            "GB/s": round(mdl["bytes"] * B / (pms / 1e3) / 1e9, 1),
+            "hbm_frac": round(mdl["bytes"] * B / (pms / 1e3) / 1e9 / bw, 3),
+            "TFLOP/s": round(mdl["flops"] * B / (pms / 1e3) / 1e12, 2),
+        }
+    # dominant own-kernel phase for the roofline object
+    own = {k: v for k, v in comp.items() if k != "coarse solve"}
+    dom = max(own, key=lambda k: own[k]["ms_per_batch"])
+    mdl = model[dom]
+    if mdl["flops"] > 0 and mdl["flops"] / mdl["bytes"] > (FP64_PEAK_TFLOPS * 1e12) / (bw * 1e9):
+        ach = mdl["flops"] * B / (comp[dom]["ms_per_batch"] / 1e3) / 1e12
+        roof = {"bound": "tensor", "achieved": round(ach, 3), "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                "frac": round(ach / FP64_PEAK_TFLOPS, 4), "traffic": None, "kernel": dom,
+                "peak_source": "measured FP64 MMA (tools/fp64_peak.cu)"}
+    else:
+        ach = mdl["bytes"] * B / (comp[dom]["ms_per_batch"] / 1e3) / 1e9
+        roof = {"bound": "hbm", "achieved": round(ach, 1), "peak": bw, "unit": "GB/s", "frac": round(ach / bw, 4),
+                "traffic": None, "kernel": dom, "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})"}
+    t_roof = composite_roof(model, bw, FP64_PEAK_TFLOPS)
+    composite = {"T_roof_ms_per_vector": round(t_roof * 1e3, 4), "measured_ms_per_vector": round(ms / B, 4),
+                 "frac": round(t_roof / (ms / B / 1e3), 4)}
+
+    # ---- e2e through the public API with host buffers (pinned), H2D + D2H inside the timed region ----
+    Yh = torch.empty_like(Xh).pin_memory()
+    M.apply(Xh, out=Yh)
+    torch.cuda.synchronize()
+    te = time.perf_counter()
+    e2e_steps = max(1, min(a.steps, 3))
+    for _ in range(e2e_steps):
+        M.apply(Xh, out=Yh)
+    torch.cuda.synchronize()
+    e2e_s = (time.perf_counter() - te) / e2e_steps
+    e2e = {"value": round(world * B / e2e_s, 3), "unit": UNIT, "h2d_bytes_per_step": int(Xh.numel() * 16),
+           "d2h_bytes_per_step": int(Yh.numel() * 16)}
+
+    # ---- GMRES on the config-5 operator, centre point source ----
+    gm = {}
+    if a.gmres:
+        rep = hb.gmres(prob.A, M, prob.f, hb.GmresConfig(rtol=1e-6, max_iter=1000))
+        gm = {"iterations": rep.iterations, "converged": rep.converged, "seconds": round(rep.wall_seconds, 4),
+              "iter_per_s": round(rep.iterations / rep.wall_seconds, 2), "final_residual": rep.final_residual}
+        rep = hb.gmres(prob.A, M, prob.f, hb.GmresConfig(rtol=1e-30, max_iter=a.gmres))
+        gm["fixed_iterations"] = rep.iterations
+        gm["fixed_iter_per_s"] = round(rep.iterations / rep.wall_seconds, 2)
+
+    return dict(value=value, ms=ms, setup_s=setup_s, clocks=clk.summary(), launches=launches, comp=comp,
+                roof=roof, composite=composite, e2e=e2e, gmres=gm)
+
+
+def cpu_sample(a, budget_s=30.0):
+    import scipy.sparse.linalg  # noqa: F401  (load scipy's BLAS before limiting it)
+    from threadpoolctl import threadpool_limits
+
+    # the reference hot path is single-threaded; BLAS threads inside SuperLU only oversubscribe
+    with threadpool_limits(1):
+        return _cpu_sample(a)
+
+
+def _cpu_sample(a):
+    """Time the CPU oracle port on a bounded sample of the config-5 workload (host cores).
+
+    The reference hot path is single-threaded (SuperLU + scipy CSR + Python loops), so
+    one core is used.  Sample: A x, R0 x, R0^T c on one vector; the one-level term on
+    a subset of the 4,096 subdomains (factorise + solve, scaled); the coarse SuperLU
+    solve on the config-5 Galerkin matrix when its factorisation fits the budget,
+    else on the largest coarse problem that does, scaled by the measured fill growth.
+    """
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import scipy.sparse as sp
+    from scipy.sparse.linalg import splu
+
+    import helmdd_oracle as O
+
+    t_start = time.time()
+    grid = O.OGrid(a.n, "sommerfeld")
+    prob = O.assemble(grid, a.k, "MP2")
+    dec = O.decompose(grid, a.p, CFG["overlap_layers"])
+    N = prob.A.shape[0]
+    x = rng_batch(N, 1)[0]
+    P = O.bezier_1d(grid, 2)
+    R0 = sp.kron(P, P, format="csr")
+
+    def best(fn, reps=3):
+        ts = []
+        for _ in range(reps):
+            t = time.perf_counter()
+            fn()
+            ts.append(time.perf_counter() - t)
+        return min(ts)
+
+    t_ax = best(lambda: prob.A @ x)
+    c = R0 @ x
+    t_r0 = best(lambda: R0 @ x)
+    t_r0t = best(lambda: R0.T @ c)
+    # one-level: factor + solve a sample of subdomains (interior ones dominate: 94 %)
+    nsub = len(dec.index_sets)
+    sample = list(range(0, nsub, max(1, nsub // 64)))
+    t_solve = 0.0
+    out = np.zeros(N, dtype=complex)
+    for i in sample:
+        s_, w = dec.index_sets[i], dec.weights[i]
+        lu = splu(sp.csc_matrix(prob.A[s_][:, s_]))
+        t = time.perf_counter()
+        out[s_] += w * lu.solve(x[s_])  # the loop body of schwarz.py:67-72
+        t_solve += time.perf_counter() - t
+    t_loc = t_solve * nsub / len(sample)
+    # coarse: SuperLU of the config-5 Galerkin matrix (N0 = 1.05M) takes far longer than the
+    # bench budget to factorise, so the solve is measured on the same-kh coarse problems at
+    # n = 257 and 513 and extrapolated with the measured growth exponent of the solve time.
+    pts = []
+    for trial_n in (257, 513):
+        g2 = O.OGrid(trial_n, "sommerfeld")
+        p2 = O.assemble(g2, a.k * (trial_n - 1) / (a.n - 1), "MP2")
+        ocs = O.coarse_space(g2, p2.A, 2)
+        c2 = ocs.r0 @ rng_batch(p2.A.shape[0], 1)[0]
+        pts.append((ocs.a0.shape[0], best(lambda: ocs.lu.solve(c2), reps=2), ocs.lu.L.nnz + ocs.lu.U.nnz))
+    (n1, t1, f1), (n2, t2, f2) = pts
+    alpha = np.log(t2 / t1) / np.log(n2 / n1)
+    N0 = ((a.n + 1) // 2) ** 2
+    t_coarse = t2 * (N0 / n2) ** alpha
+    note = (f"coarse SuperLU solve measured at N0={n1:,} ({t1 * 1e3:.1f} ms, fill {f1:,}) and N0={n2:,} "
+            f"({t2 * 1e3:.1f} ms, fill {f2:,}) and extrapolated to N0={N0:,} with exponent {alpha:.2f}")
+    cs_n = 513
+    t_m = t_r0 + t_coarse + t_r0t + t_ax + t_loc
+    return {
+        "ms_per_vector": {"A x": t_ax * 1e3, "R0 x": t_r0 * 1e3, "R0^T c": t_r0t * 1e3,
+                          "coarse solve": float(t_coarse) * 1e3, "local sum": t_loc * 1e3, "M^-1": float(t_m) * 1e3},
+        "value": float(1.0 / t_m),
+        "sample": (f"oracle port (scipy SuperLU/CSR, as the reference) on config 5: A x, R0, R0^T best of 3 on one "
+                   f"vector; one-level from {len(sample)}/{nsub} subdomain solves scaled; {note}"),
+        "coarse_n": cs_n,
+        "seconds": time.time() - t_start,
+    }
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--batch", type=int, default=CFG["batch"])
+    ap.add_argument("--n", type=int, default=CFG["n"])
+    ap.add_argument("--k", type=float, default=CFG["k"])
+    ap.add_argument("--p", type=int, default=CFG["p"])
+    ap.add_argument("--gmres", type=int, default=50, help="fixed-length GMRES run for iter/s (0: skip)")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    a = ap.parse_args()
+    a.warmup = max(a.warmup, 3)
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    config = {"workload": f"config 5: MP-2 complex128 n={a.n} k={a.k:g}, {a.p}x{a.p} subdomains overlap 2h, "
+                          f"HOCS H=2h, SHS2 M^-1 on a batch of {a.batch} seed-1 random vectors",
+              "n": a.n, "k": a.k, "p": a.p, "batch": a.batch,
+              "l2": "inputs larger than L2 (batch = %.2f GB of complex128)" % (a.batch * (a.n**2) * 16 / 1e9),
+              "parallelism": "replicas" if world > 1 else "single-gpu"}
+
+    if a.impl == "reference":
+        if rank != 0:
+            return
+        steps = []
+        cs = None
+        for _ in range(max(1, min(a.steps, 1))):
+            cs = cpu_sample(a)
+            steps.append(cs["value"])
+        v = float(np.median(steps))
+        line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": len(steps), "warmup": 0,
+                "ms_per_step": 1e3 * a.batch / v, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+                "dtype": "c128", "data": "synthetic", "config": config, "impl": "reference",
+                "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "port", "sample": cs["sample"],
+                                 "ms_per_vector": cs["ms_per_vector"], "host_cores": os.cpu_count()},
+                "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return
+
+    if world > 1:
+        import torch
+        import torch.distributed as tdist
+
+        torch.cuda.set_device(local_rank)
+        tdist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    r = run_ours(a, rank, world, local_rank)
+    cpu = None
+    if rank == 0 and world == 1 and not a.no_cpu:
+        c = cpu_sample(a)
+        cpu = {"value": c["value"], "unit": UNIT, "cores": 1, "kind": "port", "sample": c["sample"],
+               "ms_per_vector": {k: round(v, 3) for k, v in c["ms_per_vector"].items()},
+               "host_cores": os.cpu_count()}
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(r["value"], 3), "unit": UNIT, "n_gpus": world, "steps": a.steps,
+            "warmup": a.warmup, "ms_per_step": round(r["ms"], 4), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "c128", "data": "synthetic", "config": config,
+            "roofline": r["roof"], "roofline_composite": r["composite"], "phases": r["comp"],
+            "cpu_baseline": cpu, "e2e": r["e2e"], "gpu_launches": int(r["launches"]), "clocks": r["clocks"],
+            "gmres": r["gmres"], "setup_s": round(r["setup_s"], 2),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as tdist
+
+        tdist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -98,6 +98,8 @@ typedef struct helm_gmres_report {
 } helm_gmres_report;
 
 int32_t helm_abi_version(void);
+/* number of libhelmb200 kernels launched by this process so far (cuBLAS not counted) */
+uint64_t helm_kernel_launches(void);
 const char* helm_last_error(void);
 
 int helm_plan_create(const helm_desc* desc, helm_plan** out);

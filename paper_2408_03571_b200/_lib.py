@@ -66,6 +66,7 @@ class HelmGmresReport(ctypes.Structure):
 _vp, _i32, _dbl = ctypes.c_void_p, ctypes.c_int32, ctypes.c_double
 SYMBOLS = [
     ("helm_abi_version", ctypes.c_int32, []),
+    ("helm_kernel_launches", ctypes.c_uint64, []),
     ("helm_last_error", ctypes.c_char_p, []),
     ("helm_plan_create", ctypes.c_int, [ctypes.POINTER(HelmDesc), ctypes.POINTER(_vp)]),
     ("helm_plan_destroy", ctypes.c_int, [_vp]),

@@ -2,6 +2,7 @@
 // workspace lifetime, the operator entry points, and the native GMRES driver
 // (gmres.py:65-177) that strings the kernels together with one scalar
 // read-back per iteration.
+#include <atomic>
 #include <chrono>
 #include <cmath>
 #include <cstring>
@@ -12,6 +13,8 @@ namespace helm {
 
 static thread_local std::string g_last_error;
 void set_last_error(const std::string& msg) { g_last_error = msg; }
+static std::atomic<uint64_t> g_launches{0};
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 template <typename F>
 static int guarded(F&& f) {
@@ -329,6 +332,7 @@ using namespace helm;
 extern "C" {
 
 int32_t helm_abi_version(void) { return HELM_ABI_VERSION; }
+uint64_t helm_kernel_launches(void) { return g_launches.load(); }
 const char* helm_last_error(void) { return g_last_error.c_str(); }
 
 int helm_plan_create(const helm_desc* desc, helm_plan** out) {

@@ -103,7 +103,12 @@ void set_last_error(const std::string& msg);
   do {                                                                                    \
     if (!(cond)) throw ::helm::Error(msg);                                                \
   } while (0)
-#define HELM_LAUNCH_CHECK() HELM_CUDA(cudaGetLastError())
+void count_launch();
+#define HELM_LAUNCH_CHECK()        \
+  do {                             \
+    ::helm::count_launch();        \
+    HELM_CUDA(cudaGetLastError()); \
+  } while (0)
 
 // ----------------------------------------------------------------------------
 // grid geometry shared by the stencil, transfer and local kernels

@@ -48,7 +48,12 @@ class _Vec:
 
     def __init__(self, x, N: int, dtype: torch.dtype):
         self.numpy = isinstance(x, np.ndarray) or not isinstance(x, torch.Tensor)
-        if self.numpy:
+        self.host_torch = isinstance(x, torch.Tensor) and not x.is_cuda
+        if self.host_torch:  # host tensor (ideally pinned): async H2D, result copied back to the host
+            if x.is_complex() and dtype == torch.float64:
+                raise TypeError("complex input to a real (MP-1) operator is not supported on the device path")
+            t = x.to(dtype).contiguous().to("cuda", non_blocking=True)
+        elif self.numpy:
             arr = np.asarray(x)
             self.np_dtype = np.result_type(arr.dtype, np.complex128 if dtype == torch.complex128 else np.float64)
             if np.iscomplexobj(arr) and dtype == torch.float64:
@@ -56,8 +61,6 @@ class _Vec:
             t = torch.from_numpy(np.ascontiguousarray(arr)).to(dtype)
             t = t.pin_memory().to("cuda", non_blocking=True) if t.numel() else t.to("cuda")
         else:
-            if not x.is_cuda:
-                raise ValueError("torch inputs must live on a CUDA device")
             if x.is_complex() and dtype == torch.float64:
                 raise TypeError("complex input to a real (MP-1) operator is not supported on the device path")
             t = x.to(dtype).contiguous()
@@ -72,9 +75,15 @@ class _Vec:
         shape = self.t.shape if n is None else (*self.t.shape[:-1], n)
         return torch.empty(shape, dtype=self.t.dtype, device=self.t.device)
 
-    def out(self, y: torch.Tensor):
+    def out(self, y: torch.Tensor, host_out=None):
         if self.numpy:
             return y.cpu().numpy()
+        if self.host_torch:
+            if host_out is None:
+                host_out = torch.empty(y.shape, dtype=y.dtype, pin_memory=True)
+            host_out.copy_(y, non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+            return host_out
         return y
 
 
@@ -296,20 +305,23 @@ class SchwarzPreconditioner:
         self.N0 = self.plan.N0
 
     # -- the individual operators (for parity tests and benchmarks) ---------
-    def _run(self, fn, x, out_len=None, in_len=None, *extra):
+    def _run(self, fn, x, out_len=None, in_len=None, out=None):
         v = _Vec(x, in_len or self.N, self.A.torch_dtype)
         if v.batch > self.max_batch:
             raise ValueError(f"batch {v.batch} exceeds max_batch {self.max_batch}")
-        y = v.empty_like(out_len or self.N)
+        y = out if (out is not None and out.is_cuda) else v.empty_like(out_len or self.N)
         with self.plan.lock:
-            _lib.check(fn(v.t, y, v.batch, *extra))
-        return v.out(y)
+            _lib.check(fn(v.t, y, v.batch))
+        return v.out(y, host_out=out if (out is not None and not out.is_cuda) else None)
 
-    def apply(self, x):
+    def apply(self, x, out=None):
+        """y = M^{-1} x.  ``out``: optional preallocated result (CUDA tensor, or pinned host
+        tensor when ``x`` is a host tensor)."""
         if isinstance(x, np.ndarray) and np.iscomplexobj(x) and self.A.dtype == np.float64:
             return _real_split(self.apply, x, self.N)
         p = self.plan
-        return self._run(lambda a, b, n: p.lib.helm_apply_M(p.handle, p.ws, _ptr(a), _ptr(b), n, _stream()), x)
+        return self._run(lambda a, b, n: p.lib.helm_apply_M(p.handle, p.ws, _ptr(a), _ptr(b), n, _stream()), x,
+                         out=out)
 
     __call__ = apply
 

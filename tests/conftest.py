@@ -1,6 +1,10 @@
 import os
 import sys
 
+# the oracle (scipy SuperLU) is single-threaded by design; BLAS threads only oversubscribe
+for _v in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS"):
+    os.environ.setdefault(_v, "1")
+
 import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))

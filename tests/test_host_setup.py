@@ -94,7 +94,7 @@ def test_library_exports_every_declared_symbol():
 
     lib = _lib.load()
     hdr = open(os.path.join(ROOT, "include", "helmb200.h")).read()
-    declared = set(re.findall(r"^\s*(?:int|int32_t|int64_t|const char\*)\s+(helm_\w+)\(", hdr, re.M))
+    declared = set(re.findall(r"^\s*(?:int|int32_t|int64_t|uint64_t|const char\*)\s+(helm_\w+)\(", hdr, re.M))
     assert declared, "no declarations parsed"
     bound = {s[0] for s in _lib.SYMBOLS}
     assert declared == bound
