@@ -45,7 +45,7 @@
 extern "C" {
 #endif
 
-#define HELM_ABI_VERSION 1
+#define HELM_ABI_VERSION 2
 
 enum helm_bc { HELM_DIRICHLET = 0, HELM_SOMMERFELD = 1 };
 enum helm_kind { HELM_AS2 = 0, HELM_SAS2 = 1, HELM_SHS2 = 2 };
@@ -75,16 +75,28 @@ typedef struct helm_desc {
   const void* class_V;        /* S, concatenated [L][L] row-major per class,
                                  T V = W V diag(lambda), V^T W V = I             */
   const void* class_lambda;   /* S, concatenated [L] per class                   */
-  /* --- coarse level (HOCS ratio 2, coarse.py:148-174): A0 = T0(x)M0 + M0(x)T0 - k^2 M0(x)M0 */
+  /* --- coarse level (HOCS ratio 2, coarse.py:148-174):
+   *     A0 = T0(x)M0 + M0(x)T0 - k^2 M0(x)M0  (y (x) x), solved by a fast
+   *     sine/cosine transform along x, one pivoted pentadiagonal solve per
+   *     x-mode along y, and (Sommerfeld) a Woodbury correction on n_strip
+   *     columns whose capacitance is 4x4-block-diagonal in the y-pencil
+   *     eigenbasis.  coarse_scale == NULL -> plan without a coarse solver.     */
   int32_t m0;                 /* coarse unknowns per dimension                   */
-  const void* coarse_V;       /* S [m0][m0]  T0 V = M0 V diag(lambda0), V^T M0 V = I */
-  const void* coarse_lambda;  /* S [m0]                                          */
+  const double* coarse_scale; /* [m0]  forward pre-scale sigma_a                 */
+  const double* coarse_lamT;  /* [m0]  Dirichlet: DST eigenvalues of T0          */
+  const double* coarse_lamM;  /* [m0]  Dirichlet: DST eigenvalues of M0          */
+  double coarse_qn;           /* Dirichlet DST normalisation 2/(m0+1)            */
   const void* t0_band;        /* S [m0][5]   T0[i][i+d-2]                        */
   const void* m0_band;        /* S [m0][5]   M0[i][i+d-2]                        */
-  /* pivoted band LU of T0 + (lambda0[a] - k^2) M0, stored [row][a] for coalescing */
+  /* Sommerfeld: pivoted band LU of T0 + s_a M0, stored [row][a] (coalescing) */
   const uint8_t* band_piv;    /* [m0][m0] pivot offset 0..2                      */
   const void* band_l;         /* S [m0][m0][2] multipliers                       */
   const void* band_u;         /* S [m0][m0][5] {1/U_jj, U_j,j+1 .. U_j,j+4}      */
+  int32_t n_strip;            /* 0 (Dirichlet) or 4 (Sommerfeld)                 */
+  const double* strip_q;      /* [m0][n_strip]  Q[strip_x[i], a]                 */
+  const void* cap_left;       /* S [m0][m0]  V^T M0 (V: y-pencil eigenvectors)   */
+  const void* cap_right;      /* S [m0][m0]  M0 V                                */
+  const void* cap_mode;       /* S [m0][n_strip][n_strip]                        */
   int32_t refine_steps;       /* iterative-refinement steps of the coarse solve  */
 } helm_desc;
 

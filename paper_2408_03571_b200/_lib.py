@@ -15,6 +15,7 @@ LIB_PATH = os.path.join(_HERE, "libhelmb200.so")
 
 HELM_DIRICHLET, HELM_SOMMERFELD = 0, 1
 KINDS = {"AS2": 0, "SAS2": 1, "SHS2": 2}
+ABI_VERSION = 2
 
 c_int32_p = ctypes.POINTER(ctypes.c_int32)
 
@@ -40,13 +41,20 @@ class HelmDesc(ctypes.Structure):
         ("class_V", ctypes.c_void_p),
         ("class_lambda", ctypes.c_void_p),
         ("m0", ctypes.c_int32),
-        ("coarse_V", ctypes.c_void_p),
-        ("coarse_lambda", ctypes.c_void_p),
+        ("coarse_scale", ctypes.c_void_p),
+        ("coarse_lamT", ctypes.c_void_p),
+        ("coarse_lamM", ctypes.c_void_p),
+        ("coarse_qn", ctypes.c_double),
         ("t0_band", ctypes.c_void_p),
         ("m0_band", ctypes.c_void_p),
         ("band_piv", ctypes.POINTER(ctypes.c_uint8)),
         ("band_l", ctypes.c_void_p),
         ("band_u", ctypes.c_void_p),
+        ("n_strip", ctypes.c_int32),
+        ("strip_q", ctypes.c_void_p),
+        ("cap_left", ctypes.c_void_p),
+        ("cap_right", ctypes.c_void_p),
+        ("cap_mode", ctypes.c_void_p),
         ("refine_steps", ctypes.c_int32),
     ]
 
@@ -112,7 +120,7 @@ def load() -> ctypes.CDLL:
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args
-    if lib.helm_abi_version() != 1:
+    if lib.helm_abi_version() != ABI_VERSION:
         raise ImportError("libhelmb200.so ABI version mismatch")
     _lib = lib
     return lib

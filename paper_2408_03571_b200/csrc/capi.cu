@@ -237,14 +237,33 @@ static void build_plan(const helm_desc* d, helm_plan* P) {
   PlanDev& dv = P->dev;
   std::memset(&dv, 0, sizeof(dv));
   const size_t m0 = g.m0;
-  if (d->coarse_V) {
-    dv.coarse_V = upload_bytes(d->coarse_V, m0 * m0 * P->elem);
-    dv.coarse_lambda = upload_bytes(d->coarse_lambda, m0 * P->elem);
+  if (d->coarse_scale) {
+    dv.m0 = (int)m0;
+    const int L = d->n - 1;
+    dv.fft_len = (L >= 8 && (L & (L - 1)) == 0 && L <= 2048) ? L : 0;  // else: direct transform
+    dv.coarse_scale = upload<double>(d->coarse_scale, m0);
     dv.t0_band = upload_bytes(d->t0_band, m0 * 5 * P->elem);
     dv.m0_band = upload_bytes(d->m0_band, m0 * 5 * P->elem);
-    dv.band_piv = (uint8_t*)upload_bytes(d->band_piv, m0 * m0);
-    dv.band_l = upload_bytes(d->band_l, m0 * m0 * 2 * P->elem);
-    dv.band_u = upload_bytes(d->band_u, m0 * m0 * 5 * P->elem);
+    if (d->bc == HELM_SOMMERFELD) {
+      HELM_CHECK(d->band_piv && d->band_l && d->band_u, "Sommerfeld coarse solver needs the band factors");
+      std::vector<int> piv32(d->band_piv, d->band_piv + m0 * m0);
+      dv.band_piv = upload<int>(piv32.data(), piv32.size());
+      dv.band_l = upload_bytes(d->band_l, m0 * m0 * 2 * P->elem);
+      dv.band_u = upload_bytes(d->band_u, m0 * m0 * 5 * P->elem);
+    } else {
+      dv.coarse_lamT = upload<double>(d->coarse_lamT, m0);
+      dv.coarse_lamM = upload<double>(d->coarse_lamM, m0);
+      dv.coarse_qn = d->coarse_qn;
+    }
+    HELM_CHECK(d->n_strip == (d->bc == HELM_SOMMERFELD ? 4 : 0), "n_strip must be 4 (Sommerfeld) or 0 (Dirichlet)");
+    dv.n_strip = d->n_strip;
+    if (d->n_strip) {
+      const size_t ns = d->n_strip;
+      dv.strip_q = upload<double>(d->strip_q, m0 * ns);
+      dv.cap_left = upload_bytes(d->cap_left, m0 * m0 * P->elem);
+      dv.cap_right = upload_bytes(d->cap_right, m0 * m0 * P->elem);
+      dv.cap_mode = upload_bytes(d->cap_mode, m0 * ns * ns * P->elem);
+    }
   }
   if (p == 0) return;
   P->h_box_start.assign(d->box_start, d->box_start + p);
@@ -294,6 +313,35 @@ static void build_plan(const helm_desc* d, helm_plan* P) {
   dv.class_off_lam = upload<int>(offL.data(), offL.size());
   dv.class_V = upload_bytes(d->class_V, totV * P->elem);
   dv.class_lambda = upload_bytes(d->class_lambda, totL * P->elem);
+  // real classes (the middle-class pencil tridiag(-1,2,-1)/h^2 with W = I) get a real copy of V
+  std::vector<int> creal(d->n_classes, 1);
+  std::vector<double> vr(totV, 0.0);
+  for (int c = 0; c < d->n_classes; ++c) {
+    const size_t L = P->h_class_len[c];
+    for (size_t e = 0; e < L * L; ++e) {
+      const size_t i = offV[c] + e;
+      if (d->is_complex) {
+        const double* v = (const double*)d->class_V + 2 * i;
+        vr[i] = v[0];
+        if (v[1] != 0.0) creal[c] = 0;
+      } else {
+        vr[i] = ((const double*)d->class_V)[i];
+      }
+    }
+    if (d->is_complex)
+      for (size_t e = 0; e < L; ++e)
+        if (((const double*)d->class_lambda)[2 * (offL[c] + e) + 1] != 0.0) creal[c] = 0;
+  }
+  dv.class_real = upload<int>(creal.data(), creal.size());
+  dv.class_Vr = upload<double>(vr.data(), vr.size());
+  std::vector<int> rr, mix;
+  for (int ay = 0; ay < p; ++ay)
+    for (int ax = 0; ax < p; ++ax)
+      (creal[P->h_box_class[ay]] && creal[P->h_box_class[ax]] ? rr : mix).push_back(ay * p + ax);
+  dv.n_rr = (int)rr.size();
+  dv.n_mix = (int)mix.size();
+  dv.box_rr = upload<int>(rr.data(), rr.size());
+  dv.box_mix = upload<int>(mix.data(), mix.size());
   dv.node_first_box = upload<int>(first.data(), nu);
   dv.node_mult = upload<int>(mult.data(), nu);
   dv.node_band = upload<int>(band.data(), nu);
@@ -303,16 +351,19 @@ static void build_plan(const helm_desc* d, helm_plan* P) {
 static void finish_desc(helm_plan* P) {
   // pointer members of the stored descriptor are not owned: clear them
   P->desc.box_start = P->desc.box_len = P->desc.box_class = P->desc.class_len = nullptr;
-  P->desc.class_V = P->desc.class_lambda = P->desc.coarse_V = P->desc.coarse_lambda = nullptr;
+  P->desc.class_V = P->desc.class_lambda = nullptr;
+  P->desc.coarse_scale = P->desc.strip_q = P->desc.coarse_lamT = P->desc.coarse_lamM = nullptr;
   P->desc.t0_band = P->desc.m0_band = P->desc.band_l = P->desc.band_u = nullptr;
+  P->desc.cap_left = P->desc.cap_right = P->desc.cap_mode = nullptr;
   P->desc.band_piv = nullptr;
 }
 
 static void free_plan(helm_plan* P) {
   PlanDev& dv = P->dev;
   void* ptrs[] = {dv.box_start, dv.box_len, dv.box_class, dv.class_len, dv.class_off_V, dv.class_off_lam,
-                  dv.class_V, dv.class_lambda, dv.node_first_box, dv.node_mult, dv.node_band, dv.band_node,
-                  dv.coarse_V, dv.coarse_lambda, dv.t0_band, dv.m0_band, dv.band_piv, dv.band_l, dv.band_u};
+                  dv.class_V, dv.class_lambda, dv.class_real, dv.class_Vr, dv.box_rr, dv.box_mix, dv.node_first_box, dv.node_mult, dv.node_band, dv.band_node,
+                  dv.coarse_scale, dv.coarse_lamT, dv.coarse_lamM, dv.t0_band, dv.m0_band, dv.band_piv, dv.band_l, dv.band_u, dv.strip_q,
+                  dv.cap_left, dv.cap_right, dv.cap_mode};
   for (void* q : ptrs)
     if (q) cudaFree(q);
 }
@@ -370,13 +421,15 @@ int helm_workspace_create(const helm_plan* P, int32_t max_batch, helm_workspace*
     w->plan = P;
     w->max_batch = max_batch;
     const size_t B = max_batch, e = P->elem;
-    HELM_CUBLAS(cublasCreate(&w->cublas));
     HELM_CUDA(cudaMalloc(&w->z, B * P->N * e));
     HELM_CUDA(cudaMalloc(&w->d, B * P->N * e));
-    void** coarse[] = {&w->c, &w->g, &w->y0, &w->r0, &w->e0};
+    void** coarse[] = {&w->c, &w->g, &w->y0, &w->r0, &w->e0, &w->f0};
     for (void** q : coarse) HELM_CUDA(cudaMalloc(q, B * P->N0 * e));
     const size_t novl = std::max<size_t>(1, B * 6 * (size_t)P->dev.nbands * P->geo.nu);
     HELM_CUDA(cudaMalloc(&w->ovl, novl * e));
+    for (int s = 0; s < 4; ++s)
+      if (P->dev.n_strip)
+        HELM_CUDA(cudaMalloc(&w->strip[s], (size_t)(s == 3 ? 4 : 1) * P->dev.m0 * B * P->dev.n_strip * e));
     w->red_bytes = krylov_scratch_bytes(4096);
     HELM_CUDA(cudaMalloc(&w->red, w->red_bytes));
     HELM_CUDA(cudaMallocHost(&w->pinned, 64 * sizeof(double)));
@@ -387,11 +440,11 @@ int helm_workspace_create(const helm_plan* P, int32_t max_batch, helm_workspace*
 int helm_workspace_destroy(helm_workspace* w) {
   return guarded([&] {
     if (!w) return;
-    void* ptrs[] = {w->z, w->d, w->c, w->g, w->y0, w->r0, w->e0, w->ovl, w->red};
+    void* ptrs[] = {w->z, w->d, w->c, w->g, w->y0, w->r0, w->e0, w->f0, w->ovl, w->red, w->strip[0], w->strip[1],
+                    w->strip[2], w->strip[3]};
     for (void* q : ptrs)
       if (q) cudaFree(q);
     if (w->pinned) cudaFreeHost(w->pinned);
-    if (w->cublas) cublasDestroy(w->cublas);
     delete w;
   });
 }

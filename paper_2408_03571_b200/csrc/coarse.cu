@@ -1,59 +1,197 @@
 // K5: the coarse solve  y = A0^{-1} c  (reference: linalg.solve(cs.a0_factorization, .)
 // at coarse.py:174, SuperLU factor of the symmetrised Galerkin matrix, coarse.py:154-167).
 //
-// A0 = R0 A R0^T is the Kronecker sum T0(x)M0 + M0(x)T0 - k^2 M0(x)M0 of two
-// pentadiagonal m0 x m0 pencils (T0 = P T P^T, M0 = P W P^T).  Partial fast
-// diagonalisation along x (the fast index):
-//   1. G = C V                (GEMM, V^T M0 V = I, T0 V = M0 V diag(lambda))
-//   2. (T0 + (lambda_a - k^2) M0) H[:,a] = G[:,a]   (m0 pivoted pentadiagonal solves)
-//   3. Y = H V^T              (GEMM)
-// followed by iterative refinement  r = c - A0 Y,  Y += solve(r)  (25-point
-// residual kernel), which pulls the FDM rounding (~1e-12 near coarse
-// resonances) down to SuperLU's own level.
-#include "common.cuh"
+// A0 = T0(x)M0 + M0(x)T0 - k^2 M0(x)M0 (y (x) x) with pentadiagonal 1-D pencils
+// T0 = P T P^T, M0 = P W P^T (verified bitwise against the reference).
+//
+// Dirichlet (MP-1): T0 and M0 are exactly diagonalised by the DST-I (the Bezier
+// restriction is consistent with the odd extension), so
+//   A0^{-1} = (Q(x)Q) diag(1 / (lT_y lM_x + lM_y lT_x - k^2 lM_y lM_x)) (Q^-1(x)Q^-1)
+// = row DST, transpose, row DST + 2-D scaling, row DST, transpose, row DST.
+//
+// Sommerfeld (MP-2): along x, T0 = T~ + L_T and M0 = M~ + L_M where (T~, M~) is
+// diagonalised by the DCT-I (T~ Q = W Q lamT, M~ Q = W Q lamM) and L_T, L_M live
+// on the 2x2 corner blocks (the restriction drops its out-of-range taps,
+// coarse.py:116-128, instead of reflecting them).  One solve is
+//   1. F^ = DCT_x(F) * sigma_a                                    (xform.cu)
+//   2. per x-mode a: (T0 + s_a M0) Y^[:,a] = F^[:,a]                (band.cu; the exact,
+//      damped y-operator, so no near-resonant division appears)
+//   3. Woodbury on the 4 strip columns x in {0, 1, m0-2, m0-1}:
+//        Z = Y^ q (strip values), z^ = (V^T M0) Z, c^_b = H_b z^_b (4x4 per y-mode b
+//        of the y-pencil T0 V = M0 V diag(lam)), cS = (M0 V) c^,
+//        F^ -= sigma_a cS q^T, and step 2 again
+//   4. Y = DCT_x(Y^).
+// Everything is O(m0^2 log m0) per right-hand side and HBM-bound (dense fast
+// diagonalisation would be O(m0^3) FP64).  refine_steps iterative-refinement
+// steps r = c - A0 y (25-point residual), y += solve(r) follow.
+#include "ops.cuh"
 
 namespace helm {
 
-// --- pivoted pentadiagonal solves, one thread per (batch, column a) ---------
-// Factor layout [row][a]: piv (0..2), l[2], u[5] = {1/U_jj, U_j,j+1 .. U_j,j+4}.
+// ----------------------------------------------------------------------------
+// Woodbury strip step
+// ----------------------------------------------------------------------------
+// Z[y][b*4+i] = sum_a q[a][i] Yh[b][y][a]   (one warp per (batch, row))
 template <typename S>
-__global__ void __launch_bounds__(128) band_solve_kernel(S* __restrict__ G, const uint8_t* __restrict__ piv,
-                                                         const S* __restrict__ L, const S* __restrict__ U,
-                                                         int m0) {
-  const int a = blockIdx.x * blockDim.x + threadIdx.x;
-  if (a >= m0) return;
-  S* col = G + (size_t)blockIdx.y * m0 * m0 + a;
-  const size_t ld = m0;
-  // forward: apply the row interchanges and eliminations to the right-hand side
-  S r0 = col[0];
-  S r1 = m0 > 1 ? col[ld] : Sc<S>::zero();
-  S r2 = m0 > 2 ? col[2 * ld] : Sc<S>::zero();
-  for (int j = 0; j < m0; ++j) {
-    const size_t f = (size_t)j * m0 + a;
-    const int pv = piv[f];
-    if (pv == 1) { S t = r0; r0 = r1; r1 = t; }
-    else if (pv == 2) { S t = r0; r0 = r2; r2 = t; }
-    r1 = fms_(L[2 * f], r0, r1);
-    r2 = fms_(L[2 * f + 1], r0, r2);
-    col[(size_t)j * ld] = r0;
-    r0 = r1;
-    r1 = r2;
-    r2 = (j + 3 < m0) ? col[(size_t)(j + 3) * ld] : Sc<S>::zero();
+__global__ void __launch_bounds__(256) strip_reduce_kernel(const S* __restrict__ Yh, const double* __restrict__ q,
+                                                           S* __restrict__ Z, int m0, int ldz) {
+  const int y = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int b = blockIdx.y;
+  if (y >= m0) return;
+  const S* row = Yh + ((size_t)b * m0 + y) * m0;
+  S acc[4] = {Sc<S>::zero(), Sc<S>::zero(), Sc<S>::zero(), Sc<S>::zero()};
+  for (int a = lane; a < m0; a += 32) {
+    const S v = row[a];
+    const double4 qa = *reinterpret_cast<const double4*>(q + (size_t)a * 4);
+    acc[0] = fma_(qa.x, v, acc[0]);
+    acc[1] = fma_(qa.y, v, acc[1]);
+    acc[2] = fma_(qa.z, v, acc[2]);
+    acc[3] = fma_(qa.w, v, acc[3]);
   }
-  // backward substitution with the 4 super-diagonals of U
-  S x1 = Sc<S>::zero(), x2 = x1, x3 = x1, x4 = x1;
-  for (int j = m0 - 1; j >= 0; --j) {
-    const size_t f = (size_t)j * m0 + a;
-    const S* u = U + 5 * f;
-    S v = col[(size_t)j * ld];
-    v = fms_(u[1], x1, v);
-    v = fms_(u[2], x2, v);
-    v = fms_(u[3], x3, v);
-    v = fms_(u[4], x4, v);
-    v = mul(v, u[0]);
-    col[(size_t)j * ld] = v;
-    x4 = x3; x3 = x2; x2 = x1; x1 = v;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) acc[i] = warp_sum(acc[i]);
+  if (lane < 4) Z[(size_t)y * ldz + (size_t)b * 4 + lane] = acc[lane];
+}
+
+// out[m][b*4+i] = (Hm)? sum_j Hm[m][i][j] t[j] : t[i],  t[j] = sum_y A[m][y] Z[y][b*4+j]
+// Tiled form for many columns: 64 rows x 8 column groups of 4 per CTA (2 rows x 1 group
+// per thread, register-blocked), K split GT_KS ways into a partial-sum scratch that a
+// second kernel reduces in a fixed order (deterministic) and applies the 4x4 epilogue.
+constexpr int GT_M = 64, GT_G = 8, GT_K = 16, GT_KS = 4;
+template <typename S>
+__global__ void __launch_bounds__(256) strip_gemm_part_kernel(const S* __restrict__ A, const S* __restrict__ Z,
+                                                              S* __restrict__ part, int m0, int ngroups) {
+  __shared__ S As[GT_M][GT_K + 1];
+  __shared__ S Zs[GT_K][GT_G * 4];
+  const int ldz = ngroups * 4;
+  const int tr = threadIdx.x / GT_G, tg = threadIdx.x % GT_G;
+  const int kchunk = ((m0 + GT_KS - 1) / GT_KS + GT_K - 1) / GT_K * GT_K;
+  const int kbeg = blockIdx.z * kchunk, kend = min(m0, kbeg + kchunk);
+  S acc[2][4];
+#pragma unroll
+  for (int q = 0; q < 2; ++q)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) acc[q][i] = Sc<S>::zero();
+  for (int k0 = kbeg; k0 < kend; k0 += GT_K) {
+    for (int e = threadIdx.x; e < GT_M * GT_K; e += blockDim.x) {
+      const int r = e / GT_K, kk = e % GT_K;
+      const int mm = blockIdx.y * GT_M + r, k = k0 + kk;
+      As[r][kk] = (mm < m0 && k < kend) ? A[(size_t)mm * m0 + k] : Sc<S>::zero();
+    }
+    for (int e = threadIdx.x; e < GT_K * GT_G * 4; e += blockDim.x) {
+      const int kk = e / (GT_G * 4), c = e % (GT_G * 4);
+      const int k = k0 + kk, col = blockIdx.x * GT_G * 4 + c;
+      Zs[kk][c] = (k < kend && col < ldz) ? Z[(size_t)k * ldz + col] : Sc<S>::zero();
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < GT_K; ++kk) {
+      const S a0 = As[2 * tr][kk], a1 = As[2 * tr + 1][kk];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const S zv = Zs[kk][tg * 4 + i];
+        acc[0][i] = fma_(a0, zv, acc[0][i]);
+        acc[1][i] = fma_(a1, zv, acc[1][i]);
+      }
+    }
+    __syncthreads();
   }
+  const int g = blockIdx.x * GT_G + tg;
+  if (g >= ngroups) return;
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const int m = blockIdx.y * GT_M + 2 * tr + q;
+    if (m >= m0) continue;
+    S* o = part + ((size_t)blockIdx.z * m0 + m) * ldz + (size_t)g * 4;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) o[i] = acc[q][i];
+  }
+}
+
+template <typename S>
+__global__ void __launch_bounds__(256) strip_gemm_reduce_kernel(const S* __restrict__ part, S* __restrict__ out,
+                                                                const S* __restrict__ Hm, int m0, int ngroups) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= m0 * ngroups) return;
+  const int m = e / ngroups, g = e % ngroups;
+  const int ldz = ngroups * 4;
+  S t[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    S s = Sc<S>::zero();
+    for (int ks = 0; ks < GT_KS; ++ks) s = add(s, part[((size_t)ks * m0 + m) * ldz + g * 4 + i]);
+    t[i] = s;
+  }
+  S* o = out + (size_t)m * ldz + (size_t)g * 4;
+  if (Hm) {
+    const S* h = Hm + (size_t)m * 16;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      S s = Sc<S>::zero();
+#pragma unroll
+      for (int j = 0; j < 4; ++j) s = fma_(h[i * 4 + j], t[j], s);
+      o[i] = s;
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) o[i] = t[i];
+  }
+}
+
+// Warp-per-row form for few columns (batch <= 4): lanes stride over y.
+template <typename S, int NG>
+__global__ void __launch_bounds__(256) strip_gemm_rows_kernel(const S* __restrict__ A, const S* __restrict__ Z,
+                                                              S* __restrict__ out, const S* __restrict__ Hm, int m0) {
+  const int m = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (m >= m0) return;
+  constexpr int NC = NG * 4;
+  S acc[NC];
+#pragma unroll
+  for (int c = 0; c < NC; ++c) acc[c] = Sc<S>::zero();
+  for (int y = lane; y < m0; y += 32) {
+    const S av = A[(size_t)m * m0 + y];
+#pragma unroll
+    for (int c = 0; c < NC; ++c) acc[c] = fma_(av, Z[(size_t)y * NC + c], acc[c]);
+  }
+#pragma unroll
+  for (int c = 0; c < NC; ++c) acc[c] = warp_sum(acc[c]);
+  if (lane != 0) return;
+  const S* h = Hm ? Hm + (size_t)m * 16 : nullptr;
+#pragma unroll
+  for (int g = 0; g < NG; ++g) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      S s;
+      if (h) {
+        s = Sc<S>::zero();
+#pragma unroll
+        for (int j = 0; j < 4; ++j) s = fma_(h[i * 4 + j], acc[g * 4 + j], s);
+      } else {
+        s = acc[g * 4 + i];
+      }
+      out[(size_t)m * NC + g * 4 + i] = s;
+    }
+  }
+}
+
+template <typename S>
+static void strip_gemm(const S* A, const S* Z, S* out, const S* Hm, int m0, int batch, S* part, cudaStream_t st) {
+  const int rows_blocks = (m0 * 32 + 255) / 256;
+  switch (batch) {
+    case 1: strip_gemm_rows_kernel<S, 1><<<rows_blocks, 256, 0, st>>>(A, Z, out, Hm, m0); break;
+    case 2: strip_gemm_rows_kernel<S, 2><<<rows_blocks, 256, 0, st>>>(A, Z, out, Hm, m0); break;
+    case 3: strip_gemm_rows_kernel<S, 3><<<rows_blocks, 256, 0, st>>>(A, Z, out, Hm, m0); break;
+    case 4: strip_gemm_rows_kernel<S, 4><<<rows_blocks, 256, 0, st>>>(A, Z, out, Hm, m0); break;
+    default: {
+      dim3 grd((batch + GT_G - 1) / GT_G, (m0 + GT_M - 1) / GT_M, GT_KS);
+      strip_gemm_part_kernel<S><<<grd, 256, 0, st>>>(A, Z, part, m0, batch);
+      HELM_LAUNCH_CHECK();
+      strip_gemm_reduce_kernel<S><<<(m0 * batch + 255) / 256, 256, 0, st>>>(part, out, Hm, m0, batch);
+    }
+  }
+  HELM_LAUNCH_CHECK();
 }
 
 // --- r = c - A0 y  (25-point Kronecker-sum stencil from the 1-D bands) ------
@@ -61,26 +199,46 @@ template <typename S>
 __global__ void __launch_bounds__(256) a0_residual_kernel(const S* __restrict__ c, const S* __restrict__ y,
                                                           S* __restrict__ r, const S* __restrict__ t0b,
                                                           const S* __restrict__ m0b, double k2, int m0) {
-  const int V = blockIdx.x * blockDim.x + threadIdx.x;
-  const int Uc = blockIdx.y * blockDim.y + threadIdx.y;
-  if (V >= m0 || Uc >= m0) return;
+  // 32 x 8 outputs per CTA; the (8+4) x (32+4) window of y is staged in shared
+  // memory (zero outside = the band ends), then the separable x-pass (M0, T0 rows)
+  // and y-pass run from shared memory.
+  constexpr int RX = 32, RY = 8;
+  __shared__ S ys[RY + 4][RX + 4];
+  __shared__ S xm[RY + 4][RX], xt[RY + 4][RX];
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  const int V0 = blockIdx.x * RX, U0 = blockIdx.y * RY;
   const size_t off = (size_t)blockIdx.z * m0 * m0;
-  S acc = Sc<S>::zero();
-  for (int dy = -2; dy <= 2; ++dy) {
-    const int U = Uc + dy;
-    if (U < 0 || U >= m0) continue;
-    const S ty = t0b[Uc * 5 + dy + 2], my = m0b[Uc * 5 + dy + 2];
-    S rowT = Sc<S>::zero(), rowM = Sc<S>::zero();  // sum_dx M0 y, sum_dx T0 y along x
-    for (int dx = -2; dx <= 2; ++dx) {
-      const int W = V + dx;
-      if (W < 0 || W >= m0) continue;
-      const S yv = y[off + (size_t)U * m0 + W];
-      rowM = fma_(m0b[V * 5 + dx + 2], yv, rowM);
-      rowT = fma_(t0b[V * 5 + dx + 2], yv, rowT);
+  for (int e = ty * RX + tx; e < (RY + 4) * (RX + 4); e += RX * RY) {
+    const int rr = e / (RX + 4), q = e % (RX + 4);
+    const int U = U0 + rr - 2, W = V0 + q - 2;
+    ys[rr][q] = (U >= 0 && U < m0 && W >= 0 && W < m0) ? y[off + (size_t)U * m0 + W] : Sc<S>::zero();
+  }
+  __syncthreads();
+  const int V = V0 + tx;
+  S bm[5], bt[5];
+#pragma unroll
+  for (int d = 0; d < 5; ++d) {
+    bm[d] = V < m0 ? m0b[V * 5 + d] : Sc<S>::zero();
+    bt[d] = V < m0 ? t0b[V * 5 + d] : Sc<S>::zero();
+  }
+  for (int rr = ty; rr < RY + 4; rr += RY) {  // x-pass: sum_dx M0[V][V+dx] y, T0[V][V+dx] y
+    S sm = Sc<S>::zero(), stt = Sc<S>::zero();
+#pragma unroll
+    for (int d = 0; d < 5; ++d) {
+      sm = fma_(bm[d], ys[rr][tx + d], sm);
+      stt = fma_(bt[d], ys[rr][tx + d], stt);
     }
-    // T0(y) M0(x) + M0(y) T0(x) - k^2 M0(y) M0(x)
-    acc = fma_(ty, rowM, acc);
-    acc = fma_(my, sub(rowT, scale(rowM, k2)), acc);
+    xm[rr][tx] = sm;
+    xt[rr][tx] = sub(stt, scale(sm, k2));
+  }
+  __syncthreads();
+  const int Uc = U0 + ty;
+  if (V >= m0 || Uc >= m0) return;
+  S acc = Sc<S>::zero();  // T0(y) M0(x) + M0(y) (T0(x) - k^2 M0(x))
+#pragma unroll
+  for (int d = 0; d < 5; ++d) {
+    acc = fma_(t0b[Uc * 5 + d], xm[ty + d][tx], acc);
+    acc = fma_(m0b[Uc * 5 + d], xt[ty + d][tx], acc);
   }
   const size_t p = off + (size_t)Uc * m0 + V;
   r[p] = sub(c[p], acc);
@@ -92,52 +250,56 @@ __global__ void axpy_kernel(S* __restrict__ y, const S* __restrict__ d, size_t n
     y[i] = add(y[i], d[i]);
 }
 
-// Row-major G[(b,Iy)][a] = sum_Ix C[(b,Iy)][Ix] V[Ix][a]  (column-major: G^T = V^T C^T)
-// Row-major Y[(b,Iy)][Ix] = sum_a H[(b,Iy)][a] V[Ix][a]   (column-major: Y^T = V H^T)
+// ----------------------------------------------------------------------------
+// composition
+// ----------------------------------------------------------------------------
+// One fast solve: out = A0^{-1} in  (in, out distinct from ws->g / ws->f0)
 template <typename S>
-void coarse_gemm(cublasHandle_t h, const S* Vm, const S* in, S* out, int m0, int rows, bool transposeV) {
-  cublasOperation_t op = transposeV ? CUBLAS_OP_T : CUBLAS_OP_N;
-  if constexpr (Sc<S>::cplx) {
-    const cuDoubleComplex one = make_cuDoubleComplex(1.0, 0.0), zero = make_cuDoubleComplex(0.0, 0.0);
-    HELM_CUBLAS(cublasZgemm(h, op, CUBLAS_OP_N, m0, rows, m0, &one, (const cuDoubleComplex*)Vm, m0,
-                            (const cuDoubleComplex*)in, m0, &zero, (cuDoubleComplex*)out, m0));
-  } else {
-    const double one = 1.0, zero = 0.0;
-    HELM_CUBLAS(cublasDgemm(h, op, CUBLAS_OP_N, m0, rows, m0, &one, Vm, m0, in, m0, &zero, out, m0));
-  }
-}
-
-// One partial-FDM solve: out = A0~^{-1} in  (in and out distinct; tmp scratch [B][N0])
-template <typename S>
-static void fdm_solve(const helm_plan* P, helm_workspace* ws, const S* in, S* out, S* tmp, int batch,
-                      cudaStream_t st) {
+static void fast_solve(const helm_plan* P, helm_workspace* ws, const S* in, S* out, int batch, cudaStream_t st) {
   const PlanDev& d = P->dev;
-  const int m0 = P->geo.m0;
-  HELM_CUBLAS(cublasSetStream(ws->cublas, st));
-  coarse_gemm<S>(ws->cublas, (const S*)d.coarse_V, in, tmp, m0, m0 * batch, false);
-  dim3 grd((m0 + 127) / 128, batch);
-  band_solve_kernel<S><<<grd, 128, 0, st>>>(tmp, d.band_piv, (const S*)d.band_l, (const S*)d.band_u, m0);
-  HELM_LAUNCH_CHECK();
-  coarse_gemm<S>(ws->cublas, (const S*)d.coarse_V, tmp, out, m0, m0 * batch, true);
+  S* T1 = (S*)ws->g;
+  S* T2 = (S*)ws->f0;
+  if constexpr (!Sc<S>::cplx) {
+    // Dirichlet: separable 2-D DST
+    launch_xform<S>(P, in, T1, d.coarse_scale, false, batch, st);
+    launch_transpose<S>(T1, T2, d.m0, batch, st);
+    launch_xform<S>(P, T2, T1, nullptr, true, batch, st);
+    launch_xform<S>(P, T1, T2, nullptr, false, batch, st);
+    launch_transpose<S>(T2, T1, d.m0, batch, st);
+    launch_xform<S>(P, T1, out, nullptr, false, batch, st);
+  } else {
+    launch_xform<S>(P, in, T1, d.coarse_scale, false, batch, st);
+    launch_band_solve(P, T1, T2, nullptr, batch, st);
+    S* Z = (S*)ws->strip[0];
+    S* Ch = (S*)ws->strip[1];
+    S* Cs = (S*)ws->strip[2];
+    dim3 grd((d.m0 * 32 + 255) / 256, batch);
+    strip_reduce_kernel<S><<<grd, 256, 0, st>>>(T2, d.strip_q, Z, d.m0, batch * 4);
+    HELM_LAUNCH_CHECK();
+    S* part = (S*)ws->strip[3];
+    strip_gemm<S>((const S*)d.cap_left, Z, Ch, (const S*)d.cap_mode, d.m0, batch, part, st);
+    strip_gemm<S>((const S*)d.cap_right, Ch, Cs, nullptr, d.m0, batch, part, st);
+    launch_band_solve(P, T1, T2, Cs, batch, st);
+    launch_xform<S>(P, T2, out, nullptr, false, batch, st);
+  }
 }
 
 template <typename S>
 void launch_coarse_solve(const helm_plan* P, helm_workspace* ws, const S* c, S* y, int batch, cudaStream_t st) {
-  HELM_CHECK(P->dev.coarse_V != nullptr, "plan was created without a coarse solver");
+  HELM_CHECK(P->dev.coarse_scale != nullptr, "plan was created without a coarse solver");
   const int m0 = P->geo.m0;
   const size_t n0 = (size_t)batch * m0 * m0;
-  S* tmp = (S*)ws->g;
   S* r = (S*)ws->r0;
   S* corr = (S*)ws->e0;
   // c is only read; y is written last when it aliases c
   S* yy = ((const void*)c == (const void*)y) ? (S*)ws->y0 : y;
-  fdm_solve<S>(P, ws, c, yy, tmp, batch, st);
+  fast_solve<S>(P, ws, c, yy, batch, st);
   for (int it = 0; it < P->desc.refine_steps; ++it) {
     dim3 blk(32, 8), grd((m0 + 31) / 32, (m0 + 7) / 8, batch);
     a0_residual_kernel<S><<<grd, blk, 0, st>>>(c, yy, r, (const S*)P->dev.t0_band, (const S*)P->dev.m0_band,
                                                P->geo.k2, m0);
     HELM_LAUNCH_CHECK();
-    fdm_solve<S>(P, ws, r, corr, tmp, batch, st);
+    fast_solve<S>(P, ws, r, corr, batch, st);
     axpy_kernel<S><<<1184, 256, 0, st>>>(yy, corr, n0);
     HELM_LAUNCH_CHECK();
   }

@@ -4,7 +4,6 @@
 #pragma once
 
 #include <cuda_runtime.h>
-#include <cublas_v2.h>
 #include <cstdint>
 #include <cstdio>
 #include <string>
@@ -78,6 +77,21 @@ __host__ __device__ __forceinline__ double2 recip(double2 b) {
   return mk(b.x / d, -b.y / d);
 }
 
+// warp-level sums (xor butterfly: every lane ends with the total)
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ double2 warp_sum(double2 v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    v.x += __shfl_xor_sync(0xffffffffu, v.x, o);
+    v.y += __shfl_xor_sync(0xffffffffu, v.y, o);
+  }
+  return v;
+}
+
 // ----------------------------------------------------------------------------
 // error plumbing
 // ----------------------------------------------------------------------------
@@ -92,12 +106,6 @@ void set_last_error(const std::string& msg);
     if (e_ != cudaSuccess)                                                                \
       throw ::helm::Error(std::string(#call) + ": " + cudaGetErrorString(e_) + " @" +      \
                           __FILE__ + ":" + std::to_string(__LINE__));                     \
-  } while (0)
-#define HELM_CUBLAS(call)                                                                 \
-  do {                                                                                    \
-    cublasStatus_t s_ = (call);                                                           \
-    if (s_ != CUBLAS_STATUS_SUCCESS)                                                      \
-      throw ::helm::Error(std::string(#call) + ": cublas status " + std::to_string((int)s_)); \
   } while (0)
 #define HELM_CHECK(cond, msg)                                                             \
   do {                                                                                    \
@@ -137,20 +145,35 @@ struct PlanDev {
   int* class_off_lam;  // element offset of class c in class_lambda
   void* class_V;
   void* class_lambda;
+  int* class_real;     // 1: V and lambda of the class are real (class_Vr holds V)
+  double* class_Vr;
+  int* box_rr;         // subdomain ids (ay * p + ax) whose two classes are real
+  int n_rr;
+  int* box_mix;        // the other subdomains
+  int n_mix;
   // per-unknown 1-D overlap bookkeeping
   int* node_first_box; // first box containing unknown i
   int* node_mult;      // 1 or 2
   int* node_band;      // compact overlap-band index or -1
   int* band_node;      // inverse of node_band
   int nbands;          // number of 1-D unknowns with multiplicity 2
-  // coarse
-  void* coarse_V;
-  void* coarse_lambda;
+  // coarse (fast x-transform + band solves + Woodbury strips)
+  int m0;
+  int fft_len;         // n - 1 when it is a power of two, else 0 (direct transform)
+  double* coarse_scale;
+  double* coarse_lamT;  // Dirichlet 2-D DST scaling
+  double* coarse_lamM;
+  double coarse_qn;
   void* t0_band;
   void* m0_band;
-  uint8_t* band_piv;
+  int* band_piv;        // Sommerfeld band LU (pivot offsets widened to int for 4-byte cp.async)
   void* band_l;
   void* band_u;
+  int n_strip;
+  double* strip_q;
+  void* cap_left;
+  void* cap_right;
+  void* cap_mode;
 };
 
 }  // namespace helm
@@ -168,7 +191,6 @@ struct helm_plan {
 struct helm_workspace {
   const helm_plan* plan;
   int max_batch;
-  cublasHandle_t cublas;
   void* z;        // [B][N]
   void* d;        // [B][N]
   void* c;        // [B][N0]
@@ -176,7 +198,9 @@ struct helm_workspace {
   void* y0;       // [B][N0]
   void* r0;       // [B][N0]
   void* e0;       // [B][N0]
+  void* f0;       // [B][N0]
   void* ovl;      // overlap scratch [B][6][nbands][nu]
+  void* strip[4]; // coarse Woodbury scratch [m0][B * n_strip] x3, split-K partials x4
   void* red;      // reduction scratch (doubles)
   size_t red_bytes;
   void* pinned;   // small pinned host buffer for scalar read-back

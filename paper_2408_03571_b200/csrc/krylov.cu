@@ -17,21 +17,6 @@ constexpr int KB = 256;        // threads per block
 constexpr int KNB = 4 * 148;   // reduction blocks (4 per SM)
 constexpr int KG = 8;          // vectors per multi-dot group
 
-template <typename T>
-__device__ __forceinline__ T warp_sum(T v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  return v;
-}
-__device__ __forceinline__ double2 warp_sum(double2 v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    v.x += __shfl_xor_sync(0xffffffffu, v.x, o);
-    v.y += __shfl_xor_sync(0xffffffffu, v.y, o);
-  }
-  return v;
-}
-
 // partial[i * gridDim.x + block] = sum over the block's elements of conj(V_i) w
 template <typename S>
 __global__ void __launch_bounds__(KB) dots_kernel(const S* __restrict__ V, int nvec, size_t ldv,

@@ -12,27 +12,10 @@
 // are written directly (base + contribution); nodes in an overlap band write
 // their contribution into a per-slot scratch that a deterministic combine pass
 // sums (no atomics, so the result is bitwise reproducible).
-#include "common.cuh"
+#include "local.cuh"
 
 namespace helm {
 
-struct LocalArgs {
-  int nu;
-  int p;
-  int nbands;
-  double k2;
-  int weighted;
-  int wbs;  // weights before solve
-  const int* box_start;
-  const int* box_len;
-  const int* box_class;
-  const int* class_len;
-  const int* class_off_V;
-  const int* class_off_lam;
-  const int* node_first_box;
-  const int* node_mult;
-  const int* node_band;
-};
 
 // C[M][N] (row-major, ldc) = sum_k A(m,k) * B(k,n), operands in shared memory.
 // transA: A(m,k) = Asm[k][m]; transB: B(k,n) = Bsm[n][k].
@@ -168,6 +151,7 @@ __global__ void combine_cols_kernel(const S* __restrict__ base, S* __restrict__ 
   y[b * N + pidx] = base ? add(base[b * N + pidx], acc) : acc;
 }
 
+
 size_t local_smem_bytes(int ld, size_t elem) { return (size_t)(4 * ld * ld + 2 * ld) * elem; }
 
 template <typename S>
@@ -192,15 +176,18 @@ void launch_local_sum(const helm_plan* P, const S* x, const S* base, S* y, S* ov
   a.node_mult = d.node_mult;
   a.node_band = d.node_band;
   const int ld = d.max_len;
-  const size_t smem = local_smem_bytes(ld, sizeof(S));
-  static bool attr_set[2] = {false, false};
-  if (!attr_set[Sc<S>::cplx]) {
-    HELM_CUDA(cudaFuncSetAttribute(local_fdm_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    attr_set[Sc<S>::cplx] = true;
-  }
   dim3 grd(d.p * d.p, batch);
-  local_fdm_kernel<S><<<grd, 256, smem, st>>>(x, base, y, ovl, (const S*)d.class_V, (const S*)d.class_lambda, a, ld);
-  HELM_LAUNCH_CHECK();
+  if (!launch_local_fast<S>(P, x, base, y, ovl, a, batch, st)) {
+    const size_t smem = local_smem_bytes(ld, sizeof(S));
+    static bool attr_set[2] = {false, false};
+    if (!attr_set[Sc<S>::cplx]) {
+      HELM_CUDA(cudaFuncSetAttribute(local_fdm_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+      attr_set[Sc<S>::cplx] = true;
+    }
+    local_fdm_kernel<S><<<grd, 256, smem, st>>>(x, base, y, ovl, (const S*)d.class_V, (const S*)d.class_lambda, a,
+                                                ld);
+    HELM_LAUNCH_CHECK();
+  }
   if (d.nbands > 0) {
     dim3 g1((a.nu + 127) / 128, d.nbands, batch);
     combine_rows_kernel<S><<<g1, 128, 0, st>>>(base, y, ovl, band_node, d.node_mult, a.nu, d.nbands);

@@ -13,6 +13,14 @@ void launch_local_sum(const helm_plan* P, const S* x, const S* base, S* y, S* ov
 template <typename S>
 void launch_coarse_solve(const helm_plan* P, helm_workspace* ws, const S* c, S* y, int batch, cudaStream_t st);
 
+// coarse-solve building blocks (xform.cu, band.cu)
+template <typename S>
+void launch_xform(const helm_plan* P, const S* in, S* out, const double* sig, bool scale2d, int batch,
+                  cudaStream_t st);
+template <typename S> void launch_transpose(const S* in, S* out, int m, int batch, cudaStream_t st);
+void launch_band_solve(const helm_plan* P, const double2* in, double2* out, const double2* corr, int batch,
+                       cudaStream_t st);
+
 // composite operators (capi.cu)
 template <typename S> void op_apply_A(const helm_plan* P, const S* x, S* y, int batch, cudaStream_t st);
 template <typename S>

@@ -1,0 +1,287 @@
+// Fast sine / cosine transforms along the rows of coarse vectors (part of K5,
+// the coarse solve; see coarse.cu for the algorithm and the reference lines).
+//
+//   out[r][a] = s(r, a) * sum_J Q[J][a] in[r][J]
+//   DCT-I (Sommerfeld): Q[J][a] = cos(pi a J / M),        M = m0 - 1, FFT length L = 2M = n - 1
+//   DST-I (Dirichlet):  Q[J][a] = sin(pi (J+1)(a+1) / K), K = m0 + 1, FFT length L = 2K = n - 1
+//   s(r, a) = 1, sig[a], or the 2-D Dirichlet eigenvalue scaling
+//             qn / (lamT[a] lamM[kx] + lamM[a] lamT[kx] - k^2 lamM[a] lamM[kx]),  kx = r mod m0.
+//
+// A CTA runs FFTs of the symmetric extension (L/8 threads each) in shared
+// memory: radix-8 Stockham stages (radix 4/2 for the remainder) in registers,
+// in place through a barrier, twiddles tabulated once per CTA with sincospi.
+// Real rows are packed two per FFT: Q is real, so DST(x + i y) = DST(x) + i DST(y).  Rows are read and written with coalesced
+// 8/16-byte accesses; the transform is HBM-bound at the BASELINE sizes.
+#include "ops.cuh"
+
+namespace helm {
+
+struct XScale {
+  const double* sig;   // per-mode scale, or NULL
+  const double* lamT;  // 2-D Dirichlet scaling (NULL: off)
+  const double* lamM;
+  double k2;
+  double qn;
+};
+
+__device__ __forceinline__ double xscale(const XScale& s, int r, int a, int m0) {
+  if (s.lamT) {
+    const int kx = r % m0;
+    return s.qn / (s.lamT[a] * s.lamM[kx] + s.lamM[a] * s.lamT[kx] - s.k2 * s.lamM[a] * s.lamM[kx]);
+  }
+  return s.sig ? s.sig[a] : 1.0;
+}
+
+// In-register 8-point DFT (natural order in and out): radix-2 decimation in frequency.
+__device__ __forceinline__ void dft8(double2 v[8]) {
+  constexpr double h = 0.70710678118654752440;
+  const double2 w8[4] = {mk(1.0, 0.0), mk(h, -h), mk(0.0, -1.0), mk(-h, -h)};
+#pragma unroll
+  for (int n = 0; n < 4; ++n) {
+    const double2 t = sub(v[n], v[n + 4]);
+    v[n] = add(v[n], v[n + 4]);
+    v[n + 4] = mul(t, w8[n]);
+  }
+#pragma unroll
+  for (int g = 0; g < 8; g += 4) {
+#pragma unroll
+    for (int n = 0; n < 2; ++n) {
+      const double2 t = sub(v[g + n], v[g + n + 2]);
+      v[g + n] = add(v[g + n], v[g + n + 2]);
+      v[g + n + 2] = n ? mk(t.y, -t.x) : t;  // * (-i)^n
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 8; i += 2) {
+    const double2 t = sub(v[i], v[i + 1]);
+    v[i] = add(v[i], v[i + 1]);
+    v[i + 1] = t;
+  }
+  // bit-reversed -> natural
+  double2 t = v[1]; v[1] = v[4]; v[4] = t;
+  t = v[3]; v[3] = v[6]; v[6] = t;
+}
+__device__ __forceinline__ void dft4(double2 v[4]) {
+  const double2 a = add(v[0], v[2]), b = sub(v[0], v[2]), c = add(v[1], v[3]), d = sub(v[1], v[3]);
+  v[0] = add(a, c);
+  v[2] = sub(a, c);
+  v[1] = mk(b.x + d.y, b.y - d.x);  // b - i d
+  v[3] = mk(b.x - d.y, b.y + d.x);  // b + i d
+}
+
+// One in-place Stockham stage of radix R over a row of length L held in smem.
+// Butterfly j: inputs buf[j + r L/R], twiddle W_{Ns R}^{(j mod Ns) r}, outputs at
+// (j / Ns) Ns R + (j mod Ns) + r Ns.  All reads complete (barrier) before any write.
+template <int R>
+__device__ __forceinline__ void stockham_stage(double2* buf, const double2* tw, int L, int Ns, int tid, int T) {
+  const int nb = L / R;           // = (8 / R) T butterflies: each thread owns NBT of them
+  constexpr int NBT = 8 / R;
+  double2 v[NBT][R];
+#pragma unroll
+  for (int c = 0; c < NBT; ++c) {
+    const int j = tid + c * T;
+#pragma unroll
+    for (int r = 0; r < R; ++r) v[c][r] = buf[j + r * nb];
+  }
+  __syncthreads();
+  const int tstep = L / (Ns * R);
+#pragma unroll
+  for (int c = 0; c < NBT; ++c) {
+    const int j = tid + c * T;
+    const int k = j % Ns;
+#pragma unroll
+    for (int r = 1; r < R; ++r) {
+      const double2 w = tw[k * r * tstep];
+      const double2 xv = v[c][r];
+      v[c][r] = mk(w.x * xv.x - w.y * xv.y, w.x * xv.y + w.y * xv.x);
+    }
+    if constexpr (R == 8) {
+      dft8(v[c]);
+    } else if constexpr (R == 4) {
+      dft4(v[c]);
+    } else {
+      const double2 t = sub(v[c][0], v[c][1]);
+      v[c][0] = add(v[c][0], v[c][1]);
+      v[c][1] = t;
+    }
+    const int base = (j / Ns) * Ns * R + k;
+#pragma unroll
+    for (int r = 0; r < R; ++r) buf[base + r * Ns] = v[c][r];
+  }
+  __syncthreads();
+}
+
+// T = L/8 threads per row FFT; a CTA of blockDim threads transforms blockDim/T rows at a time.
+template <typename S>
+__global__ void __launch_bounds__(256) xform_fft_kernel(const S* __restrict__ in, S* __restrict__ out, XScale sc,
+                                                        int rows, int m0, int L, int dct) {
+  extern __shared__ __align__(16) unsigned char sraw[];
+  const int T = L >= 8 ? L / 8 : 1;
+  const int rpc = blockDim.x / T;
+  double2* tw = reinterpret_cast<double2*>(sraw);  // [L]  exp(-2 pi i k / L)
+  for (int k = threadIdx.x; k < L; k += blockDim.x) {
+    double s, c;
+    sincospi(-2.0 * k / L, &s, &c);
+    tw[k] = mk(c, s);
+  }
+  const int g = threadIdx.x / T, tid = threadIdx.x % T;
+  double2* buf = tw + L + (size_t)g * L;
+  constexpr int RPF = Sc<S>::cplx ? 1 : 2;  // rows per FFT
+  const int nfft = (rows + RPF - 1) / RPF;
+  const int K = L / 2;
+  for (int f0 = blockIdx.x * rpc; f0 < nfft; f0 += gridDim.x * rpc) {
+    const int f = f0 + g;
+    const bool active = g < rpc && f < nfft;
+    const int r0 = f * RPF;
+    const bool two = active && (RPF == 2) && (r0 + 1 < rows);
+    __syncthreads();
+    if (active) {
+      for (int j = tid; j < L; j += T) {
+        int J;
+        double sg = 1.0;
+        if (dct) {
+          J = j < K ? j : L - j;
+        } else if (j == 0 || j == K) {
+          J = -1;
+        } else if (j < K) {
+          J = j - 1;
+        } else {
+          J = L - j - 1;
+          sg = -1.0;
+        }
+        double2 v = mk(0.0, 0.0);
+        if (J >= 0) {
+          if constexpr (Sc<S>::cplx) {
+            const double2 x = in[(size_t)r0 * m0 + J];
+            v = mk(sg * x.x, sg * x.y);
+          } else {
+            const double a = in[(size_t)r0 * m0 + J];
+            const double b = two ? in[(size_t)(r0 + 1) * m0 + J] : 0.0;
+            v = mk(sg * a, sg * b);
+          }
+        }
+        buf[j] = v;
+      }
+    }
+    __syncthreads();
+    int Ns = 1, rem = L;
+    while (rem >= 8) {
+      stockham_stage<8>(buf, tw, L, Ns, tid, T);
+      Ns *= 8;
+      rem /= 8;
+    }
+    if (rem == 4) stockham_stage<4>(buf, tw, L, Ns, tid, T);
+    else if (rem == 2) stockham_stage<2>(buf, tw, L, Ns, tid, T);
+    if (!active) continue;
+    for (int a = tid; a < m0; a += T) {
+      double2 R;
+      if (dct) {  // sum_J cos(pi a J/M) x_J = (DFT[a] + x_0 + (-1)^a x_M) / 2
+        double2 x0, xm;
+        if constexpr (Sc<S>::cplx) {
+          x0 = in[(size_t)r0 * m0];
+          xm = in[(size_t)r0 * m0 + m0 - 1];
+        } else {
+          x0 = mk(in[(size_t)r0 * m0], two ? in[(size_t)(r0 + 1) * m0] : 0.0);
+          xm = mk(in[(size_t)r0 * m0 + m0 - 1], two ? in[(size_t)(r0 + 1) * m0 + m0 - 1] : 0.0);
+        }
+        const double sgn = (a & 1) ? -1.0 : 1.0;
+        const double2 d = buf[a];
+        R = mk(0.5 * (d.x + x0.x + sgn * xm.x), 0.5 * (d.y + x0.y + sgn * xm.y));
+      } else {    // sum_J sin(pi (J+1)(a+1)/K) x_J = (i/2) DFT[a+1]
+        const double2 d = buf[a + 1];
+        R = mk(-0.5 * d.y, 0.5 * d.x);
+      }
+      if constexpr (Sc<S>::cplx) {
+        out[(size_t)r0 * m0 + a] = scale(R, xscale(sc, r0, a, m0));
+      } else {
+        out[(size_t)r0 * m0 + a] = R.x * xscale(sc, r0, a, m0);
+        if (two) out[(size_t)(r0 + 1) * m0 + a] = R.y * xscale(sc, r0 + 1, a, m0);
+      }
+    }
+  }
+}
+
+// Direct O(m0^2)-per-row transform for grids whose n - 1 is not a power of two.
+template <typename S>
+__global__ void __launch_bounds__(256) xform_direct_kernel(const S* __restrict__ in, S* __restrict__ out, XScale sc,
+                                                           int rows, int m0, int dct) {
+  const int a = blockIdx.x * blockDim.x + threadIdx.x;
+  const int r = blockIdx.y;
+  if (a >= m0 || r >= rows) return;
+  const S* row = in + (size_t)r * m0;
+  const long long P = dct ? 2LL * (m0 - 1) : 2LL * (m0 + 1);  // period of the integer argument
+  S acc = Sc<S>::zero();
+  for (int J = 0; J < m0; ++J) {
+    double q;
+    if (dct)
+      q = cospi((double)(((long long)a * J) % P) / (double)(m0 - 1));
+    else
+      q = sinpi((double)(((long long)(a + 1) * (J + 1)) % P) / (double)(m0 + 1));
+    acc = fma_(q, row[J], acc);
+  }
+  out[(size_t)r * m0 + a] = scale(acc, xscale(sc, r, a, m0));
+}
+
+// out[b][x][y] = in[b][y][x]  (32 x 32 tiles through shared memory)
+template <typename S>
+__global__ void __launch_bounds__(256) transpose_kernel(const S* __restrict__ in, S* __restrict__ out, int m) {
+  __shared__ S tile[32][33];
+  const size_t off = (size_t)blockIdx.z * m * m;
+  const int x0 = blockIdx.x * 32, y0 = blockIdx.y * 32;
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    const int y = y0 + r, x = x0 + threadIdx.x;
+    if (y < m && x < m) tile[r][threadIdx.x] = in[off + (size_t)y * m + x];
+  }
+  __syncthreads();
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    const int x = x0 + r, y = y0 + threadIdx.x;
+    if (y < m && x < m) out[off + (size_t)x * m + y] = tile[threadIdx.x][r];
+  }
+}
+
+template <typename S>
+void launch_xform(const helm_plan* P, const S* in, S* out, const double* sig, bool scale2d, int batch,
+                  cudaStream_t st) {
+  HELM_CHECK((const void*)in != (const void*)out, "xform: input and output must not alias");
+  const PlanDev& d = P->dev;
+  const int m0 = d.m0, rows = m0 * batch, dct = P->geo.sommerfeld;
+  XScale sc{sig, nullptr, nullptr, 0.0, 0.0};
+  if (scale2d) sc = XScale{nullptr, d.coarse_lamT, d.coarse_lamM, P->geo.k2, d.coarse_qn};
+  if (d.fft_len) {
+    const int L = d.fft_len;
+    const int T = L / 8;
+    const int threads = std::max(T, std::min(256, std::max(32, L)));
+    const int rpc = threads / T;
+    const size_t smem = (size_t)(L + rpc * L) * sizeof(double2);
+    HELM_CHECK(smem <= 200 * 1024, "coarse FFT row too long for shared memory");
+    static bool attr[2] = {false, false};
+    if (!attr[Sc<S>::cplx]) {
+      HELM_CUDA(cudaFuncSetAttribute(xform_fft_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     200 * 1024));
+      attr[Sc<S>::cplx] = true;
+    }
+    const int nfft = Sc<S>::cplx ? rows : (rows + 1) / 2;
+    const int blocks = std::min((nfft + rpc - 1) / rpc, 148 * 16);
+    xform_fft_kernel<S><<<blocks, threads, smem, st>>>(in, out, sc, rows, m0, L, dct);
+  } else {
+    dim3 grd((m0 + 255) / 256, rows);
+    xform_direct_kernel<S><<<grd, 256, 0, st>>>(in, out, sc, rows, m0, dct);
+  }
+  HELM_LAUNCH_CHECK();
+}
+
+template <typename S>
+void launch_transpose(const S* in, S* out, int m, int batch, cudaStream_t st) {
+  dim3 grd((m + 31) / 32, (m + 31) / 32, batch), blk(32, 8);
+  transpose_kernel<S><<<grd, blk, 0, st>>>(in, out, m);
+  HELM_LAUNCH_CHECK();
+}
+
+#define HELM_INST(S)                                                                                          \
+  template void launch_xform<S>(const helm_plan*, const S*, S*, const double*, bool, int, cudaStream_t);       \
+  template void launch_transpose<S>(const S*, S*, int, int, cudaStream_t);
+HELM_INST(double)
+HELM_INST(double2)
+#undef HELM_INST
+
+}  // namespace helm

@@ -155,38 +155,119 @@ def local_classes(grid: Grid, k: float, boxes) -> LocalClasses:
 
 
 @dataclass
-class CoarseFDM:
+class CoarseFast:
+    """Setup of the fast coarse solver (one-time, host).
+
+    A0 = T0(x)M0 + M0(x)T0 - k^2 M0(x)M0 (y (x) x).  Along x the 1-D pencil is
+    split as T0 = T~ + L_T, M0 = M~ + L_M where (T~, M~) is diagonalised by a
+    fast sine/cosine transform Q (T~ Q = W Q diag(lamT), M~ Q = W Q diag(lamM)):
+    DST-I for Dirichlet (exact, L = 0), DCT-I for Sommerfeld (L_T, L_M live on
+    the 2x2 corner blocks: the Bezier restriction drops its out-of-range taps
+    instead of reflecting them, coarse.py:116-128).  B = T0(x)M~ + M0(x)T~ -
+    k^2 M0(x)M~ is then x-transform + one pentadiagonal solve per x-mode; the
+    corner corrections (4 strip columns) are removed by a Woodbury step whose
+    capacitance matrix is block-diagonal (4x4) in the eigenbasis of the y-pencil.
+    """
+
     m0: int
-    V: np.ndarray
-    lam: np.ndarray
+    transform: int          # 0: DST-I (Dirichlet), 1: DCT-I (Sommerfeld)
+    scale: np.ndarray       # [m0] forward pre-scale sigma_a (Sommerfeld: qnorm/lamM[a]; Dirichlet: qnorm)
+    lamT: np.ndarray        # [m0] eigenvalues of the ideal x-pencil (T~ Q = W Q diag(lamT))
+    lamM: np.ndarray        # [m0]
+    qn: float               # Dirichlet inverse-transform normalisation 2/(m0+1)
+    k2: float
+    shifts: np.ndarray      # [m0] s_a = lamT[a]/lamM[a] - k^2
     t0b: np.ndarray
     m0b: np.ndarray
-    piv: np.ndarray
+    piv: np.ndarray         # band LU of T0 + s_a M0, layout [row][a]
     L: np.ndarray
     U: np.ndarray
+    strip_x: np.ndarray     # [ns] x indices of the corrected columns (ns = 0 or 4)
+    strip_q: np.ndarray     # [m0][ns] Q[strip_x[i], a]
+    cap_left: np.ndarray    # [m0][m0]  V^T M0  (y-pencil eigenbasis, V^T M0 V = I)
+    cap_right: np.ndarray   # [m0][m0]  M0 V
+    cap_mode: np.ndarray    # [m0][ns][ns]  G_b (I + Gamma_b G_b)^{-1}
 
 
-def coarse_fdm(grid: Grid, k: float) -> CoarseFDM:
-    """Partial-FDM data of A0 = T0(x)M0 + M0(x)T0 - k^2 M0(x)M0."""
-    import scipy.sparse as sp
+def _dense_from_bands(b: np.ndarray) -> np.ndarray:
+    m = len(b)
+    A = np.zeros((m, m), dtype=b.dtype)
+    for d in range(-2, 3):
+        i = np.arange(max(0, -d), min(m, m - d))
+        A[i, i + d] = b[i, d + 2]
+    return A
 
-    nu, h = grid.unknowns_per_dim, grid.h
-    e = np.ones(nu)
-    dt = complex if grid.bc == "sommerfeld" else float
-    d0 = np.full(nu, 2.0 / h**2, dtype=dt)
-    w = np.ones(nu)
+
+def coarse_pencil(grid: Grid, k: float):
+    """T0 = P T P^T, M0 = P W P^T (pentadiagonal; A0 = T0(x)M0 + M0(x)T0 - k^2 M0(x)M0)."""
+    T, w = pencil_1d(grid, k)
+    P = bezier_1d(grid, 2)
+    T0 = P @ T @ P.T
+    M0 = P @ (w[:, None] * P.T)
+    return 0.5 * (T0 + T0.T), 0.5 * (M0 + M0.T), P, T, w
+
+
+def coarse_fast(grid: Grid, k: float) -> CoarseFast:
+    """Fast-transform + Woodbury setup of A0^{-1} (replaces SuperLU of A0, coarse.py:154-167)."""
+    T0, M0, P, T, w = coarse_pencil(grid, k)
+    m = len(M0)
+    I = np.arange(m)
     if grid.bc == "sommerfeld":
-        d0[0] = d0[-1] = 1.0 / h**2 - 1j * k / h
-        w[0] = w[-1] = 0.5
-    T = sp.diags([-e[1:] / h**2, d0, -e[1:] / h**2], [-1, 0, 1], format="csr")
-    P = sp.csr_matrix(bezier_1d(grid, 2))
-    T0 = (P @ T @ P.T).toarray()
-    M0 = (P @ sp.diags(w) @ P.T).toarray()
-    T0 = 0.5 * (T0 + T0.T)
-    M0 = 0.5 * (M0 + M0.T)
-    lam, V = _general_pencil_eig(T0, M0)
+        Mx = m - 1
+        Q = np.cos(np.pi * np.outer(I, I) / Mx)
+        c = np.ones(m)
+        c[0] = c[-1] = 2.0
+        qnorm = 2.0 / (Mx * c)            # Q^{-1} W^{-1} = diag(qnorm) Q^T
+        # Pi = P^T + E: the Bezier prolongation of the even (reflected) extension
+        nu = grid.unknowns_per_dim
+        Pi = P.T.copy()
+        Pi[0, 1] += 1.0 / 8.0
+        Pi[nu - 1, m - 2] += 1.0 / 8.0
+        Tt = Pi.T @ T.real @ Pi
+        Mt = Pi.T @ (w[:, None] * Pi)
+        strip = np.array([0, 1, m - 2, m - 1], dtype=np.int32)
+    else:
+        Q = np.sin(np.pi * np.outer(I + 1, I + 1) / (m + 1))
+        qnorm = np.full(m, 2.0 / (m + 1))
+        Tt, Mt = T0.real, M0.real
+        strip = np.zeros(0, dtype=np.int32)
+    Qi = qnorm[:, None] * Q.T                 # Q^{-1} W^{-1}
+    lamT = np.einsum("aj,ja->a", Qi, Tt @ Q).real
+    lamM = np.einsum("aj,ja->a", Qi, Mt @ Q).real
+    if np.any(lamM <= 0):
+        raise SingularMatrixError("coarse mass pencil is not positive definite")
+    shifts = lamT / lamM - k**2
     t0b, m0b = _bands(T0), _bands(M0)
-    shifts = (lam - k**2).astype(np.result_type(lam.dtype, T0.dtype))
-    piv, L, U = band_lu(t0b, m0b, shifts)
     dt = T0.dtype
-    return CoarseFDM(len(M0), V.astype(dt), lam.astype(dt), t0b, m0b.astype(dt), piv, L.astype(dt), U.astype(dt))
+    if grid.bc == "sommerfeld":
+        piv, L, U = band_lu(t0b, m0b.astype(dt), shifts.astype(dt))
+        scale = qnorm / lamM
+    else:  # the Dirichlet pencil is DST-diagonal in y as well: no band solves
+        den = lamT[:, None] * lamM[None, :] + lamM[:, None] * lamT[None, :] - k**2 * np.outer(lamM, lamM)
+        if np.any(np.abs(den) <= 1e-14 * np.abs(den).max()):
+            raise SingularMatrixError("coarse Galerkin matrix is singular (k^2 at a coarse eigenvalue)")
+        piv = np.zeros((0, 0), np.uint8)
+        L = np.zeros((0, 0, 2), dt)
+        U = np.zeros((0, 0, 5), dt)
+        scale = qnorm.copy()
+    ns = len(strip)
+    strip_q = np.ascontiguousarray(Q[strip, :].T)  # [a][i]
+    if ns:
+        LT = (T0 - Tt)[np.ix_(strip, strip)]
+        LM = (M0 - Mt)[np.ix_(strip, strip)]
+        lam, V = _general_pencil_eig(T0, M0)
+        den = lamM[None, :] * lam[:, None] + (lamT - k**2 * lamM)[None, :]  # [b][a]
+        # Gamma_b[i][j] = sum_a Q[x_i,a] (Q^{-1}W^{-1})[a,x_j] / den[b,a]
+        Gam = np.einsum("ai,aj,ba->bij", strip_q, Qi[:, strip], 1.0 / den)
+        G = lam[:, None, None] * LM[None] + (LT - k**2 * LM)[None]
+        K = np.eye(ns)[None] + Gam @ G
+        cap_mode = G @ np.linalg.inv(K)
+        cap_left, cap_right = V.T @ M0, M0 @ V
+    else:
+        cap_mode = np.zeros((m, 0, 0), dt)
+        cap_left = cap_right = np.zeros((0, 0), dt)
+    return CoarseFast(m, 1 if grid.bc == "sommerfeld" else 0, scale, lamT, lamM, float(qnorm[0]), float(k**2), shifts,
+                      t0b,
+                      m0b.astype(dt), piv,
+                      L.astype(dt), U.astype(dt), strip, strip_q, cap_left.astype(dt), cap_right.astype(dt),
+                      cap_mode.astype(dt))

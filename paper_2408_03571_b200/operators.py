@@ -22,7 +22,7 @@ import torch
 
 from . import _lib
 from .discretization import CoarseSpace, Decomposition, Grid, PROBLEMS, build_hocs, extend, partition
-from .fdm_setup import SingularMatrixError, coarse_fdm, local_classes
+from .fdm_setup import SingularMatrixError, coarse_fast, local_classes
 
 __all__ = [
     "HelmholtzOperator",
@@ -179,7 +179,7 @@ def galerkin(cs: CoarseSpace, A) -> CoarseSpace:
     op = _as_operator(A, cs.grid)
     from dataclasses import replace
 
-    return replace(cs, fdm=coarse_fdm(cs.grid, op.k))
+    return replace(cs, fdm=coarse_fast(cs.grid, op.k))
 
 
 class _Plan:
@@ -215,14 +215,23 @@ class _Plan:
             d.box_class, d.class_len = i32(keep["box_class"]), i32(keep["class_len"])
             d.n_classes = len(lc.V)
             d.class_V, d.class_lambda = vp(keep["classV"]), vp(keep["classL"])
-        if cf is not None:  # partial-FDM coarse solver
-            arrays = dict(V=cf.V, lam=cf.lam, t0b=cf.t0b, m0b=cf.m0b, piv=cf.piv, L=cf.L, U=cf.U)
-            for key, v in arrays.items():
-                keep[key] = np.ascontiguousarray(v, dtype=(np.uint8 if key == "piv" else dt))
-            d.coarse_V, d.coarse_lambda = vp(keep["V"]), vp(keep["lam"])
+        if cf is not None:  # fast-transform + Woodbury coarse solver
+            arrays = dict(scale=(cf.scale, np.float64), lamT=(cf.lamT, np.float64), lamM=(cf.lamM, np.float64),
+                          t0b=(cf.t0b, dt), m0b=(cf.m0b, dt), piv=(cf.piv, np.uint8),
+                          L=(cf.L, dt), U=(cf.U, dt), q=(cf.strip_q, np.float64), cl=(cf.cap_left, dt),
+                          cr=(cf.cap_right, dt), cm=(cf.cap_mode, dt))
+            for key, (v, t) in arrays.items():
+                keep[key] = np.ascontiguousarray(v, dtype=t)
+            d.coarse_scale = vp(keep["scale"])
+            d.coarse_lamT, d.coarse_lamM, d.coarse_qn = vp(keep["lamT"]), vp(keep["lamM"]), cf.qn
             d.t0_band, d.m0_band = vp(keep["t0b"]), vp(keep["m0b"])
-            d.band_piv = keep["piv"].ctypes.data_as(ctypes.POINTER(ctypes.c_uint8))
-            d.band_l, d.band_u = vp(keep["L"]), vp(keep["U"])
+            if cplx:
+                d.band_piv = keep["piv"].ctypes.data_as(ctypes.POINTER(ctypes.c_uint8))
+                d.band_l, d.band_u = vp(keep["L"]), vp(keep["U"])
+            d.n_strip = len(cf.strip_x)
+            if d.n_strip:
+                d.strip_q, d.cap_left, d.cap_right = vp(keep["q"]), vp(keep["cl"]), vp(keep["cr"])
+                d.cap_mode = vp(keep["cm"])
         d.refine_steps = int(refine_steps)
         h = ctypes.c_void_p()
         _lib.check(lib.helm_plan_create(ctypes.byref(d), ctypes.byref(h)))
@@ -295,7 +304,7 @@ class SchwarzPreconditioner:
             raise NotImplementedError("the GPU path implements the HOCS coarse space at ratio 2")
         cf = getattr(coarse_space, "fdm", None)
         if cf is None:
-            cf = coarse_fdm(grid, self.A.k)
+            cf = coarse_fast(grid, self.A.k)
         self.coarse_space = CoarseSpace("HOCS", grid, 2, cf)
         self.weights_before_solve = bool(weights_before_solve)
         self.max_batch = int(max_batch)

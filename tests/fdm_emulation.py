@@ -1,7 +1,7 @@
 """numpy emulation of the device FDM algorithms (test helper, CPU only).
 
 Re-implements, statement for statement, what the CUDA kernels K4 (local FDM)
-and K5 (partial FDM + band solves + iterative refinement) compute, so the
+and K5 (fast x-transform + band solves + Woodbury strip correction + iterative refinement) compute, so the
 host setup (eigen-pairs, band LU) can be validated against the oracle's
 SuperLU solves without a GPU.
 """
@@ -56,18 +56,43 @@ def a0_apply(cf, k, Y):
     return T0 @ Y @ M0.T + M0 @ Y @ T0.T - k**2 * (M0 @ Y @ M0.T)
 
 
+def x_transform(cf, X):
+    """Raw DST-I / DCT-I sums along x (rows of X): out[y, a] = sum_J Q[J, a] X[y, J]."""
+    m = cf.m0
+    I = np.arange(m)
+    if cf.transform == 1:
+        Q = np.cos(np.pi * np.outer(I, I) / (m - 1))
+    else:
+        Q = np.sin(np.pi * np.outer(I + 1, I + 1) / (m + 1))
+    return X @ Q
+
+
+def fast_solve(cf, R):
+    """One pass of the device coarse solve (coarse.cu): x-transform, band solves + Woodbury strip
+    step (Sommerfeld) or the separable 2-D DST scaling (Dirichlet), inverse transform."""
+    Fh = x_transform(cf, R) * cf.scale[None, :]
+    if cf.transform == 0:
+        lT, lM = cf.lamT, cf.lamM
+        den = lT[:, None] * lM[None, :] + lM[:, None] * lT[None, :] - cf.k2 * np.outer(lM, lM)  # [ky][kx]
+        G = x_transform(cf, Fh.T).T * cf.qn / den
+        return x_transform(cf, x_transform(cf, G.T).T)
+    if len(cf.strip_x):
+        Y0h = band_solve(cf.piv, cf.L, cf.U, Fh)
+        Y0S = Y0h @ cf.strip_q                          # strip columns of B^{-1} R
+        yh = cf.cap_left @ Y0S                          # y-eigen coordinates
+        ch = np.einsum("bij,bj->bi", cf.cap_mode, yh)   # per-mode 4x4
+        cS = cf.cap_right @ ch
+        Fh = Fh - (cS @ cf.strip_q.T) * cf.scale[None, :]
+    Yh = band_solve(cf.piv, cf.L, cf.U, Fh)
+    return x_transform(cf, Yh)
+
+
 def coarse_solve(cf, k, c, refine=1):
     m = cf.m0
     C = c.reshape(m, m)
-
-    def fdm(R):
-        G = R @ cf.V
-        H = band_solve(cf.piv, cf.L, cf.U, G)
-        return H @ cf.V.T
-
-    Y = fdm(C)
+    Y = fast_solve(cf, C)
     for _ in range(refine):
-        Y = Y + fdm(C - a0_apply(cf, k, Y))
+        Y = Y + fast_solve(cf, C - a0_apply(cf, k, Y))
     return Y.ravel()
 
 

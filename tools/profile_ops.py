@@ -31,6 +31,9 @@ def main():
     ap.add_argument("--p", type=int, default=64)
     ap.add_argument("--batch", type=int, default=32)
     ap.add_argument("--gmres", type=int, default=30)
+    ap.add_argument("--only", default="", help="comma-separated op names to time (default: all)")
+    ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--batches", default="1,32")
     a = ap.parse_args()
     t = time.time()
     grid = hb.Grid(a.n, "sommerfeld")
@@ -42,7 +45,7 @@ def main():
     N, N0 = M.N, M.N0
     p, lib = M.plan, M.plan.lib
     st = lambda: torch.cuda.current_stream().cuda_stream  # noqa: E731
-    for B in (1, a.batch):
+    for B in [int(v) for v in a.batches.split(",")]:
         X = torch.randn(B, N, dtype=torch.complex128, device="cuda")
         Y = torch.empty_like(X)
         C = torch.randn(B, N0, dtype=torch.complex128, device="cuda")
@@ -56,7 +59,9 @@ def main():
             "M^-1": lambda: lib.helm_apply_M(p.handle, p.ws, X.data_ptr(), Y.data_ptr(), B, st()),
         }
         for name, fn in ops.items():
-            ms = timeit(fn)
+            if a.only and name not in a.only.split(","):
+                continue
+            ms = timeit(fn, reps=a.reps, warm=min(2, a.reps))
             print(f"B={B:3d} {name:14s} {ms:9.3f} ms  ({ms / B:8.3f} ms/vec)", flush=True)
     if a.gmres:
         rep = hb.gmres(prob.A, M, prob.f, hb.GmresConfig(rtol=1e-6, max_iter=a.gmres))
