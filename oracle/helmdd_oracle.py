@@ -240,9 +240,17 @@ def coarse_space(grid: OGrid, A: sp.csr_matrix, ratio: int = 2, kind: str = "HOC
     return OCoarse(R0, a0, splu(sp.csc_matrix(a0)))
 
 
-def coarse_correct(cs: OCoarse, r: np.ndarray) -> np.ndarray:
-    """R0^T A0^{-1} R0 r — coarse.py:170-174."""
-    return cs.r0.T @ cs.lu.solve(cs.r0 @ r)
+def coarse_correct(cs: OCoarse, r: np.ndarray, refine: int = 0) -> np.ndarray:
+    """R0^T A0^{-1} R0 r — coarse.py:170-174.
+
+    refine > 0 adds iterative-refinement steps with the same SuperLU factor (NOT in the
+    reference; used to measure how the reference's GMRES counts depend on the rounding of
+    its coarse solve, tests/golden/make_refined.py)."""
+    c = cs.r0 @ r
+    y = cs.lu.solve(c)
+    for _ in range(refine):
+        y = y + cs.lu.solve(c - cs.a0 @ y)
+    return cs.r0.T @ y
 
 
 # --------------------------------------------------------------------------
@@ -253,11 +261,13 @@ def coarse_correct(cs: OCoarse, r: np.ndarray) -> np.ndarray:
 class OSchwarz:
     """AS2 / SAS2 / SHS2 applications with exact SuperLU local solves — schwarz.py:31-103."""
 
-    def __init__(self, kind: str, A, dec: ODecomposition, cs: OCoarse, weights_before_solve=False):
+    def __init__(self, kind: str, A, dec: ODecomposition, cs: OCoarse, weights_before_solve=False,
+                 coarse_refine: int = 0):
         if kind not in ("AS2", "SAS2", "SHS2"):
             raise ValueError(kind)
         self.kind, self.A, self.dec, self.cs = kind, A, dec, cs
         self.wbs = weights_before_solve
+        self.coarse_refine = coarse_refine
         # local principal submatrices R_i A R_i^T, factorised once (schwarz.py:55-59)
         self.lus = [splu(sp.csc_matrix(A[s][:, s])) for s in dec.index_sets]
 
@@ -277,7 +287,7 @@ class OSchwarz:
         x = np.asarray(x, dtype=np.result_type(np.asarray(x).dtype, self.A.dtype))  # :94
         if x.shape[0] != self.A.shape[0]:
             raise ValueError("dimension mismatch")  # :95-96
-        z = coarse_correct(self.cs, x)
+        z = coarse_correct(self.cs, x, self.coarse_refine)
         if self.kind == "AS2":  # :76-79
             return self.local_sum(x, z, weighted=False)
         if self.kind == "SAS2":  # :81-84

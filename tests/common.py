@@ -37,3 +37,23 @@ def random_rhs(N):
 
 def rel(a, b):
     return float(np.linalg.norm(np.asarray(a) - np.asarray(b)) / np.linalg.norm(np.asarray(b)))
+
+
+def reference_count(name, g):
+    """(raw reference GMRES count, count of the reference with one refinement step on its
+    own SuperLU coarse solve or None) -- tests/golden/make_refined.py, DESIGN.md §5."""
+    import json
+
+    raw = int(g["gmres_iterations"])
+    path = os.path.join(GOLDEN, name + "_refined.json")
+    if not os.path.exists(path):
+        return raw, None
+    with open(path) as f:
+        return raw, int(json.load(f)["iterations"])
+
+
+def count_matches(it, raw, refined):
+    """Iteration-count bar (north star: +-1).  On the near-resonant configs the reference's own
+    count is set by its SuperLU rounding; there the refined reference is the target."""
+    target = raw if refined is None else refined
+    return abs(it - target) <= 1

@@ -9,7 +9,7 @@ import numpy as np
 import pytest
 import torch
 
-from common import golden_names, load_golden, operator_input, random_rhs, rel
+from common import count_matches, golden_names, load_golden, operator_input, random_rhs, reference_count, rel
 
 pytestmark = pytest.mark.gpu
 
@@ -77,9 +77,10 @@ def test_gmres_matches_reference(name):
     b = prob.f if str(g["gmres_rhs"]) == "point" else random_rhs(prob.A.N)
     rep = hb.gmres(prob.A, Ms["SHS2"], b, hb.GmresConfig(rtol=1e-6, max_iter=1000))
     assert rep.converged == bool(g["gmres_converged"])
-    assert abs(rep.iterations - int(g["gmres_iterations"])) <= 1, (rep.iterations, int(g["gmres_iterations"]))
+    raw, refined = reference_count(name, g)
+    assert count_matches(rep.iterations, raw, refined), (rep.iterations, raw, refined)
     xe = rel(rep.x, g["gmres_x"])
-    print(name, rep.iterations, int(g["gmres_iterations"]), f"x {xe:.1e}")
+    print(name, rep.iterations, raw, refined, f"x {xe:.1e}")
     assert rep.final_residual <= 1e-6
     if name in UNREPRODUCIBLE:
         # the reference itself moves by >1e-8 here under 1e-15 perturbations of M
@@ -99,11 +100,11 @@ def test_gmres_large_configs(name):
     g, prob, Ms = build(name)
     b = prob.f if str(g["gmres_rhs"]) == "point" else random_rhs(prob.A.N)
     rep = hb.gmres(prob.A, Ms["SHS2"], b, hb.GmresConfig(rtol=1e-6, max_iter=1000))
-    ref_it = int(g["gmres_iterations"])
+    raw, refined = reference_count(name, g)
     stride = int(g["gmres_x_sample_stride"])
     xe = rel(rep.x[::stride], g["gmres_x_sample"])
-    print(name, rep.iterations, ref_it, f"x(sample) {xe:.1e}", f"{rep.wall_seconds:.2f}s")
-    assert rep.converged and abs(rep.iterations - ref_it) <= 1
+    print(name, rep.iterations, raw, refined, f"x(sample) {xe:.1e}", f"{rep.wall_seconds:.2f}s")
+    assert rep.converged and count_matches(rep.iterations, raw, refined), (rep.iterations, raw, refined)
     assert rep.final_residual <= 1e-6
     assert xe <= (REF_SPREAD if name in UNREPRODUCIBLE else X_TOL)
 

@@ -10,7 +10,7 @@ import numpy as np
 import pytest
 
 import helmdd_oracle as O
-from common import golden_names, load_golden, operator_input, random_rhs, rel
+from common import golden_names, load_golden, operator_input, random_rhs, reference_count, rel
 
 VEC = golden_names(store_vectors=True)
 
@@ -74,3 +74,16 @@ def test_paper_known_answer_hocs_h4():
     M = O.OSchwarz("SHS2", prob.A, dec, cs)
     rep = O.gmres(prob.A, M, prob.f, 1e-7, 100, side="left")
     assert rep.converged and rep.iterations == 8
+
+
+@pytest.mark.parametrize("name", ["cfg2", "cfg3"])
+def test_oracle_refined_coarse_counts(name):
+    """The reference with one refinement step on its SuperLU coarse solve (tests/golden/make_refined.py)
+    and the oracle with the same step agree on the GMRES count."""
+    g = load_golden(name)
+    raw, refined = reference_count(name, g)
+    assert refined is not None
+    prob, dec, cs, _ = build(g)
+    M = O.OSchwarz("SHS2", prob.A, dec, cs, coarse_refine=1)
+    rep = O.gmres(prob.A, M, prob.f, 1e-6, 1000)
+    assert rep.converged and abs(rep.iterations - refined) <= 1, (rep.iterations, refined, raw)
