@@ -3,20 +3,20 @@
 //
 //   (T0 + s_a M0) out[b][:, a] = in[b][:, a] - sig_a * sum_i corr[y][b*4+i] q[a][i]
 //
-// One warp owns 32 consecutive modes a (coalesced: the factors and vectors are
-// stored [row][a]) and RB right-hand sides.  The recurrence is sequential in the
-// row index, so the factors (int pivot, two multipliers, five U entries) and the
-// right-hand-side rows are streamed into shared memory with cp.async in chunks of
-// BR rows, BST chunks in flight, which hides the HBM latency behind the FP64
-// recurrence instead of exposing it once per row.  The forward sweep writes the
-// eliminated right-hand side to `out`; the backward sweep streams it back with U.
+// A CTA owns 32 consecutive modes a (lane = mode: the factors and the vectors are
+// stored [row][a], so every access is a coalesced 512-byte row segment) and NW*RB
+// right-hand sides: warp w carries RB independent recurrences per lane, which gives
+// the sequential row recurrence instruction-level parallelism and shares one read of
+// the factors among NW*RB right-hand sides.  Factors (int pivot, two multipliers,
+// five U entries) and right-hand-side rows stream through shared memory with
+// cp.async in chunks of R rows, ST chunks in flight, so HBM latency hides behind
+// the FP64 recurrence.  The forward sweep writes the eliminated right-hand side to
+// `out`; the backward sweep streams it back with U.
 #include "ops.cuh"
 
 namespace helm {
 
-constexpr int BW = 32;   // modes per CTA (one warp)
-constexpr int BR = 8;    // rows per chunk
-constexpr int BST = 3;   // chunks in flight
+constexpr int BW = 32;  // modes per CTA
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool pred) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
@@ -33,86 +33,93 @@ template <int N> __device__ __forceinline__ void cp_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
 
-template <int RB>
+template <int RB, int NW, int R>
 struct BandFwdStage {
-  double2 L[BR][BW][2];
-  int piv[BR][BW];
-  double2 rhs[RB][BR][BW];
-  double2 corr[RB][BR][4];
+  double2 L[R][BW][2];
+  int piv[R][BW];
+  double2 rhs[NW][RB][R][BW];
+  double2 corr[NW][RB][R][4];
 };
-template <int RB>
+template <int RB, int NW, int R>
 struct BandBwdStage {
-  double2 U[BR][BW][5];
-  double2 v[RB][BR][BW];
+  double2 U[R][BW][5];
+  double2 v[NW][RB][R][BW];
 };
-template <int RB>
+template <int RB, int NW, int R, int ST>
 constexpr size_t band_smem_bytes() {
-  return BST * (sizeof(BandFwdStage<RB>) > sizeof(BandBwdStage<RB>) ? sizeof(BandFwdStage<RB>)
-                                                                      : sizeof(BandBwdStage<RB>));
+  return ST * (sizeof(BandFwdStage<RB, NW, R>) > sizeof(BandBwdStage<RB, NW, R>) ? sizeof(BandFwdStage<RB, NW, R>)
+                                                                                  : sizeof(BandBwdStage<RB, NW, R>));
 }
 
-template <int RB>
-__global__ void __launch_bounds__(BW) band_solve_kernel(const double2* __restrict__ in, double2* __restrict__ out,
-                                                        const int* __restrict__ piv, const double2* __restrict__ L,
-                                                        const double2* __restrict__ U, int m0, int batch,
-                                                        const double2* __restrict__ corr,
-                                                        const double* __restrict__ q,
-                                                        const double* __restrict__ sig, int ldc) {
+template <int RB, int NW, int R, int ST>
+__global__ void __launch_bounds__(BW* NW) band_solve_kernel(const double2* __restrict__ in, double2* __restrict__ out,
+                                                            const int* __restrict__ piv,
+                                                            const double2* __restrict__ L,
+                                                            const double2* __restrict__ U, int m0, int batch,
+                                                            const double2* __restrict__ corr,
+                                                            const double* __restrict__ q,
+                                                            const double* __restrict__ sig, int ldc) {
   extern __shared__ __align__(16) unsigned char sraw[];
-  const int t = threadIdx.x;
-  const int a = blockIdx.x * BW + t;
+  const int t = threadIdx.x & (BW - 1), w = threadIdx.x / BW;
+  const int a0 = blockIdx.x * BW;
+  const int a = a0 + t;
   const bool va = a < m0;
-  const int ac = va ? a : m0 - 1;  // clamped (valid) address for predicated-off copies
-  const int b0 = blockIdx.y * RB;
+  const int b0 = blockIdx.y * (RB * NW) + w * RB;  // this warp's first right-hand side
   const size_t N0 = (size_t)m0 * m0;
-  const int nch = (m0 + BR - 1) / BR;
+  const int nch = (m0 + R - 1) / R;
   double qa[4] = {0.0, 0.0, 0.0, 0.0};
   double sa = 0.0;
   if (corr && va) {
     for (int i = 0; i < 4; ++i) qa[i] = q[(size_t)a * 4 + i];
     sa = sig[a];
   }
-
-  // ---------------- forward elimination ----------------
-  BandFwdStage<RB>* fs = reinterpret_cast<BandFwdStage<RB>*>(sraw);
-  auto issue_fwd = [&](int c) {
-    BandFwdStage<RB>& S = fs[c % BST];
-    for (int rr = 0; rr < BR; ++rr) {
-      const int j = c * BR + rr;
-      const bool vj = va && j < m0;
-      const size_t f = (size_t)(j < m0 ? j : m0 - 1) * m0 + ac;
-      cp_async16(&S.L[rr][t][0], L + 2 * f, vj);
-      cp_async16(&S.L[rr][t][1], L + 2 * f + 1, vj);
-      cp_async4(&S.piv[rr][t], piv + f, vj);
-      const int jr = j + 3;  // the forward sweep consumes right-hand-side row j+3 at step j
-      const size_t fr = (size_t)(jr < m0 ? jr : m0 - 1) * m0 + ac;
-#pragma unroll
-      for (int r = 0; r < RB; ++r) {
-        const int b = b0 + r < batch ? b0 + r : batch - 1;
-        cp_async16(&S.rhs[r][rr][t], in + (size_t)b * N0 + fr, va && jr < m0 && b0 + r < batch);
-      }
-      if (corr && t < 4 * RB) {
-        const int r = t >> 2, i = t & 3;
-        const int b = b0 + r < batch ? b0 + r : batch - 1;
-        const size_t jc = jr < m0 ? jr : m0 - 1;
-        cp_async16(&S.corr[r][rr][i], corr + jc * ldc + (size_t)b * 4 + i, jr < m0 && b0 + r < batch);
-      }
-    }
-    cp_commit();
-  };
   auto corrected = [&](double2 v, const double2* c4) {
     double2 c = mk(0.0, 0.0);
 #pragma unroll
     for (int i = 0; i < 4; ++i) c = fma_(qa[i], c4[i], c);
     return sub(v, scale(c, sa));
   };
+
+  // ---------------- forward elimination ----------------
+  using FS = BandFwdStage<RB, NW, R>;
+  FS* fs = reinterpret_cast<FS*>(sraw);
+  auto issue_fwd = [&](int c) {
+    FS& S = fs[c % ST];
+    // factors: shared by the CTA's warps; warp w copies rows w, w + NW, ... (lane = mode)
+    for (int rr = w; rr < R; rr += NW) {
+      const int j = c * R + rr;
+      const bool ok = va && j < m0;
+      const size_t f = (size_t)(j < m0 ? j : 0) * m0 + (va ? a : 0);
+      cp_async16(&S.L[rr][t][0], L + 2 * f, ok);
+      cp_async16(&S.L[rr][t][1], L + 2 * f + 1, ok);
+      cp_async4(&S.piv[rr][t], piv + f, ok);
+    }
+    // this warp's right-hand-side rows (the forward sweep consumes row j+3 at step j)
+    for (int rr = 0; rr < R; ++rr) {
+      const int jr = c * R + rr + 3;
+      const size_t fr = (size_t)(jr < m0 ? jr : 0) * m0 + (va ? a : 0);
+#pragma unroll
+      for (int r = 0; r < RB; ++r) {
+        const bool okb = b0 + r < batch;
+        cp_async16(&S.rhs[w][r][rr][t], in + (size_t)(okb ? b0 + r : 0) * N0 + fr, va && jr < m0 && okb);
+      }
+      if (corr && t < 4 * RB) {
+        const int r = t >> 2, i = t & 3;
+        const bool okb = b0 + r < batch;
+        const size_t jc = jr < m0 ? jr : 0;
+        cp_async16(&S.corr[w][r][rr][i], corr + jc * ldc + (size_t)(okb ? b0 + r : 0) * 4 + i, jr < m0 && okb);
+      }
+    }
+    cp_commit();
+  };
   double2 r0[RB], r1[RB], r2[RB];
 #pragma unroll
   for (int r = 0; r < RB; ++r) {
     const int b = b0 + r;
     const bool ok = va && b < batch;
-    const double2* col = in + (size_t)(ok ? b : 0) * N0 + ac;
+    const double2* col = in + (size_t)(ok ? b : 0) * N0 + (va ? a : 0);
     double2 c4[4];
+    double2 v3[3];
     for (int jj = 0; jj < 3; ++jj) {
       double2 v = mk(0.0, 0.0);
       if (ok && jj < m0) {
@@ -122,22 +129,25 @@ __global__ void __launch_bounds__(BW) band_solve_kernel(const double2* __restric
           v = corrected(v, c4);
         }
       }
-      (jj == 0 ? r0[r] : jj == 1 ? r1[r] : r2[r]) = v;
+      v3[jj] = v;
     }
+    r0[r] = v3[0];
+    r1[r] = v3[1];
+    r2[r] = v3[2];
   }
-  for (int c = 0; c < BST - 1; ++c) {
+  for (int c = 0; c < ST - 1; ++c) {
     if (c < nch) issue_fwd(c);
     else cp_commit();
   }
   for (int c = 0; c < nch; ++c) {
-    cp_wait<BST - 2>();
-    __syncwarp();
-    if (c + BST - 1 < nch) issue_fwd(c + BST - 1);
+    cp_wait<ST - 2>();
+    __syncthreads();
+    if (c + ST - 1 < nch) issue_fwd(c + ST - 1);
     else cp_commit();
-    const BandFwdStage<RB>& S = fs[c % BST];
-    for (int rr = 0; rr < BR; ++rr) {
-      const int j = c * BR + rr;
-      if (j >= m0) break;
+    const FS& S = fs[c % ST];
+    const int rows = min(R, m0 - c * R);
+    for (int rr = 0; rr < rows; ++rr) {
+      const int j = c * R + rr;
       const int pv = S.piv[rr][t];
       const double2 l0 = S.L[rr][t][0], l1 = S.L[rr][t][1];
 #pragma unroll
@@ -148,8 +158,8 @@ __global__ void __launch_bounds__(BW) band_solve_kernel(const double2* __restric
         x1 = fms_(l0, x0, x1);
         x2 = fms_(l1, x0, x2);
         if (va && b0 + r < batch) out[(size_t)(b0 + r) * N0 + (size_t)j * m0 + a] = x0;
-        double2 nx = S.rhs[r][rr][t];
-        if (corr) nx = corrected(nx, S.corr[r][rr]);
+        double2 nx = S.rhs[w][r][rr][t];
+        if (corr) nx = corrected(nx, S.corr[w][r][rr]);
         r0[r] = x1;
         r1[r] = x2;
         r2[r] = nx;
@@ -157,28 +167,33 @@ __global__ void __launch_bounds__(BW) band_solve_kernel(const double2* __restric
     }
   }
   cp_wait<0>();
-  __syncwarp();
+  __syncthreads();
   __threadfence();  // the backward sweep re-reads `out` through cp.async
 
   // ---------------- backward substitution ----------------
-  BandBwdStage<RB>* bs = reinterpret_cast<BandBwdStage<RB>*>(sraw);
+  using BS = BandBwdStage<RB, NW, R>;
+  BS* bs = reinterpret_cast<BS*>(sraw);
   auto issue_bwd = [&](int c) {
-    BandBwdStage<RB>& S = bs[c % BST];
-    for (int rr = 0; rr < BR; ++rr) {
-      const int j = m0 - 1 - (c * BR + rr);
-      const bool vj = va && j >= 0;
-      const size_t f = (size_t)(j >= 0 ? j : 0) * m0 + ac;
+    BS& S = bs[c % ST];
+    for (int rr = w; rr < R; rr += NW) {
+      const int j = m0 - 1 - (c * R + rr);
+      const bool ok = va && j >= 0;
+      const double2* u = U + 5 * ((size_t)(j >= 0 ? j : 0) * m0 + (va ? a : 0));
 #pragma unroll
-      for (int e = 0; e < 5; ++e) cp_async16(&S.U[rr][t][e], U + 5 * f + e, vj);
+      for (int e = 0; e < 5; ++e) cp_async16(&S.U[rr][t][e], u + e, ok);
+    }
+    for (int rr = 0; rr < R; ++rr) {
+      const int j = m0 - 1 - (c * R + rr);
+      const size_t f = (size_t)(j >= 0 ? j : 0) * m0 + (va ? a : 0);
 #pragma unroll
       for (int r = 0; r < RB; ++r) {
-        const int b = b0 + r < batch ? b0 + r : batch - 1;
-        cp_async16(&S.v[r][rr][t], out + (size_t)b * N0 + f, vj && b0 + r < batch);
+        const bool okb = b0 + r < batch;
+        cp_async16(&S.v[w][r][rr][t], out + (size_t)(okb ? b0 + r : 0) * N0 + f, va && j >= 0 && okb);
       }
     }
     cp_commit();
   };
-  for (int c = 0; c < BST - 1; ++c) {
+  for (int c = 0; c < ST - 1; ++c) {
     if (c < nch) issue_bwd(c);
     else cp_commit();
   }
@@ -186,19 +201,19 @@ __global__ void __launch_bounds__(BW) band_solve_kernel(const double2* __restric
 #pragma unroll
   for (int r = 0; r < RB; ++r) y1[r] = y2[r] = y3[r] = y4[r] = mk(0.0, 0.0);
   for (int c = 0; c < nch; ++c) {
-    cp_wait<BST - 2>();
-    __syncwarp();
-    if (c + BST - 1 < nch) issue_bwd(c + BST - 1);
+    cp_wait<ST - 2>();
+    __syncthreads();
+    if (c + ST - 1 < nch) issue_bwd(c + ST - 1);
     else cp_commit();
-    const BandBwdStage<RB>& S = bs[c % BST];
-    for (int rr = 0; rr < BR; ++rr) {
-      const int j = m0 - 1 - (c * BR + rr);
-      if (j < 0) break;
+    const BS& S = bs[c % ST];
+    const int rows = min(R, m0 - c * R);
+    for (int rr = 0; rr < rows; ++rr) {
+      const int j = m0 - 1 - (c * R + rr);
       const double2 u0 = S.U[rr][t][0], u1 = S.U[rr][t][1], u2 = S.U[rr][t][2], u3 = S.U[rr][t][3],
                     u4 = S.U[rr][t][4];
 #pragma unroll
       for (int r = 0; r < RB; ++r) {
-        double2 v = S.v[r][rr][t];
+        double2 v = S.v[w][r][rr][t];
         v = fms_(u1, y1[r], v);
         v = fms_(u2, y2[r], v);
         v = fms_(u3, y3[r], v);
@@ -215,20 +230,22 @@ __global__ void __launch_bounds__(BW) band_solve_kernel(const double2* __restric
   cp_wait<0>();
 }
 
-template <int RB>
+template <int RB, int NW, int R, int ST>
 static void band_launch(const helm_plan* P, const double2* in, double2* out, const double2* corr, int batch,
                         cudaStream_t st) {
   const PlanDev& d = P->dev;
-  constexpr size_t smem = band_smem_bytes<RB>();
+  constexpr size_t smem = band_smem_bytes<RB, NW, R, ST>();
+  static_assert(smem <= 227 * 1024, "band-solve stages exceed shared memory");
   static bool attr = false;
   if (!attr) {
-    HELM_CUDA(cudaFuncSetAttribute(band_solve_kernel<RB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    HELM_CUDA(cudaFuncSetAttribute(band_solve_kernel<RB, NW, R, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)smem));
     attr = true;
   }
-  dim3 grd((d.m0 + BW - 1) / BW, (batch + RB - 1) / RB);
-  band_solve_kernel<RB><<<grd, BW, smem, st>>>(in, out, d.band_piv, (const double2*)d.band_l,
-                                               (const double2*)d.band_u, d.m0, batch, corr, d.strip_q,
-                                               d.coarse_scale, batch * 4);
+  dim3 grd((d.m0 + BW - 1) / BW, (batch + RB * NW - 1) / (RB * NW));
+  band_solve_kernel<RB, NW, R, ST><<<grd, BW * NW, smem, st>>>(in, out, d.band_piv, (const double2*)d.band_l,
+                                                               (const double2*)d.band_u, d.m0, batch, corr,
+                                                               d.strip_q, d.coarse_scale, batch * 4);
   HELM_LAUNCH_CHECK();
 }
 
@@ -237,11 +254,11 @@ void launch_band_solve(const helm_plan* P, const double2* in, double2* out, cons
   HELM_CHECK(P->dev.band_piv != nullptr, "plan has no band factors");
   HELM_CHECK((const void*)in != (const void*)out, "band solve: input and output must not alias");
   if (batch == 1)
-    band_launch<1>(P, in, out, corr, batch, st);
-  else if (batch == 2)
-    band_launch<2>(P, in, out, corr, batch, st);
+    band_launch<1, 1, 8, 4>(P, in, out, corr, batch, st);  // latency-bound recurrence
+  else if (batch <= 4)
+    band_launch<2, 2, 8, 3>(P, in, out, corr, batch, st);
   else
-    band_launch<4>(P, in, out, corr, batch, st);
+    band_launch<1, 8, 8, 3>(P, in, out, corr, batch, st);  // 8 warps (8 right-hand sides) share each factor read
 }
 
 }  // namespace helm

@@ -241,6 +241,14 @@ static void build_plan(const helm_desc* d, helm_plan* P) {
     dv.m0 = (int)m0;
     const int L = d->n - 1;
     dv.fft_len = (L >= 8 && (L & (L - 1)) == 0 && L <= 2048) ? L : 0;  // else: direct transform
+    if (dv.fft_len) {
+      std::vector<double2> tw(L);
+      for (int q = 0; q < L; ++q) {  // exact octant reduction keeps the table symmetric
+        const long double ang = -2.0L * 3.14159265358979323846264338327950288L * q / L;
+        tw[q] = make_double2((double)cosl(ang), (double)sinl(ang));
+      }
+      dv.twiddle = upload<double2>(tw.data(), tw.size());
+    }
     dv.coarse_scale = upload<double>(d->coarse_scale, m0);
     dv.t0_band = upload_bytes(d->t0_band, m0 * 5 * P->elem);
     dv.m0_band = upload_bytes(d->m0_band, m0 * 5 * P->elem);
@@ -362,7 +370,7 @@ static void free_plan(helm_plan* P) {
   PlanDev& dv = P->dev;
   void* ptrs[] = {dv.box_start, dv.box_len, dv.box_class, dv.class_len, dv.class_off_V, dv.class_off_lam,
                   dv.class_V, dv.class_lambda, dv.class_real, dv.class_Vr, dv.box_rr, dv.box_mix, dv.node_first_box, dv.node_mult, dv.node_band, dv.band_node,
-                  dv.coarse_scale, dv.coarse_lamT, dv.coarse_lamM, dv.t0_band, dv.m0_band, dv.band_piv, dv.band_l, dv.band_u, dv.strip_q,
+                  dv.coarse_scale, dv.twiddle, dv.coarse_lamT, dv.coarse_lamM, dv.t0_band, dv.m0_band, dv.band_piv, dv.band_l, dv.band_u, dv.strip_q,
                   dv.cap_left, dv.cap_right, dv.cap_mode};
   for (void* q : ptrs)
     if (q) cudaFree(q);

@@ -160,6 +160,7 @@ struct PlanDev {
   // coarse (fast x-transform + band solves + Woodbury strips)
   int m0;
   int fft_len;         // n - 1 when it is a power of two, else 0 (direct transform)
+  double2* twiddle;    // [fft_len] exp(-2 pi i k / fft_len)
   double* coarse_scale;
   double* coarse_lamT;  // Dirichlet 2-D DST scaling
   double* coarse_lamM;

@@ -69,126 +69,133 @@ __device__ __forceinline__ void dft4(double2 v[4]) {
   v[3] = mk(b.x - d.y, b.y + d.x);  // b + i d
 }
 
-// One in-place Stockham stage of radix R over a row of length L held in smem.
-// Butterfly j: inputs buf[j + r L/R], twiddle W_{Ns R}^{(j mod Ns) r}, outputs at
-// (j / Ns) Ns R + (j mod Ns) + r Ns.  All reads complete (barrier) before any write.
-template <int R>
-__device__ __forceinline__ void stockham_stage(double2* buf, const double2* tw, int L, int Ns, int tid, int T) {
-  const int nb = L / R;           // = (8 / R) T butterflies: each thread owns NBT of them
+// Padded shared-memory index: one spare slot every 8 and every 64 elements, so the
+// strided Stockham stores of the first stages (stride 8 and 64 double2) hit
+// distinct bank groups.
+__device__ __forceinline__ int pidx(int i) { return i + (i >> 3) + (i >> 6); }
+__host__ __device__ constexpr int padded_len(int L) { return L + L / 8 + L / 64 + 1; }
+
+// One Stockham stage of radix R over a row of length L (T threads, NBT = 8/R butterflies
+// each).  Butterfly j: inputs X[j + r L/R], twiddles W^r with W = W_{Ns R}^{j mod Ns}
+// (plan-owned table in L1), outputs at (j / Ns) Ns R + (j mod Ns) + r Ns.
+// FIRST: inputs come from `load(i)` (global); LAST: outputs go to `store(i, v)` (global);
+// otherwise through the padded shared buffer, in place across a barrier.
+template <int R, bool FIRST, bool LAST, typename LD, typename STO>
+__device__ __forceinline__ void stockham_stage(double2* buf, const double2* __restrict__ tw, int L, int Ns, int tid,
+                                               int T, LD load, STO store) {
+  const int nb = L / R;
   constexpr int NBT = 8 / R;
   double2 v[NBT][R];
 #pragma unroll
   for (int c = 0; c < NBT; ++c) {
     const int j = tid + c * T;
 #pragma unroll
-    for (int r = 0; r < R; ++r) v[c][r] = buf[j + r * nb];
+    for (int r = 0; r < R; ++r) v[c][r] = FIRST ? load(j + r * nb) : buf[pidx(j + r * nb)];
   }
-  __syncthreads();
+  if (!FIRST) __syncthreads();
   const int tstep = L / (Ns * R);
 #pragma unroll
   for (int c = 0; c < NBT; ++c) {
     const int j = tid + c * T;
     const int k = j % Ns;
+    if (!FIRST) {  // Ns == 1 on the first stage: all twiddles are 1
 #pragma unroll
-    for (int r = 1; r < R; ++r) {
-      const double2 w = tw[k * r * tstep];
-      const double2 xv = v[c][r];
-      v[c][r] = mk(w.x * xv.x - w.y * xv.y, w.x * xv.y + w.y * xv.x);
+      for (int r = 1; r < R; ++r) {  // independent L1-resident table reads, no dependency chain
+        const double2 w = tw[k * r * tstep];
+        const double2 xv = v[c][r];
+        v[c][r] = mk(w.x * xv.x - w.y * xv.y, w.x * xv.y + w.y * xv.x);
+      }
     }
     if constexpr (R == 8) {
       dft8(v[c]);
     } else if constexpr (R == 4) {
       dft4(v[c]);
     } else {
-      const double2 t = sub(v[c][0], v[c][1]);
+      const double2 t2 = sub(v[c][0], v[c][1]);
       v[c][0] = add(v[c][0], v[c][1]);
-      v[c][1] = t;
+      v[c][1] = t2;
     }
     const int base = (j / Ns) * Ns * R + k;
 #pragma unroll
-    for (int r = 0; r < R; ++r) buf[base + r * Ns] = v[c][r];
+    for (int r = 0; r < R; ++r) {
+      if (LAST) store(base + r * Ns, v[c][r]);
+      else buf[pidx(base + r * Ns)] = v[c][r];
+    }
   }
-  __syncthreads();
+  if (!LAST) __syncthreads();
 }
 
 // T = L/8 threads per row FFT; a CTA of blockDim threads transforms blockDim/T rows at a time.
 template <typename S>
-__global__ void __launch_bounds__(256) xform_fft_kernel(const S* __restrict__ in, S* __restrict__ out, XScale sc,
-                                                        int rows, int m0, int L, int dct) {
+__global__ void __launch_bounds__(256, 3) xform_fft_kernel(const S* __restrict__ in, S* __restrict__ out, XScale sc,
+                                                        int rows, int m0, int L, int dct,
+                                                        const double2* __restrict__ tw) {
+  // tw: plan-owned table exp(-2 pi i k / L), k < L (read through L1)
   extern __shared__ __align__(16) unsigned char sraw[];
-  const int T = L >= 8 ? L / 8 : 1;
-  const int rpc = blockDim.x / T;
-  double2* tw = reinterpret_cast<double2*>(sraw);  // [L]  exp(-2 pi i k / L)
-  for (int k = threadIdx.x; k < L; k += blockDim.x) {
-    double s, c;
-    sincospi(-2.0 * k / L, &s, &c);
-    tw[k] = mk(c, s);
-  }
+  const int T = L / 8;
   const int g = threadIdx.x / T, tid = threadIdx.x % T;
-  double2* buf = tw + L + (size_t)g * L;
+  const int rpc = blockDim.x / T;
+  double2* buf = reinterpret_cast<double2*>(sraw) + (size_t)g * padded_len(L);
   constexpr int RPF = Sc<S>::cplx ? 1 : 2;  // rows per FFT
   const int nfft = (rows + RPF - 1) / RPF;
   const int K = L / 2;
+  int radix[5], nst = 0;
+  for (int rem = L; rem > 1;) {
+    const int R = rem >= 8 ? 8 : rem;
+    radix[nst++] = R;
+    rem /= R;
+  }
   for (int f0 = blockIdx.x * rpc; f0 < nfft; f0 += gridDim.x * rpc) {
     const int f = f0 + g;
-    const bool active = g < rpc && f < nfft;
-    const int r0 = f * RPF;
+    const bool active = f < nfft;
+    const int r0 = (active ? f : 0) * RPF;
     const bool two = active && (RPF == 2) && (r0 + 1 < rows);
-    __syncthreads();
-    if (active) {
-      for (int j = tid; j < L; j += T) {
-        int J;
-        double sg = 1.0;
-        if (dct) {
-          J = j < K ? j : L - j;
-        } else if (j == 0 || j == K) {
-          J = -1;
-        } else if (j < K) {
-          J = j - 1;
-        } else {
-          J = L - j - 1;
-          sg = -1.0;
-        }
-        double2 v = mk(0.0, 0.0);
-        if (J >= 0) {
-          if constexpr (Sc<S>::cplx) {
-            const double2 x = in[(size_t)r0 * m0 + J];
-            v = mk(sg * x.x, sg * x.y);
-          } else {
-            const double a = in[(size_t)r0 * m0 + J];
-            const double b = two ? in[(size_t)(r0 + 1) * m0 + J] : 0.0;
-            v = mk(sg * a, sg * b);
-          }
-        }
-        buf[j] = v;
+    const S* row0 = in + (size_t)r0 * m0;
+    // symmetric extension G(j) of the row (two real rows packed as re/im)
+    auto load = [&](int j) -> double2 {
+      int J;
+      double sg = 1.0;
+      if (dct) {
+        J = j < K ? j : L - j;
+      } else if (j == 0 || j == K) {
+        return mk(0.0, 0.0);
+      } else if (j < K) {
+        J = j - 1;
+      } else {
+        J = L - j - 1;
+        sg = -1.0;
+      }
+      if (!active) return mk(0.0, 0.0);
+      if constexpr (Sc<S>::cplx) {
+        const double2 x = row0[J];
+        return mk(sg * x.x, sg * x.y);
+      } else {
+        return mk(sg * row0[J], two ? sg * row0[m0 + J] : 0.0);
+      }
+    };
+    double2 x0 = mk(0.0, 0.0), xm = mk(0.0, 0.0);
+    if (dct && active) {
+      if constexpr (Sc<S>::cplx) {
+        x0 = row0[0];
+        xm = row0[m0 - 1];
+      } else {
+        x0 = mk(row0[0], two ? row0[m0] : 0.0);
+        xm = mk(row0[m0 - 1], two ? row0[m0 + m0 - 1] : 0.0);
       }
     }
-    __syncthreads();
-    int Ns = 1, rem = L;
-    while (rem >= 8) {
-      stockham_stage<8>(buf, tw, L, Ns, tid, T);
-      Ns *= 8;
-      rem /= 8;
-    }
-    if (rem == 4) stockham_stage<4>(buf, tw, L, Ns, tid, T);
-    else if (rem == 2) stockham_stage<2>(buf, tw, L, Ns, tid, T);
-    if (!active) continue;
-    for (int a = tid; a < m0; a += T) {
+    // DFT index e -> transform output (sum_J Q[J][a] x_J, then the scale)
+    auto store = [&](int e, double2 d) {
+      if (!active) return;
+      int a;
       double2 R;
       if (dct) {  // sum_J cos(pi a J/M) x_J = (DFT[a] + x_0 + (-1)^a x_M) / 2
-        double2 x0, xm;
-        if constexpr (Sc<S>::cplx) {
-          x0 = in[(size_t)r0 * m0];
-          xm = in[(size_t)r0 * m0 + m0 - 1];
-        } else {
-          x0 = mk(in[(size_t)r0 * m0], two ? in[(size_t)(r0 + 1) * m0] : 0.0);
-          xm = mk(in[(size_t)r0 * m0 + m0 - 1], two ? in[(size_t)(r0 + 1) * m0 + m0 - 1] : 0.0);
-        }
+        if (e > K) return;
+        a = e;
         const double sgn = (a & 1) ? -1.0 : 1.0;
-        const double2 d = buf[a];
         R = mk(0.5 * (d.x + x0.x + sgn * xm.x), 0.5 * (d.y + x0.y + sgn * xm.y));
       } else {    // sum_J sin(pi (J+1)(a+1)/K) x_J = (i/2) DFT[a+1]
-        const double2 d = buf[a + 1];
+        if (e < 1 || e >= K) return;
+        a = e - 1;
         R = mk(-0.5 * d.y, 0.5 * d.x);
       }
       if constexpr (Sc<S>::cplx) {
@@ -197,7 +204,24 @@ __global__ void __launch_bounds__(256) xform_fft_kernel(const S* __restrict__ in
         out[(size_t)r0 * m0 + a] = R.x * xscale(sc, r0, a, m0);
         if (two) out[(size_t)(r0 + 1) * m0 + a] = R.y * xscale(sc, r0 + 1, a, m0);
       }
+    };
+    int Ns = 1;
+    for (int s = 0; s < nst; ++s) {
+      const bool first = s == 0, last = s == nst - 1;
+      const int R = radix[s];
+      if (R == 8) {
+        if (first && last) stockham_stage<8, true, true>(buf, tw, L, Ns, tid, T, load, store);
+        else if (first) stockham_stage<8, true, false>(buf, tw, L, Ns, tid, T, load, store);
+        else if (last) stockham_stage<8, false, true>(buf, tw, L, Ns, tid, T, load, store);
+        else stockham_stage<8, false, false>(buf, tw, L, Ns, tid, T, load, store);
+      } else if (R == 4) {  // never first (L >= 8)
+        stockham_stage<4, false, true>(buf, tw, L, Ns, tid, T, load, store);
+      } else {
+        stockham_stage<2, false, true>(buf, tw, L, Ns, tid, T, load, store);
+      }
+      Ns *= R;
     }
+    __syncthreads();  // the next row's first stage overwrites nothing, but keep rows in lockstep
   }
 }
 
@@ -252,7 +276,7 @@ void launch_xform(const helm_plan* P, const S* in, S* out, const double* sig, bo
     const int T = L / 8;
     const int threads = std::max(T, std::min(256, std::max(32, L)));
     const int rpc = threads / T;
-    const size_t smem = (size_t)(L + rpc * L) * sizeof(double2);
+    const size_t smem = (size_t)(rpc * padded_len(L)) * sizeof(double2);
     HELM_CHECK(smem <= 200 * 1024, "coarse FFT row too long for shared memory");
     static bool attr[2] = {false, false};
     if (!attr[Sc<S>::cplx]) {
@@ -261,8 +285,8 @@ void launch_xform(const helm_plan* P, const S* in, S* out, const double* sig, bo
       attr[Sc<S>::cplx] = true;
     }
     const int nfft = Sc<S>::cplx ? rows : (rows + 1) / 2;
-    const int blocks = std::min((nfft + rpc - 1) / rpc, 148 * 16);
-    xform_fft_kernel<S><<<blocks, threads, smem, st>>>(in, out, sc, rows, m0, L, dct);
+    const int blocks = std::min((nfft + rpc - 1) / rpc, 148 * 32);
+    xform_fft_kernel<S><<<blocks, threads, smem, st>>>(in, out, sc, rows, m0, L, dct, d.twiddle);
   } else {
     dim3 grd((m0 + 255) / 256, rows);
     xform_direct_kernel<S><<<grd, 256, 0, st>>>(in, out, sc, rows, m0, dct);

@@ -329,10 +329,61 @@ class SchwarzPreconditioner:
         if isinstance(x, np.ndarray) and np.iscomplexobj(x) and self.A.dtype == np.float64:
             return _real_split(self.apply, x, self.N)
         p = self.plan
+        if (isinstance(x, torch.Tensor) and not x.is_cuda and x.is_pinned() and x.dim() == 2 and x.is_contiguous()
+                and x.dtype == self.A.torch_dtype and x.shape[0] > self.PIPE_CHUNK and x.shape[1] == self.N
+                and out is not None and not out.is_cuda and out.is_pinned() and out.shape == x.shape):
+            return self._apply_pipelined(x, out)
         return self._run(lambda a, b, n: p.lib.helm_apply_M(p.handle, p.ws, _ptr(a), _ptr(b), n, _stream()), x,
                          out=out)
 
     __call__ = apply
+
+    PIPE_CHUNK = 8
+
+    def _apply_pipelined(self, xh: torch.Tensor, yh: torch.Tensor):
+        """Host batch -> host batch with the PCIe copies overlapped with the kernels.
+
+        The batch is cut into chunks of PIPE_CHUNK vectors; chunk i+1 is copied
+        host->device on one stream while chunk i runs through the kernels on the current
+        stream and chunk i-1 is copied device->host on a third, with two device buffers
+        per direction (events order the reuse).  Returns when ``yh`` holds the result."""
+        p = self.plan
+        cb = self.PIPE_CHUNK
+        comp = torch.cuda.current_stream()
+        st = getattr(self, "_pipe", None)
+        if st is None or st["bufs_in"][0].shape[0] != cb:
+            mk = lambda: torch.empty((cb, self.N), dtype=self.A.torch_dtype, device="cuda")  # noqa: E731
+            st = dict(s_in=torch.cuda.Stream(), s_out=torch.cuda.Stream(), bufs_in=[mk(), mk()],
+                      bufs_out=[mk(), mk()])
+            self._pipe = st
+        s_in, s_out = st["s_in"], st["s_out"]
+        ev_in = [torch.cuda.Event() for _ in range(2)]
+        ev_comp = [torch.cuda.Event() for _ in range(2)]
+        ev_out = [torch.cuda.Event() for _ in range(2)]
+        used = [False, False]
+        nb = xh.shape[0]
+        with self.plan.lock:
+            for i, lo in enumerate(range(0, nb, cb)):
+                hi, k = min(nb, lo + cb), i % 2
+                bi, bo = st["bufs_in"][k][: hi - lo], st["bufs_out"][k][: hi - lo]
+                if used[k]:
+                    s_in.wait_event(ev_comp[k])  # the kernels of chunk i-2 have consumed bufs_in[k]
+                with torch.cuda.stream(s_in):
+                    bi.copy_(xh[lo:hi], non_blocking=True)
+                    ev_in[k].record(s_in)
+                comp.wait_event(ev_in[k])
+                if used[k]:
+                    comp.wait_event(ev_out[k])  # chunk i-2's result has left bufs_out[k]
+                _lib.check(p.lib.helm_apply_M(p.handle, p.ws, _ptr(bi), _ptr(bo), hi - lo,
+                                              ctypes.c_void_p(comp.cuda_stream)))
+                ev_comp[k].record(comp)
+                s_out.wait_event(ev_comp[k])
+                with torch.cuda.stream(s_out):
+                    yh[lo:hi].copy_(bo, non_blocking=True)
+                    ev_out[k].record(s_out)
+                used[k] = True
+            s_out.synchronize()
+        return yh
 
     def restrict(self, x):
         p = self.plan
