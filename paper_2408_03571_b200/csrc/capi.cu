@@ -342,14 +342,51 @@ static void build_plan(const helm_desc* d, helm_plan* P) {
   }
   dv.class_real = upload<int>(creal.data(), creal.size());
   dv.class_Vr = upload<double>(vr.data(), vr.size());
-  std::vector<int> rr, mix;
+  // folded (symmetric) real classes: V[L-1-j][k] = sigma_k V[j][k]; even modes (sigma = +1)
+  // are packed at [0, 18) and odd modes at [18, 36) of a 36 x 36 table (local_fast.cu)
+  constexpr int FT = 36, FH = 18;
+  std::vector<int> cfold(d->n_classes, 0);
+  std::vector<double> vf((size_t)d->n_classes * FT * FT, 0.0), lf((size_t)d->n_classes * FT, 1.0);
+  for (int c = 0; c < d->n_classes; ++c) {
+    const int L = P->h_class_len[c];
+    if (!creal[c] || L > FT) continue;
+    const double* V = vr.data() + offV[c];  // V[j][k] row-major
+    const double* lam = (const double*)d->class_lambda;
+    const int h = L / 2, hp = (L + 1) / 2;
+    double vmax = 0.0;
+    for (int e = 0; e < L * L; ++e) vmax = std::max(vmax, std::fabs(V[e]));
+    bool ok = true;
+    int ne = 0, no = 0;
+    for (int k = 0; k < L && ok; ++k) {
+      const double sg = V[(L - 1) * L + k] * V[k] >= 0.0 ? 1.0 : -1.0;
+      for (int j = 0; j < L && ok; ++j)
+        if (std::fabs(V[(L - 1 - j) * L + k] - sg * V[j * L + k]) > 1e-12 * vmax) ok = false;
+      if (!ok) break;
+      const int col = sg > 0 ? ne++ : FH + no++;
+      if (ne > hp || no > h) {
+        ok = false;
+        break;
+      }
+      const int rows = sg > 0 ? hp : h;
+      for (int j = 0; j < rows; ++j) vf[((size_t)c * FT + (sg > 0 ? j : FH + j)) * FT + col] = V[j * L + k];
+      lf[(size_t)c * FT + col] = d->is_complex ? lam[2 * (offL[c] + k)] : lam[offL[c] + k];
+    }
+    cfold[c] = ok && ne == hp && no == h;
+  }
+  std::vector<int> ff, rr, mix;
   for (int ay = 0; ay < p; ++ay)
-    for (int ax = 0; ax < p; ++ax)
-      (creal[P->h_box_class[ay]] && creal[P->h_box_class[ax]] ? rr : mix).push_back(ay * p + ax);
+    for (int ax = 0; ax < p; ++ax) {
+      const int cy = P->h_box_class[ay], cx = P->h_box_class[ax];
+      (cfold[cy] && cfold[cx] ? ff : creal[cy] && creal[cx] ? rr : mix).push_back(ay * p + ax);
+    }
+  dv.n_ff = (int)ff.size();
   dv.n_rr = (int)rr.size();
   dv.n_mix = (int)mix.size();
+  dv.box_ff = upload<int>(ff.data(), ff.size());
   dv.box_rr = upload<int>(rr.data(), rr.size());
   dv.box_mix = upload<int>(mix.data(), mix.size());
+  dv.class_Vf = upload<double>(vf.data(), vf.size());
+  dv.class_lamf = upload<double>(lf.data(), lf.size());
   dv.node_first_box = upload<int>(first.data(), nu);
   dv.node_mult = upload<int>(mult.data(), nu);
   dv.node_band = upload<int>(band.data(), nu);
@@ -369,7 +406,8 @@ static void finish_desc(helm_plan* P) {
 static void free_plan(helm_plan* P) {
   PlanDev& dv = P->dev;
   void* ptrs[] = {dv.box_start, dv.box_len, dv.box_class, dv.class_len, dv.class_off_V, dv.class_off_lam,
-                  dv.class_V, dv.class_lambda, dv.class_real, dv.class_Vr, dv.box_rr, dv.box_mix, dv.node_first_box, dv.node_mult, dv.node_band, dv.band_node,
+                  dv.class_V, dv.class_lambda, dv.class_real, dv.class_Vr, dv.box_ff, dv.class_Vf, dv.class_lamf, dv.box_rr, dv.box_mix,
+                  dv.node_first_box, dv.node_mult, dv.node_band, dv.band_node,
                   dv.coarse_scale, dv.twiddle, dv.coarse_lamT, dv.coarse_lamM, dv.t0_band, dv.m0_band, dv.band_piv, dv.band_l, dv.band_u, dv.strip_q,
                   dv.cap_left, dv.cap_right, dv.cap_mode};
   for (void* q : ptrs)

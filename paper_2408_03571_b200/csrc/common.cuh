@@ -147,7 +147,11 @@ struct PlanDev {
   void* class_lambda;
   int* class_real;     // 1: V and lambda of the class are real (class_Vr holds V)
   double* class_Vr;
-  int* box_rr;         // subdomain ids (ay * p + ax) whose two classes are real
+  int* box_ff;         // subdomain ids (ay * p + ax) whose two classes are real and symmetric (folded FDM)
+  int n_ff;
+  double* class_Vf;    // [n_classes][36][36] folded eigenvectors (even modes | odd modes)
+  double* class_lamf;  // [n_classes][36] eigenvalues in the folded mode order (padding 1)
+  int* box_rr;         // other subdomains whose two classes are real
   int n_rr;
   int* box_mix;        // the other subdomains
   int n_mix;

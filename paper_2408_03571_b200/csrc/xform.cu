@@ -7,7 +7,7 @@
 //   s(r, a) = 1, sig[a], or the 2-D Dirichlet eigenvalue scaling
 //             qn / (lamT[a] lamM[kx] + lamM[a] lamT[kx] - k^2 lamM[a] lamM[kx]),  kx = r mod m0.
 //
-// A CTA runs FFTs of the symmetric extension (L/8 threads each) in shared
+// A CTA runs FFTs of the symmetric extension (L/16 threads each) in shared
 // memory: radix-8 Stockham stages (radix 4/2 for the remainder) in registers,
 // in place through a barrier, twiddles tabulated once per CTA with sincospi.
 // Real rows are packed two per FFT: Q is real, so DST(x + i y) = DST(x) + i DST(y).  Rows are read and written with coalesced
@@ -78,19 +78,19 @@ __host__ __device__ constexpr int padded_len(int L) { return L + L / 8 + L / 64 
 // One Stockham stage of radix R over a row of length L (T threads, NBT = 8/R butterflies
 // each).  Butterfly j: inputs X[j + r L/R], twiddles W^r with W = W_{Ns R}^{j mod Ns}
 // (plan-owned table in L1), outputs at (j / Ns) Ns R + (j mod Ns) + r Ns.
-// FIRST: inputs come from `load(i)` (global); LAST: outputs go to `store(i, v)` (global);
+// FIRST: inputs come from `load(c, r, i)` (registers); LAST: outputs go to `store(i, v)` (global);
 // otherwise through the padded shared buffer, in place across a barrier.
-template <int R, bool FIRST, bool LAST, typename LD, typename STO>
+template <int VPT, int R, bool FIRST, bool LAST, typename LD, typename STO>
 __device__ __forceinline__ void stockham_stage(double2* buf, const double2* __restrict__ tw, int L, int Ns, int tid,
                                                int T, LD load, STO store) {
   const int nb = L / R;
-  constexpr int NBT = 8 / R;
+  constexpr int NBT = VPT / R;  // butterflies per thread (T = L / VPT threads per row)
   double2 v[NBT][R];
 #pragma unroll
   for (int c = 0; c < NBT; ++c) {
     const int j = tid + c * T;
 #pragma unroll
-    for (int r = 0; r < R; ++r) v[c][r] = FIRST ? load(j + r * nb) : buf[pidx(j + r * nb)];
+    for (int r = 0; r < R; ++r) v[c][r] = FIRST ? load(c, r, j + r * nb) : buf[pidx(j + r * nb)];
   }
   if (!FIRST) __syncthreads();
   const int tstep = L / (Ns * R);
@@ -99,12 +99,20 @@ __device__ __forceinline__ void stockham_stage(double2* buf, const double2* __re
     const int j = tid + c * T;
     const int k = j % Ns;
     if (!FIRST) {  // Ns == 1 on the first stage: all twiddles are 1
-#pragma unroll
-      for (int r = 1; r < R; ++r) {  // independent L1-resident table reads, no dependency chain
-        const double2 w = tw[k * r * tstep];
-        const double2 xv = v[c][r];
-        v[c][r] = mk(w.x * xv.x - w.y * xv.y, w.x * xv.y + w.y * xv.x);
+      // W^1 and W^2 from the table, the other powers by a depth-2 product tree
+      // (2 loads instead of R-1: the load/store queue is this kernel's limiter)
+      double2 w[8];
+      w[1] = tw[k * tstep];
+      if (R > 2) w[2] = tw[2 * k * tstep];
+      if (R > 3) w[3] = mul(w[1], w[2]);
+      if (R > 4) {
+        w[4] = mul(w[2], w[2]);
+        w[5] = mul(w[1], w[4]);
+        w[6] = mul(w[2], w[4]);
+        w[7] = mul(w[3], w[4]);
       }
+#pragma unroll
+      for (int r = 1; r < R; ++r) v[c][r] = mul(v[c][r], w[r]);
     }
     if constexpr (R == 8) {
       dft8(v[c]);
@@ -125,11 +133,15 @@ __device__ __forceinline__ void stockham_stage(double2* buf, const double2* __re
   if (!LAST) __syncthreads();
 }
 
-// T = L/8 threads per row FFT; a CTA of blockDim threads transforms blockDim/T rows at a time.
-template <typename S>
-__global__ void __launch_bounds__(256, 3) xform_fft_kernel(const S* __restrict__ in, S* __restrict__ out, XScale sc,
+// T = L/8 threads per row FFT (8 values in registers per thread); a CTA of
+// blockDim threads transforms blockDim/T rows at a time.  The first radix-8 stage
+// takes its inputs from registers that were loaded from HBM while the previous
+// row was in its shared-memory stages (one row of prefetch per thread).
+template <typename S, int VPT>
+__global__ void __launch_bounds__(256) xform_fft_kernel(const S* __restrict__ in, S* __restrict__ out, XScale sc,
                                                         int rows, int m0, int L, int dct,
                                                         const double2* __restrict__ tw) {
+  static_assert(VPT == 8, "one radix-8 butterfly per thread in the first stage");
   // tw: plan-owned table exp(-2 pi i k / L), k < L (read through L1)
   extern __shared__ __align__(16) unsigned char sraw[];
   const int T = L / 8;
@@ -139,40 +151,57 @@ __global__ void __launch_bounds__(256, 3) xform_fft_kernel(const S* __restrict__
   constexpr int RPF = Sc<S>::cplx ? 1 : 2;  // rows per FFT
   const int nfft = (rows + RPF - 1) / RPF;
   const int K = L / 2;
-  int radix[5], nst = 0;
+  int nst = 0, rlast = 8;
   for (int rem = L; rem > 1;) {
-    const int R = rem >= 8 ? 8 : rem;
-    radix[nst++] = R;
-    rem /= R;
+    rlast = rem >= 8 ? 8 : rem;
+    ++nst;
+    rem /= rlast;
   }
+  // symmetric extension G(j) of FFT f (two real rows packed as re/im)
+  auto load = [&](int f, int j) -> double2 {
+    if (f >= nfft) return mk(0.0, 0.0);
+    const int r0 = f * RPF;
+    const S* row0 = in + (size_t)r0 * m0;
+    int J;
+    double sg = 1.0;
+    if (dct) {
+      J = j < K ? j : L - j;
+    } else if (j == 0 || j == K) {
+      return mk(0.0, 0.0);
+    } else if (j < K) {
+      J = j - 1;
+    } else {
+      J = L - j - 1;
+      sg = -1.0;
+    }
+    if constexpr (Sc<S>::cplx) {
+      const double2 x = row0[J];
+      return mk(sg * x.x, sg * x.y);
+    } else {
+      return mk(sg * row0[J], (r0 + 1 < rows) ? sg * row0[m0 + J] : 0.0);
+    }
+  };
+  double2 cur[8];
+  int f = blockIdx.x * rpc + g;
+#pragma unroll
+  for (int r = 0; r < 8; ++r) cur[r] = load(f, tid + r * T);
   for (int f0 = blockIdx.x * rpc; f0 < nfft; f0 += gridDim.x * rpc) {
-    const int f = f0 + g;
+    f = f0 + g;
     const bool active = f < nfft;
     const int r0 = (active ? f : 0) * RPF;
     const bool two = active && (RPF == 2) && (r0 + 1 < rows);
+    // stage 1 from the prefetched registers, then prefetch the next row
+    double2 nxt[8];
+    {
+      const double2* c = cur;
+      stockham_stage<8, 8, true, false>(buf, tw, L, 1, tid, T, [&](int, int r, int) { return c[r]; },
+                                        [&](int, double2) {});
+    }
+    const int fn = f + gridDim.x * rpc;
+#pragma unroll
+    for (int r = 0; r < 8; ++r) nxt[r] = load(fn, tid + r * T);
+    // DFT index e -> transform output (sum_J Q[J][a] x_J, then the scale)
     const S* row0 = in + (size_t)r0 * m0;
-    // symmetric extension G(j) of the row (two real rows packed as re/im)
-    auto load = [&](int j) -> double2 {
-      int J;
-      double sg = 1.0;
-      if (dct) {
-        J = j < K ? j : L - j;
-      } else if (j == 0 || j == K) {
-        return mk(0.0, 0.0);
-      } else if (j < K) {
-        J = j - 1;
-      } else {
-        J = L - j - 1;
-        sg = -1.0;
-      }
-      if (!active) return mk(0.0, 0.0);
-      if constexpr (Sc<S>::cplx) {
-        const double2 x = row0[J];
-        return mk(sg * x.x, sg * x.y);
-      } else {
-        return mk(sg * row0[J], two ? sg * row0[m0 + J] : 0.0);
-      }
-    };
     double2 x0 = mk(0.0, 0.0), xm = mk(0.0, 0.0);
     if (dct && active) {
       if constexpr (Sc<S>::cplx) {
@@ -183,7 +212,6 @@ __global__ void __launch_bounds__(256, 3) xform_fft_kernel(const S* __restrict__
         xm = mk(row0[m0 - 1], two ? row0[m0 + m0 - 1] : 0.0);
       }
     }
-    // DFT index e -> transform output (sum_J Q[J][a] x_J, then the scale)
     auto store = [&](int e, double2 d) {
       if (!active) return;
       int a;
@@ -205,24 +233,48 @@ __global__ void __launch_bounds__(256, 3) xform_fft_kernel(const S* __restrict__
         if (two) out[(size_t)(r0 + 1) * m0 + a] = R.y * xscale(sc, r0 + 1, a, m0);
       }
     };
-    int Ns = 1;
-    for (int s = 0; s < nst; ++s) {
-      const bool first = s == 0, last = s == nst - 1;
-      const int R = radix[s];
-      if (R == 8) {
-        if (first && last) stockham_stage<8, true, true>(buf, tw, L, Ns, tid, T, load, store);
-        else if (first) stockham_stage<8, true, false>(buf, tw, L, Ns, tid, T, load, store);
-        else if (last) stockham_stage<8, false, true>(buf, tw, L, Ns, tid, T, load, store);
-        else stockham_stage<8, false, false>(buf, tw, L, Ns, tid, T, load, store);
-      } else if (R == 4) {  // never first (L >= 8)
-        stockham_stage<4, false, true>(buf, tw, L, Ns, tid, T, load, store);
+    auto none = [&](int, int, int) { return mk(0.0, 0.0); };
+    int Ns = 8;
+    for (int s = 1; s < nst; ++s) {
+      const bool last = s == nst - 1;
+      if (!last) {
+        stockham_stage<8, 8, false, false>(buf, tw, L, Ns, tid, T, none, store);
+        Ns *= 8;
+      } else if (rlast == 8) {
+        stockham_stage<8, 8, false, true>(buf, tw, L, Ns, tid, T, none, store);
+      } else if (rlast == 4) {
+        stockham_stage<8, 4, false, true>(buf, tw, L, Ns, tid, T, none, store);
       } else {
-        stockham_stage<2, false, true>(buf, tw, L, Ns, tid, T, load, store);
+        stockham_stage<8, 2, false, true>(buf, tw, L, Ns, tid, T, none, store);
       }
-      Ns *= R;
     }
-    __syncthreads();  // the next row's first stage overwrites nothing, but keep rows in lockstep
+    if (nst == 1) {  // L == 8: the first stage was also the last; emit from smem
+      __syncthreads();
+      if (tid == 0)
+        for (int e = 0; e < 8; ++e) store(e, buf[pidx(e)]);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < 8; ++r) cur[r] = nxt[r];
   }
+}
+
+template <typename S, int VPT>
+static void fft_launch(const S* in, S* out, const XScale& sc, int rows, int m0, int L, int dct, const double2* tw,
+                       cudaStream_t st) {
+  const int T = L / VPT;
+  const int threads = std::max(T, std::min(256, std::max(32, L)));
+  const int rpc = threads / T;
+  const size_t smem = (size_t)(rpc * padded_len(L)) * sizeof(double2);
+  HELM_CHECK(smem <= 200 * 1024 && threads <= 256, "coarse FFT row too long");
+  static bool attr = false;
+  if (!attr) {
+    HELM_CUDA(cudaFuncSetAttribute(xform_fft_kernel<S, VPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    attr = true;
+  }
+  const int nfft = Sc<S>::cplx ? rows : (rows + 1) / 2;
+  const int blocks = std::min((nfft + rpc - 1) / rpc, 148 * 4);
+  xform_fft_kernel<S, VPT><<<blocks, threads, smem, st>>>(in, out, sc, rows, m0, L, dct, tw);
 }
 
 // Direct O(m0^2)-per-row transform for grids whose n - 1 is not a power of two.
@@ -263,6 +315,7 @@ __global__ void __launch_bounds__(256) transpose_kernel(const S* __restrict__ in
   }
 }
 
+
 template <typename S>
 void launch_xform(const helm_plan* P, const S* in, S* out, const double* sig, bool scale2d, int batch,
                   cudaStream_t st) {
@@ -273,20 +326,7 @@ void launch_xform(const helm_plan* P, const S* in, S* out, const double* sig, bo
   if (scale2d) sc = XScale{nullptr, d.coarse_lamT, d.coarse_lamM, P->geo.k2, d.coarse_qn};
   if (d.fft_len) {
     const int L = d.fft_len;
-    const int T = L / 8;
-    const int threads = std::max(T, std::min(256, std::max(32, L)));
-    const int rpc = threads / T;
-    const size_t smem = (size_t)(rpc * padded_len(L)) * sizeof(double2);
-    HELM_CHECK(smem <= 200 * 1024, "coarse FFT row too long for shared memory");
-    static bool attr[2] = {false, false};
-    if (!attr[Sc<S>::cplx]) {
-      HELM_CUDA(cudaFuncSetAttribute(xform_fft_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     200 * 1024));
-      attr[Sc<S>::cplx] = true;
-    }
-    const int nfft = Sc<S>::cplx ? rows : (rows + 1) / 2;
-    const int blocks = std::min((nfft + rpc - 1) / rpc, 148 * 32);
-    xform_fft_kernel<S><<<blocks, threads, smem, st>>>(in, out, sc, rows, m0, L, dct, d.twiddle);
+    fft_launch<S, 8>(in, out, sc, rows, m0, L, dct, d.twiddle, st);
   } else {
     dim3 grd((m0 + 255) / 256, rows);
     xform_direct_kernel<S><<<grd, 256, 0, st>>>(in, out, sc, rows, m0, dct);

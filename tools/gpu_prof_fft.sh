@@ -1,0 +1,2 @@
+mkdir -p gpurun_out
+python tools/profile_ops.py --gmres 0 --only "coarse solve" --reps 1 --batches 32 > gpurun_out/plain.log 2>&1 && ncu --set full --import-source on -k "regex:xform_fft" -s 0 -c 1 -o gpurun_out/fft python tools/profile_ops.py --gmres 0 --only "coarse solve" --reps 1 --batches 32 > gpurun_out/ncu.log 2>&1; echo ncu=$?
