@@ -67,13 +67,18 @@ template <typename S>
 void op_apply_M(const helm_plan* P, helm_workspace* ws, const S* x, S* y, int batch, cudaStream_t st) {
   HELM_CHECK((const void*)x != (const void*)y, "apply_M: input and output must not alias");
   S* z = (S*)ws->z;
-  op_coarse_correct<S>(P, ws, x, z, batch, st);
   const int kind = P->desc.kind;
   if (kind == HELM_SHS2) {
+    // z = R0^T A0^{-1} R0 x and d = x - A z (schwarz.py:86-88) with the prolongation
+    // and the deflation stencil fused in one pass
+    S* c = (S*)ws->c;
     S* d = (S*)ws->d;
-    launch_stencil<S>(P->geo, x, z, d, batch, st);  // d = x - A z (schwarz.py:88)
+    launch_restrict<S>(P->geo, x, c, batch, st);
+    launch_coarse_solve<S>(P, ws, c, c, batch, st);
+    launch_prolong_deflate<S>(P->geo, c, x, z, d, batch, st);
     launch_local_sum<S>(P, d, z, y, (S*)ws->ovl, 1, batch, P->dev.band_node, st);
   } else {
+    op_coarse_correct<S>(P, ws, x, z, batch, st);
     launch_local_sum<S>(P, x, z, y, (S*)ws->ovl, kind == HELM_SAS2 ? 1 : 0, batch, P->dev.band_node, st);
   }
 }

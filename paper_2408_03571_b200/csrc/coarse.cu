@@ -195,25 +195,28 @@ static void strip_gemm(const S* A, const S* Z, S* out, const S* Hm, int m0, int 
 }
 
 // --- r = c - A0 y  (25-point Kronecker-sum stencil from the 1-D bands) ------
+// 32 x 32 outputs per CTA (256 threads, 4 rows each); the (32+4) x (32+4) window
+// of y is staged in shared memory (zero outside = the band ends), then the
+// separable x-pass (M0 and T0 - k^2 M0 rows) and y-pass run from shared memory.
+constexpr int RSX = 32, RSY = 32;
 template <typename S>
 __global__ void __launch_bounds__(256) a0_residual_kernel(const S* __restrict__ c, const S* __restrict__ y,
                                                           S* __restrict__ r, const S* __restrict__ t0b,
                                                           const S* __restrict__ m0b, double k2, int m0) {
-  // 32 x 8 outputs per CTA; the (8+4) x (32+4) window of y is staged in shared
-  // memory (zero outside = the band ends), then the separable x-pass (M0, T0 rows)
-  // and y-pass run from shared memory.
-  constexpr int RX = 32, RY = 8;
-  __shared__ S ys[RY + 4][RX + 4];
-  __shared__ S xm[RY + 4][RX], xt[RY + 4][RX];
-  const int tx = threadIdx.x, ty = threadIdx.y;
-  const int V0 = blockIdx.x * RX, U0 = blockIdx.y * RY;
+  extern __shared__ __align__(16) unsigned char sraw[];
+  S (*ys)[RSX + 4] = reinterpret_cast<S (*)[RSX + 4]>(sraw);
+  S (*xm)[RSX] = reinterpret_cast<S (*)[RSX]>(ys + (RSY + 4));
+  S (*xt)[RSX] = xm + (RSY + 4);
+  const int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
+  const int V0 = blockIdx.x * RSX, U0 = blockIdx.y * RSY;
   const size_t off = (size_t)blockIdx.z * m0 * m0;
-  for (int e = ty * RX + tx; e < (RY + 4) * (RX + 4); e += RX * RY) {
-    const int rr = e / (RX + 4), q = e % (RX + 4);
-    const int U = U0 + rr - 2, W = V0 + q - 2;
-    ys[rr][q] = (U >= 0 && U < m0 && W >= 0 && W < m0) ? y[off + (size_t)U * m0 + W] : Sc<S>::zero();
+  for (int rr = ty; rr < RSY + 4; rr += 8) {
+    const int U = U0 + rr - 2;
+    for (int q = tx; q < RSX + 4; q += 32) {
+      const int W = V0 + q - 2;
+      ys[rr][q] = (U >= 0 && U < m0 && W >= 0 && W < m0) ? y[off + (size_t)U * m0 + W] : Sc<S>::zero();
+    }
   }
-  __syncthreads();
   const int V = V0 + tx;
   S bm[5], bt[5];
 #pragma unroll
@@ -221,7 +224,8 @@ __global__ void __launch_bounds__(256) a0_residual_kernel(const S* __restrict__ 
     bm[d] = V < m0 ? m0b[V * 5 + d] : Sc<S>::zero();
     bt[d] = V < m0 ? t0b[V * 5 + d] : Sc<S>::zero();
   }
-  for (int rr = ty; rr < RY + 4; rr += RY) {  // x-pass: sum_dx M0[V][V+dx] y, T0[V][V+dx] y
+  __syncthreads();
+  for (int rr = ty; rr < RSY + 4; rr += 8) {  // x-pass: sum_dx M0[V][V+dx] y, T0[V][V+dx] y
     S sm = Sc<S>::zero(), stt = Sc<S>::zero();
 #pragma unroll
     for (int d = 0; d < 5; ++d) {
@@ -232,30 +236,30 @@ __global__ void __launch_bounds__(256) a0_residual_kernel(const S* __restrict__ 
     xt[rr][tx] = sub(stt, scale(sm, k2));
   }
   __syncthreads();
-  const int Uc = U0 + ty;
-  if (V >= m0 || Uc >= m0) return;
-  S acc = Sc<S>::zero();  // T0(y) M0(x) + M0(y) (T0(x) - k^2 M0(x))
+  if (V >= m0) return;
 #pragma unroll
-  for (int d = 0; d < 5; ++d) {
-    acc = fma_(t0b[Uc * 5 + d], xm[ty + d][tx], acc);
-    acc = fma_(m0b[Uc * 5 + d], xt[ty + d][tx], acc);
+  for (int q = 0; q < RSY / 8; ++q) {
+    const int rr = ty + 8 * q, Uc = U0 + rr;
+    if (Uc >= m0) break;
+    S acc = Sc<S>::zero();  // T0(y) M0(x) + M0(y) (T0(x) - k^2 M0(x))
+#pragma unroll
+    for (int d = 0; d < 5; ++d) {
+      acc = fma_(t0b[Uc * 5 + d], xm[rr + d][tx], acc);
+      acc = fma_(m0b[Uc * 5 + d], xt[rr + d][tx], acc);
+    }
+    const size_t p = off + (size_t)Uc * m0 + V;
+    r[p] = sub(c[p], acc);
   }
-  const size_t p = off + (size_t)Uc * m0 + V;
-  r[p] = sub(c[p], acc);
 }
 
-template <typename S>
-__global__ void axpy_kernel(S* __restrict__ y, const S* __restrict__ d, size_t n) {
-  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
-    y[i] = add(y[i], d[i]);
-}
 
 // ----------------------------------------------------------------------------
 // composition
 // ----------------------------------------------------------------------------
 // One fast solve: out = A0^{-1} in  (in, out distinct from ws->g / ws->f0)
 template <typename S>
-static void fast_solve(const helm_plan* P, helm_workspace* ws, const S* in, S* out, int batch, cudaStream_t st) {
+static void fast_solve(const helm_plan* P, helm_workspace* ws, const S* in, S* out, int batch, cudaStream_t st,
+                       bool accumulate = false) {
   const PlanDev& d = P->dev;
   S* T1 = (S*)ws->g;
   S* T2 = (S*)ws->f0;
@@ -266,7 +270,7 @@ static void fast_solve(const helm_plan* P, helm_workspace* ws, const S* in, S* o
     launch_xform<S>(P, T2, T1, nullptr, true, batch, st);
     launch_xform<S>(P, T1, T2, nullptr, false, batch, st);
     launch_transpose<S>(T2, T1, d.m0, batch, st);
-    launch_xform<S>(P, T1, out, nullptr, false, batch, st);
+    launch_xform<S>(P, T1, out, nullptr, false, batch, st, accumulate);
   } else {
     launch_xform<S>(P, in, T1, d.coarse_scale, false, batch, st);
     launch_band_solve(P, T1, T2, nullptr, batch, st);
@@ -280,7 +284,7 @@ static void fast_solve(const helm_plan* P, helm_workspace* ws, const S* in, S* o
     strip_gemm<S>((const S*)d.cap_left, Z, Ch, (const S*)d.cap_mode, d.m0, batch, part, st);
     strip_gemm<S>((const S*)d.cap_right, Ch, Cs, nullptr, d.m0, batch, part, st);
     launch_band_solve(P, T1, T2, Cs, batch, st);
-    launch_xform<S>(P, T2, out, nullptr, false, batch, st);
+    launch_xform<S>(P, T2, out, nullptr, false, batch, st, accumulate);
   }
 }
 
@@ -290,18 +294,21 @@ void launch_coarse_solve(const helm_plan* P, helm_workspace* ws, const S* c, S* 
   const int m0 = P->geo.m0;
   const size_t n0 = (size_t)batch * m0 * m0;
   S* r = (S*)ws->r0;
-  S* corr = (S*)ws->e0;
   // c is only read; y is written last when it aliases c
   S* yy = ((const void*)c == (const void*)y) ? (S*)ws->y0 : y;
   fast_solve<S>(P, ws, c, yy, batch, st);
   for (int it = 0; it < P->desc.refine_steps; ++it) {
-    dim3 blk(32, 8), grd((m0 + 31) / 32, (m0 + 7) / 8, batch);
-    a0_residual_kernel<S><<<grd, blk, 0, st>>>(c, yy, r, (const S*)P->dev.t0_band, (const S*)P->dev.m0_band,
-                                               P->geo.k2, m0);
+    const size_t smem = (size_t)((RSY + 4) * (RSX + 4) + 2 * (RSY + 4) * RSX) * sizeof(S);
+    static bool attr = false;
+    if (!attr) {
+      HELM_CUDA(cudaFuncSetAttribute(a0_residual_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      attr = true;
+    }
+    dim3 blk(32, 8), grd((m0 + RSX - 1) / RSX, (m0 + RSY - 1) / RSY, batch);
+    a0_residual_kernel<S><<<grd, blk, smem, st>>>(c, yy, r, (const S*)P->dev.t0_band, (const S*)P->dev.m0_band,
+                                                  P->geo.k2, m0);
     HELM_LAUNCH_CHECK();
-    fast_solve<S>(P, ws, r, corr, batch, st);
-    axpy_kernel<S><<<1184, 256, 0, st>>>(yy, corr, n0);
-    HELM_LAUNCH_CHECK();
+    fast_solve<S>(P, ws, r, yy, batch, st, /*accumulate=*/true);  // yy += A0~^{-1} r
   }
   if (yy != y) HELM_CUDA(cudaMemcpyAsync(y, yy, n0 * sizeof(S), cudaMemcpyDeviceToDevice, st));
 }

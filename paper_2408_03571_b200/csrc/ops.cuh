@@ -8,6 +8,8 @@ template <typename S> void launch_stencil(const Geo& g, const S* x, const S* z, 
 template <typename S> void launch_restrict(const Geo& g, const S* x, S* c, int batch, cudaStream_t st);
 template <typename S> void launch_prolong(const Geo& g, const S* c, S* z, int batch, cudaStream_t st);
 template <typename S>
+void launch_prolong_deflate(const Geo& g, const S* c, const S* x, S* z, S* d, int batch, cudaStream_t st);
+template <typename S>
 void launch_local_sum(const helm_plan* P, const S* x, const S* base, S* y, S* ovl, int weighted, int batch,
                       const int* band_node, cudaStream_t st);
 template <typename S>
@@ -16,7 +18,7 @@ void launch_coarse_solve(const helm_plan* P, helm_workspace* ws, const S* c, S* 
 // coarse-solve building blocks (xform.cu, band.cu)
 template <typename S>
 void launch_xform(const helm_plan* P, const S* in, S* out, const double* sig, bool scale2d, int batch,
-                  cudaStream_t st);
+                  cudaStream_t st, bool accumulate = false);
 template <typename S> void launch_transpose(const S* in, S* out, int m, int batch, cudaStream_t st);
 void launch_band_solve(const helm_plan* P, const double2* in, double2* out, const double2* corr, int batch,
                        cudaStream_t st);

@@ -163,10 +163,95 @@ void launch_prolong(const Geo& g, const S* c, S* z, int batch, cudaStream_t st) 
   HELM_LAUNCH_CHECK();
 }
 
+// --- K3 + K1 fused for SHS2 (schwarz.py:86-88): z = R0^T c and d = x - A z ---
+// A CTA owns a PW x PH fine tile.  The coarse window it needs is staged in shared
+// memory, z is prolongated onto the tile plus a one-node halo in shared memory,
+// and the 5-point stencil of the deflation runs from there: c is read once, x
+// once, z and d written once -- no HBM round trip of z between two kernels.
+constexpr int PW = 32, PH = 16;
+constexpr int PCW = (PW + 2) / 2 + 3, PCH = (PH + 2) / 2 + 3;  // coarse window
+
+__device__ __forceinline__ int floordiv2(int t) { return t >= 0 ? t / 2 : -((1 - t) / 2); }
+
+template <typename S>
+__device__ __forceinline__ S stencil_point(const Geo& g, int ix, int iy, S c, S up, S dn, S lf, S rt) {
+  if constexpr (!Sc<S>::cplx) {
+    return (4.0 * g.inv_h2 - g.k2) * c - g.inv_h2 * (up + dn + lf + rt);
+  } else {
+    const int nu = g.nu;
+    const bool ey = (iy == 0) | (iy == nu - 1), ex = (ix == 0) | (ix == nu - 1);
+    const double wy = ey ? 0.5 : 1.0, wx = ex ? 0.5 : 1.0;
+    const double2 ty = ey ? g.tb : mk(2.0 * g.inv_h2, 0.0);
+    const double2 tx = ex ? g.tb : mk(2.0 * g.inv_h2, 0.0);
+    const double2 diag = mk(wx * ty.x + wy * tx.x - g.k2 * wy * wx, wx * ty.y + wy * tx.y);
+    S acc = mul(diag, c);
+    acc = sub(acc, scale(add(up, dn), wx * g.inv_h2));
+    acc = sub(acc, scale(add(lf, rt), wy * g.inv_h2));
+    return acc;
+  }
+}
+
+template <typename S>
+__global__ void __launch_bounds__(256) prolong_deflate_kernel(const S* __restrict__ c, const S* __restrict__ x,
+                                                              S* __restrict__ z, S* __restrict__ d, Geo g) {
+  __shared__ S cs[PCH][PCW];
+  __shared__ S zs[PH + 2][PW + 2];
+  const int nu = g.nu, m0 = g.m0;
+  const int v0 = blockIdx.x * PW, u0 = blockIdx.y * PH;
+  const size_t boff = (size_t)blockIdx.z * nu * nu;
+  const S* cb = c + (size_t)blockIdx.z * m0 * m0;
+  const int Ub = floordiv2(u0 - 1 - g.off) - 1, Vb = floordiv2(v0 - 1 - g.off) - 1;
+  const int tid = threadIdx.y * blockDim.x + threadIdx.x;
+  for (int e = tid; e < PCH * PCW; e += 256) {
+    const int rr = e / PCW, q = e % PCW;
+    const int U = Ub + rr, V = Vb + q;
+    cs[rr][q] = (U >= 0 && U < m0 && V >= 0 && V < m0) ? cb[(size_t)U * m0 + V] : Sc<S>::zero();
+  }
+  __syncthreads();
+  for (int e = tid; e < (PH + 2) * (PW + 2); e += 256) {
+    const int rr = e / (PW + 2), q = e % (PW + 2);
+    const int u = u0 - 1 + rr, v = v0 - 1 + q;
+    S acc = Sc<S>::zero();
+    if (u >= 0 && u < nu && v >= 0 && v < nu) {
+      int Uy, ny, Ux, nx;
+      double wy[3], wx[3];
+      prolong_taps(u, g, Uy, ny, wy);
+      prolong_taps(v, g, Ux, nx, wx);
+      for (int a = 0; a < ny; ++a) {  // cs has zeros outside [0, m0): the dropped taps
+        S row = Sc<S>::zero();
+        for (int b = 0; b < nx; ++b) row = fma_(wx[b], cs[Uy + a - Ub][Ux + b - Vb], row);
+        acc = fma_(wy[a], row, acc);
+      }
+    }
+    zs[rr][q] = acc;
+  }
+  __syncthreads();
+  const int v = v0 + threadIdx.x;
+  if (v >= nu) return;
+  for (int rr = threadIdx.y; rr < PH; rr += blockDim.y) {
+    const int u = u0 + rr;
+    if (u >= nu) break;
+    const S zc = zs[rr + 1][threadIdx.x + 1];
+    const S az = stencil_point<S>(g, v, u, zc, zs[rr][threadIdx.x + 1], zs[rr + 2][threadIdx.x + 1],
+                                  zs[rr + 1][threadIdx.x], zs[rr + 1][threadIdx.x + 2]);
+    const size_t p = boff + (size_t)u * nu + v;
+    z[p] = zc;
+    d[p] = sub(x[p], az);
+  }
+}
+
+template <typename S>
+void launch_prolong_deflate(const Geo& g, const S* c, const S* x, S* z, S* d, int batch, cudaStream_t st) {
+  dim3 blk(32, 8), grd((g.nu + PW - 1) / PW, (g.nu + PH - 1) / PH, batch);
+  prolong_deflate_kernel<S><<<grd, blk, 0, st>>>(c, x, z, d, g);
+  HELM_LAUNCH_CHECK();
+}
+
 #define HELM_INST(S)                                                                           \
   template void launch_stencil<S>(const Geo&, const S*, const S*, S*, int, cudaStream_t);      \
   template void launch_restrict<S>(const Geo&, const S*, S*, int, cudaStream_t);               \
-  template void launch_prolong<S>(const Geo&, const S*, S*, int, cudaStream_t);
+  template void launch_prolong<S>(const Geo&, const S*, S*, int, cudaStream_t);                \
+  template void launch_prolong_deflate<S>(const Geo&, const S*, const S*, S*, S*, int, cudaStream_t);
 HELM_INST(double)
 HELM_INST(double2)
 #undef HELM_INST

@@ -17,6 +17,7 @@
 namespace helm {
 
 struct XScale {
+  int accum;           // 1: out += result (iterative-refinement update), 0: out = result
   const double* sig;   // per-mode scale, or NULL
   const double* lamT;  // 2-D Dirichlet scaling (NULL: off)
   const double* lamM;
@@ -227,10 +228,17 @@ __global__ void __launch_bounds__(256) xform_fft_kernel(const S* __restrict__ in
         R = mk(-0.5 * d.y, 0.5 * d.x);
       }
       if constexpr (Sc<S>::cplx) {
-        out[(size_t)r0 * m0 + a] = scale(R, xscale(sc, r0, a, m0));
+        S* o = out + (size_t)r0 * m0 + a;
+        const S v = scale(R, xscale(sc, r0, a, m0));
+        *o = sc.accum ? add(*o, v) : v;
       } else {
-        out[(size_t)r0 * m0 + a] = R.x * xscale(sc, r0, a, m0);
-        if (two) out[(size_t)(r0 + 1) * m0 + a] = R.y * xscale(sc, r0 + 1, a, m0);
+        S* o = out + (size_t)r0 * m0 + a;
+        const S v = R.x * xscale(sc, r0, a, m0);
+        *o = sc.accum ? *o + v : v;
+        if (two) {
+          const S v2 = R.y * xscale(sc, r0 + 1, a, m0);
+          o[m0] = sc.accum ? o[m0] + v2 : v2;
+        }
       }
     };
     auto none = [&](int, int, int) { return mk(0.0, 0.0); };
@@ -295,7 +303,8 @@ __global__ void __launch_bounds__(256) xform_direct_kernel(const S* __restrict__
       q = sinpi((double)(((long long)(a + 1) * (J + 1)) % P) / (double)(m0 + 1));
     acc = fma_(q, row[J], acc);
   }
-  out[(size_t)r * m0 + a] = scale(acc, xscale(sc, r, a, m0));
+  const S v = scale(acc, xscale(sc, r, a, m0));
+  out[(size_t)r * m0 + a] = sc.accum ? add(out[(size_t)r * m0 + a], v) : v;
 }
 
 // out[b][x][y] = in[b][y][x]  (32 x 32 tiles through shared memory)
@@ -318,12 +327,12 @@ __global__ void __launch_bounds__(256) transpose_kernel(const S* __restrict__ in
 
 template <typename S>
 void launch_xform(const helm_plan* P, const S* in, S* out, const double* sig, bool scale2d, int batch,
-                  cudaStream_t st) {
+                  cudaStream_t st, bool accumulate) {
   HELM_CHECK((const void*)in != (const void*)out, "xform: input and output must not alias");
   const PlanDev& d = P->dev;
   const int m0 = d.m0, rows = m0 * batch, dct = P->geo.sommerfeld;
-  XScale sc{sig, nullptr, nullptr, 0.0, 0.0};
-  if (scale2d) sc = XScale{nullptr, d.coarse_lamT, d.coarse_lamM, P->geo.k2, d.coarse_qn};
+  XScale sc{accumulate ? 1 : 0, sig, nullptr, nullptr, 0.0, 0.0};
+  if (scale2d) sc = XScale{accumulate ? 1 : 0, nullptr, d.coarse_lamT, d.coarse_lamM, P->geo.k2, d.coarse_qn};
   if (d.fft_len) {
     const int L = d.fft_len;
     fft_launch<S, 8>(in, out, sc, rows, m0, L, dct, d.twiddle, st);
@@ -342,7 +351,7 @@ void launch_transpose(const S* in, S* out, int m, int batch, cudaStream_t st) {
 }
 
 #define HELM_INST(S)                                                                                          \
-  template void launch_xform<S>(const helm_plan*, const S*, S*, const double*, bool, int, cudaStream_t);       \
+  template void launch_xform<S>(const helm_plan*, const S*, S*, const double*, bool, int, cudaStream_t, bool); \
   template void launch_transpose<S>(const S*, S*, int, int, cudaStream_t);
 HELM_INST(double)
 HELM_INST(double2)
