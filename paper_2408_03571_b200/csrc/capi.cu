@@ -109,8 +109,22 @@ static void gmres_impl(const helm_plan* P, helm_workspace* ws, const S* b, S* x,
   HELM_CHECK(side == 0 || side == 1, "side must be 0 (right) or 1 (left)");
   const size_t N = (size_t)P->N;
   const bool left = side == 1;
-  DevBuf<S> V((size_t)(mi + 1) * N, st), H((size_t)(mi + 1) * mi, st), cs(mi, st), sn(mi, st), g(mi + 1, st),
+  // The Krylov basis grows on demand (capacity doubling, contiguous so the CGS2
+  // kernels see one [vectors][N] array): the reference allocates (cap+1) N eagerly
+  // (gmres.py:88-89), which at n=2049 and cap 1000 would be 67 GB.
+  int vcap = std::min(mi + 1, 32);
+  DevBuf<S> V((size_t)vcap * N, st), H((size_t)(mi + 1) * mi, st), cs(mi, st), sn(mi, st), g(mi + 1, st),
       y(mi + 1, st), u(N, st), r(N, st);
+  auto ensure_basis = [&](int nvec) {
+    if (nvec <= vcap) return;
+    const int ncap = std::min(mi + 1, std::max(nvec, 2 * vcap));
+    S* np = nullptr;
+    HELM_CUDA(cudaMallocAsync((void**)&np, (size_t)ncap * N * sizeof(S), st));
+    HELM_CUDA(cudaMemcpyAsync(np, V.p, (size_t)vcap * N * sizeof(S), cudaMemcpyDeviceToDevice, st));
+    HELM_CUDA(cudaFreeAsync(V.p, st));
+    V.p = np;
+    vcap = ncap;
+  };
   DevBuf<char> scratch(krylov_scratch_bytes(mi + 1), st);
   DevBuf<double> scal(16, st);
   HELM_CUDA(cudaMemsetAsync(H.p, 0, (size_t)(mi + 1) * mi * sizeof(S), st));
@@ -175,6 +189,7 @@ static void gmres_impl(const helm_plan* P, helm_workspace* ws, const S* b, S* x,
 
   bool done = false;
   for (int j = 0; j < mi && !done; ++j) {
+    ensure_basis(j + 2);
     S* vj = V.p + (size_t)j * N;
     applyOp(vj, vj + N);
     krylov_cgs2_impl<S>(V.p, j, N, N, H.p + j, (size_t)mi, scal.p + 2, scratch.p, st);
