@@ -366,7 +366,7 @@ static void build_plan(const helm_desc* d, helm_plan* P) {
   // are packed at [0, 18) and odd modes at [18, 36) of a 36 x 36 table (local_fast.cu)
   constexpr int FT = 36, FH = 18;
   std::vector<int> cfold(d->n_classes, 0);
-  std::vector<double> vf((size_t)d->n_classes * FT * FT, 0.0), lf((size_t)d->n_classes * FT, 1.0);
+  std::vector<double> vf((size_t)d->n_classes * FT * FT, 0.0), lf((size_t)d->n_classes * FT, 1e30);  // pad: x / 1e30 = 0
   for (int c = 0; c < d->n_classes; ++c) {
     const int L = P->h_class_len[c];
     if (!creal[c] || L > FT) continue;

@@ -210,12 +210,25 @@ __global__ void __launch_bounds__(256) a0_residual_kernel(const S* __restrict__ 
   const int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
   const int V0 = blockIdx.x * RSX, U0 = blockIdx.y * RSY;
   const size_t off = (size_t)blockIdx.z * m0 * m0;
-  for (int rr = ty; rr < RSY + 4; rr += 8) {
-    const int U = U0 + rr - 2;
-    for (int q = tx; q < RSX + 4; q += 32) {
-      const int W = V0 + q - 2;
-      ys[rr][q] = (U >= 0 && U < m0 && W >= 0 && W < m0) ? y[off + (size_t)U * m0 + W] : Sc<S>::zero();
-    }
+  {  // all of the thread's window loads in flight at once
+    constexpr int NR = (RSY + 4 + 7) / 8, NC = (RSX + 4 + 31) / 32;
+    S v[NR][NC];
+#pragma unroll
+    for (int i = 0; i < NR; ++i)
+#pragma unroll
+      for (int j = 0; j < NC; ++j) {
+        const int rr = ty + 8 * i, q = tx + 32 * j, U = U0 + rr - 2, W = V0 + q - 2;
+        v[i][j] = (rr < RSY + 4 && q < RSX + 4 && U >= 0 && U < m0 && W >= 0 && W < m0)
+                      ? y[off + (size_t)U * m0 + W]
+                      : Sc<S>::zero();
+      }
+#pragma unroll
+    for (int i = 0; i < NR; ++i)
+#pragma unroll
+      for (int j = 0; j < NC; ++j) {
+        const int rr = ty + 8 * i, q = tx + 32 * j;
+        if (rr < RSY + 4 && q < RSX + 4) ys[rr][q] = v[i][j];
+      }
   }
   const int V = V0 + tx;
   S bm[5], bt[5];

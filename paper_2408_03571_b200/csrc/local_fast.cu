@@ -215,9 +215,11 @@ __device__ __forceinline__ void tile_product_fold(int k0n, int k1n, GA ga, GB gb
   if (act) {
 #pragma unroll
     for (int blk = 0; blk < 2; ++blk) {
-      const int kb = blk * HB, kn = blk ? k1n : k0n;
-#pragma unroll 2
-      for (int kk = 0; kk < kn; ++kk) {
+      // full HB-length blocks (the padding of Vf and of the folded tile is zero):
+      // a compile-time trip count, unrolled by 3
+      const int kb = blk * HB;
+#pragma unroll 3
+      for (int kk = 0; kk < HB; ++kk) {
         const int k = kb + kk;
         if constexpr (LEFT) {  // rows of block blk: i = 2 blk, 2 blk + 1; all 4 columns
           decltype(ga(0, 0)) av[2];
@@ -314,10 +316,11 @@ __global__ void __launch_bounds__(LTH) local_fdm_fold_kernel(const S* __restrict
       const S a01 = cj ? Sc<S>::zero() : ld(i, Lx - 1 - j);
       const S a11 = (ci || cj) ? Sc<S>::zero() : ld(Ly - 1 - i, Lx - 1 - j);
       const S sy0 = add(a00, a10), dy0 = sub(a00, a10), sy1 = add(a01, a11), dy1 = sub(a01, a11);
+      // the d components of a centre row / column are exactly zero (the padded K range reads them)
       f4[u][0] = add(sy0, sy1);
-      f4[u][1] = sub(sy0, sy1);
-      f4[u][2] = add(dy0, dy1);
-      f4[u][3] = sub(dy0, dy1);
+      f4[u][1] = cj ? Sc<S>::zero() : sub(sy0, sy1);
+      f4[u][2] = ci ? Sc<S>::zero() : add(dy0, dy1);
+      f4[u][3] = (ci || cj) ? Sc<S>::zero() : sub(dy0, dy1);
     }
   }
   __syncthreads();  // (X is not read before here; the barrier orders the V loads too)

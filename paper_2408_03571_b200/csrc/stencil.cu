@@ -58,39 +58,58 @@ __global__ void __launch_bounds__(256) stencil_kernel(const S* __restrict__ x, c
 // A CTA computes a TY x TX coarse tile.  The (2TY+3) x (2TX+3) fine window is
 // staged in shared memory (zero outside the unknown set = dropped taps), then
 // the separable 5-tap stencil runs as an x-pass and a y-pass in smem.
-constexpr int RTX = 32, RTY = 8;
+constexpr int RTX = 32, RTY = 16;
+constexpr int RFW = 2 * RTX + 3, RFH = 2 * RTY + 3;  // fine window of a coarse tile
 template <typename S>
 __global__ void __launch_bounds__(256) restrict_kernel(const S* __restrict__ x, S* __restrict__ c, Geo g) {
-  constexpr int FW = 2 * RTX + 3, FH = 2 * RTY + 3;
-  __shared__ S fin[FH][FW];
-  __shared__ S tmp[FH][RTX];
+  // 32 x 16 coarse outputs per CTA (32 x 8 threads, 2 rows each); the 67 x 35 fine
+  // window is loaded with all of a thread's loads in flight at once (registers),
+  // then the separable 5-tap x-pass and y-pass run from shared memory.
+  extern __shared__ __align__(16) unsigned char sraw[];
+  S (*fin)[RFW] = reinterpret_cast<S (*)[RFW]>(sraw);
+  S (*tmp)[RTX] = reinterpret_cast<S (*)[RTX]>(fin + RFH);
   const double w[5] = {0.125, 0.5, 0.75, 0.5, 0.125};
   const int nu = g.nu, m0 = g.m0;
   const int U0 = blockIdx.y * RTY, V0 = blockIdx.x * RTX;
   const int u0 = 2 * U0 + g.off - 2, v0 = 2 * V0 + g.off - 2;  // fine origin of the window
   const S* xb = x + (size_t)blockIdx.z * nu * nu;
-  const int tid = threadIdx.y * blockDim.x + threadIdx.x;
-  for (int e = tid; e < FH * FW; e += blockDim.x * blockDim.y) {
-    const int r = e / FW, q = e % FW;
-    const int u = u0 + r, v = v0 + q;
-    fin[r][q] = (u >= 0 && u < nu && v >= 0 && v < nu) ? xb[(size_t)u * nu + v] : Sc<S>::zero();
-  }
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  constexpr int NR = (RFH + 7) / 8, NC = (RFW + 31) / 32;
+  S v[NR][NC];
+#pragma unroll
+  for (int i = 0; i < NR; ++i)
+#pragma unroll
+    for (int j = 0; j < NC; ++j) {
+      const int r = ty + 8 * i, q = tx + 32 * j;
+      const int u = u0 + r, vv = v0 + q;
+      v[i][j] = (r < RFH && q < RFW && u >= 0 && u < nu && vv >= 0 && vv < nu) ? xb[(size_t)u * nu + vv]
+                                                                                  : Sc<S>::zero();
+    }
+#pragma unroll
+  for (int i = 0; i < NR; ++i)
+#pragma unroll
+    for (int j = 0; j < NC; ++j) {
+      const int r = ty + 8 * i, q = tx + 32 * j;
+      if (r < RFH && q < RFW) fin[r][q] = v[i][j];
+    }
   __syncthreads();
-  for (int e = tid; e < FH * RTX; e += blockDim.x * blockDim.y) {
-    const int r = e / RTX, q = e % RTX;
+  for (int r = ty; r < RFH; r += 8) {
     S a = Sc<S>::zero();
 #pragma unroll
-    for (int d = 0; d < 5; ++d) a = fma_(w[d], fin[r][2 * q + d], a);
-    tmp[r][q] = a;
+    for (int d = 0; d < 5; ++d) a = fma_(w[d], fin[r][2 * tx + d], a);
+    tmp[r][tx] = a;
   }
   __syncthreads();
-  const int q = threadIdx.x, r = threadIdx.y;
-  const int U = U0 + r, V = V0 + q;
-  if (U < m0 && V < m0) {
-    S a = Sc<S>::zero();
+  const int V = V0 + tx;
 #pragma unroll
-    for (int d = 0; d < 5; ++d) a = fma_(w[d], tmp[2 * r + d][q], a);
-    c[(size_t)blockIdx.z * m0 * m0 + (size_t)U * m0 + V] = a;
+  for (int i = 0; i < RTY / 8; ++i) {
+    const int r = ty + 8 * i, U = U0 + r;
+    if (U < m0 && V < m0) {
+      S a = Sc<S>::zero();
+#pragma unroll
+      for (int d = 0; d < 5; ++d) a = fma_(w[d], tmp[2 * r + d][tx], a);
+      c[(size_t)blockIdx.z * m0 * m0 + (size_t)U * m0 + V] = a;
+    }
   }
 }
 
@@ -151,8 +170,14 @@ void launch_stencil(const Geo& g, const S* x, const S* z, S* y, int batch, cudaS
 
 template <typename S>
 void launch_restrict(const Geo& g, const S* x, S* c, int batch, cudaStream_t st) {
-  dim3 blk(RTX, RTY), grd((g.m0 + RTX - 1) / RTX, (g.m0 + RTY - 1) / RTY, batch);
-  restrict_kernel<S><<<grd, blk, 0, st>>>(x, c, g);
+  const size_t smem = (size_t)(RFH * RFW + RFH * RTX) * sizeof(S);
+  static bool attr = false;
+  if (!attr) {
+    HELM_CUDA(cudaFuncSetAttribute(restrict_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = true;
+  }
+  dim3 blk(32, 8), grd((g.m0 + RTX - 1) / RTX, (g.m0 + RTY - 1) / RTY, batch);
+  restrict_kernel<S><<<grd, blk, smem, st>>>(x, c, g);
   HELM_LAUNCH_CHECK();
 }
 
@@ -202,6 +227,15 @@ __global__ void __launch_bounds__(256) prolong_deflate_kernel(const S* __restric
   const S* cb = c + (size_t)blockIdx.z * m0 * m0;
   const int Ub = floordiv2(u0 - 1 - g.off) - 1, Vb = floordiv2(v0 - 1 - g.off) - 1;
   const int tid = threadIdx.y * blockDim.x + threadIdx.x;
+  // this thread's x values are loaded first so their latency overlaps the z work
+  constexpr int RPT = PH / 8;
+  const int vx = v0 + threadIdx.x;
+  S xv[RPT];
+#pragma unroll
+  for (int i = 0; i < RPT; ++i) {
+    const int u = u0 + threadIdx.y + 8 * i;
+    xv[i] = (u < nu && vx < nu) ? x[boff + (size_t)u * nu + vx] : Sc<S>::zero();
+  }
   for (int e = tid; e < PCH * PCW; e += 256) {
     const int rr = e / PCW, q = e % PCW;
     const int U = Ub + rr, V = Vb + q;
@@ -226,17 +260,17 @@ __global__ void __launch_bounds__(256) prolong_deflate_kernel(const S* __restric
     zs[rr][q] = acc;
   }
   __syncthreads();
-  const int v = v0 + threadIdx.x;
-  if (v >= nu) return;
-  for (int rr = threadIdx.y; rr < PH; rr += blockDim.y) {
-    const int u = u0 + rr;
+  if (vx >= nu) return;
+#pragma unroll
+  for (int i = 0; i < RPT; ++i) {
+    const int rr = threadIdx.y + 8 * i, u = u0 + rr;
     if (u >= nu) break;
     const S zc = zs[rr + 1][threadIdx.x + 1];
-    const S az = stencil_point<S>(g, v, u, zc, zs[rr][threadIdx.x + 1], zs[rr + 2][threadIdx.x + 1],
+    const S az = stencil_point<S>(g, vx, u, zc, zs[rr][threadIdx.x + 1], zs[rr + 2][threadIdx.x + 1],
                                   zs[rr + 1][threadIdx.x], zs[rr + 1][threadIdx.x + 2]);
-    const size_t p = boff + (size_t)u * nu + v;
+    const size_t p = boff + (size_t)u * nu + vx;
     z[p] = zc;
-    d[p] = sub(x[p], az);
+    d[p] = sub(xv[i], az);
   }
 }
 
