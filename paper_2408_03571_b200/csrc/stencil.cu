@@ -65,9 +65,13 @@ __global__ void __launch_bounds__(256) restrict_kernel(const S* __restrict__ x, 
   // 32 x 16 coarse outputs per CTA (32 x 8 threads, 2 rows each); the 67 x 35 fine
   // window is loaded with all of a thread's loads in flight at once (registers),
   // then the separable 5-tap x-pass and y-pass run from shared memory.
+  // the window is stored as even and odd column planes, so the stride-2 taps of the
+  // x-pass are consecutive (bank-conflict free) across the warp
   extern __shared__ __align__(16) unsigned char sraw[];
-  S (*fin)[RFW] = reinterpret_cast<S (*)[RFW]>(sraw);
-  S (*tmp)[RTX] = reinterpret_cast<S (*)[RTX]>(fin + RFH);
+  constexpr int HW = (RFW + 1) / 2;
+  S (*fev)[HW] = reinterpret_cast<S (*)[HW]>(sraw);
+  S (*fod)[HW] = fev + RFH;
+  S (*tmp)[RTX] = reinterpret_cast<S (*)[RTX]>(fod + RFH);
   const double w[5] = {0.125, 0.5, 0.75, 0.5, 0.125};
   const int nu = g.nu, m0 = g.m0;
   const int U0 = blockIdx.y * RTY, V0 = blockIdx.x * RTX;
@@ -90,13 +94,16 @@ __global__ void __launch_bounds__(256) restrict_kernel(const S* __restrict__ x, 
 #pragma unroll
     for (int j = 0; j < NC; ++j) {
       const int r = ty + 8 * i, q = tx + 32 * j;
-      if (r < RFH && q < RFW) fin[r][q] = v[i][j];
+      if (r < RFH && q < RFW) (q & 1 ? fod : fev)[r][q >> 1] = v[i][j];
     }
   __syncthreads();
   for (int r = ty; r < RFH; r += 8) {
     S a = Sc<S>::zero();
-#pragma unroll
-    for (int d = 0; d < 5; ++d) a = fma_(w[d], fin[r][2 * tx + d], a);
+    a = fma_(w[0], fev[r][tx], a);
+    a = fma_(w[1], fod[r][tx], a);
+    a = fma_(w[2], fev[r][tx + 1], a);
+    a = fma_(w[3], fod[r][tx + 1], a);
+    a = fma_(w[4], fev[r][tx + 2], a);
     tmp[r][tx] = a;
   }
   __syncthreads();
@@ -170,7 +177,7 @@ void launch_stencil(const Geo& g, const S* x, const S* z, S* y, int batch, cudaS
 
 template <typename S>
 void launch_restrict(const Geo& g, const S* x, S* c, int batch, cudaStream_t st) {
-  const size_t smem = (size_t)(RFH * RFW + RFH * RTX) * sizeof(S);
+  const size_t smem = (size_t)(2 * RFH * ((RFW + 1) / 2) + RFH * RTX) * sizeof(S);
   static bool attr = false;
   if (!attr) {
     HELM_CUDA(cudaFuncSetAttribute(restrict_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
