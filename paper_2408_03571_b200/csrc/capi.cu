@@ -363,8 +363,8 @@ static void build_plan(const helm_desc* d, helm_plan* P) {
   dv.class_real = upload<int>(creal.data(), creal.size());
   dv.class_Vr = upload<double>(vr.data(), vr.size());
   // folded (symmetric) real classes: V[L-1-j][k] = sigma_k V[j][k]; even modes (sigma = +1)
-  // are packed at [0, 18) and odd modes at [18, 36) of a 36 x 36 table (local_fast.cu)
-  constexpr int FT = 36, FH = 18;
+  // are packed at [0, 20) and odd modes at [20, 40) of a 40 x 40 table (local_dmma.cu)
+  constexpr int FT = 40, FH = 20;
   std::vector<int> cfold(d->n_classes, 0);
   std::vector<double> vf((size_t)d->n_classes * FT * FT, 0.0), lf((size_t)d->n_classes * FT, 1e30);  // pad: x / 1e30 = 0
   for (int c = 0; c < d->n_classes; ++c) {
@@ -407,6 +407,19 @@ static void build_plan(const helm_desc* d, helm_plan* P) {
   dv.box_mix = upload<int>(mix.data(), mix.size());
   dv.class_Vf = upload<double>(vf.data(), vf.size());
   dv.class_lamf = upload<double>(lf.data(), lf.size());
+  // reciprocal eigenvalue sums per folded class pair: 1 / (lf_y[m] + lf_x[n] - k^2), padding 0
+  std::vector<double> inv((size_t)d->n_classes * d->n_classes * FT * FT, 0.0);
+  for (int cy = 0; cy < d->n_classes; ++cy)
+    for (int cx = 0; cx < d->n_classes; ++cx) {
+      if (!cfold[cy] || !cfold[cx]) continue;
+      for (int m = 0; m < FT; ++m)
+        for (int nn = 0; nn < FT; ++nn) {
+          const double ly = lf[(size_t)cy * FT + m], lx = lf[(size_t)cx * FT + nn];
+          if (ly > 1e29 || lx > 1e29) continue;
+          inv[(((size_t)cy * d->n_classes + cx) * FT + m) * FT + nn] = 1.0 / (ly + lx - d->k * d->k);
+        }
+    }
+  dv.class_invden = upload<double>(inv.data(), inv.size());
   dv.node_first_box = upload<int>(first.data(), nu);
   dv.node_mult = upload<int>(mult.data(), nu);
   dv.node_band = upload<int>(band.data(), nu);
@@ -426,7 +439,7 @@ static void finish_desc(helm_plan* P) {
 static void free_plan(helm_plan* P) {
   PlanDev& dv = P->dev;
   void* ptrs[] = {dv.box_start, dv.box_len, dv.box_class, dv.class_len, dv.class_off_V, dv.class_off_lam,
-                  dv.class_V, dv.class_lambda, dv.class_real, dv.class_Vr, dv.box_ff, dv.class_Vf, dv.class_lamf, dv.box_rr, dv.box_mix,
+                  dv.class_V, dv.class_lambda, dv.class_real, dv.class_Vr, dv.box_ff, dv.class_Vf, dv.class_lamf, dv.class_invden, dv.box_rr, dv.box_mix,
                   dv.node_first_box, dv.node_mult, dv.node_band, dv.band_node,
                   dv.coarse_scale, dv.twiddle, dv.coarse_lamT, dv.coarse_lamM, dv.t0_band, dv.m0_band, dv.band_piv, dv.band_l, dv.band_u, dv.strip_q,
                   dv.cap_left, dv.cap_right, dv.cap_mode};

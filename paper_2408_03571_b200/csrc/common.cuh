@@ -149,8 +149,9 @@ struct PlanDev {
   double* class_Vr;
   int* box_ff;         // subdomain ids (ay * p + ax) whose two classes are real and symmetric (folded FDM)
   int n_ff;
-  double* class_Vf;    // [n_classes][36][36] folded eigenvectors (even modes | odd modes)
-  double* class_lamf;  // [n_classes][36] eigenvalues in the folded mode order (padding 1)
+  double* class_Vf;    // [n_classes][40][40] folded eigenvectors (even modes | odd modes)
+  double* class_lamf;  // [n_classes][40] eigenvalues in the folded mode order (padding 1e30)
+  double* class_invden; // [n_classes][n_classes][40][40] 1 / (lamf_y + lamf_x - k^2), padding 0
   int* box_rr;         // other subdomains whose two classes are real
   int n_rr;
   int* box_mix;        // the other subdomains

@@ -28,4 +28,9 @@ template <typename S>
 bool launch_local_fast(const helm_plan* P, const S* x, const S* base, S* y, S* ovl, const LocalArgs& a, int batch,
                        cudaStream_t st);
 
+// Folded boxes (both classes real and symmetric) on the FP64 tensor pipe (local_dmma.cu).
+template <typename S>
+void launch_local_dmma(const helm_plan* P, const S* x, const S* base, S* y, S* ovl, const LocalArgs& a, int batch,
+                       cudaStream_t st);
+
 }  // namespace helm

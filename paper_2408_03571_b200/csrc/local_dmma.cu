@@ -1,0 +1,295 @@
+// K4, FP64 tensor-core path: folded fast diagonalisation of the subdomain solves
+// (reference: the p^2 SuperLU solves of SchwarzPreconditioner._local_sum,
+// schwarz.py:64-74, on R_i A R_i^T, decomposition.py:157-160).
+//
+//   Y_i = V_y [ (V_y^T X_i V_x) ./ (lam_y (+) lam_x - k^2) ] V_x^T
+//
+// For boxes whose two 1-D classes are real and symmetric (V[L-1-j][k] = +-V[j][k]:
+// the interior middle class and every MP-1 class) the box is folded along both axes
+// (s_j = x_j + x_{L-1-j}, d_j = x_j - x_{L-1-j}; even modes see only s, odd modes
+// only d), so each 1-D transform is block diagonal with two blocks of DB = 20 (padded).
+// The four products then run on the FP64 tensor pipe as mma.sync.m8n8k4.f64 (DMMA):
+// complex data is a real matrix with interleaved (re, im) columns (LEFT products) or
+// rows (RIGHT products), V stays real.  One CTA (3 warps) owns one (box, right-hand
+// side); each warp keeps 20 accumulator tiles (8 x 8) in registers, reuses one operand
+// fragment across 10 tiles per k step, and the products update the shared tile in
+// place across a barrier.  Shared strides are chosen so every fragment load is two
+// wavefronts (the minimum for 32 x 8-byte accesses).
+#include "local.cuh"
+
+namespace helm {
+
+constexpr int DB = 20;      // folded block (even / odd modes)
+constexpr int DT = 2 * DB;  // tile side
+constexpr int DVL = 41;     // V leading dimension (doubles)
+constexpr int DTH = 96;     // 3 warps
+
+template <int NP> struct DmmaDims {
+  static constexpr int XL = NP == 2 ? 88 : 40;  // X leading dimension (doubles), = 8 (mod 16)
+  static constexpr int NT = DT * NP / 8;        // real column tiles (LEFT) / real row tiles (RIGHT)
+};
+
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+// LEFT product  X <- V' X  with V'(m, k) = TRANS ? V[k][m] : V[m][k], block diagonal:
+// rows of block b use k in [b DB, b DB + DB).  Warp w owns row tiles (b, w) for b = 0, 1
+// and all NT real-column tiles.  EPI(m, c, v) stores one result element.
+template <int NP, bool TRANS, typename EPI>
+__device__ __forceinline__ void dmma_left(double* Xr, const double* V, EPI epi) {
+  constexpr int XL = DmmaDims<NP>::XL, NT = DmmaDims<NP>::NT;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int g = lane >> 2, q = lane & 3;
+  double acc[2][NT][2];
+#pragma unroll
+  for (int b = 0; b < 2; ++b)
+#pragma unroll
+    for (int t = 0; t < NT; ++t) acc[b][t][0] = acc[b][t][1] = 0.0;
+#pragma unroll
+  for (int b = 0; b < 2; ++b) {
+    const int m = b * DB + w * 8 + g;  // A row of this lane (may run into the next block: discarded)
+#pragma unroll
+    for (int ks = 0; ks < DB / 4; ++ks) {
+      const int k = b * DB + ks * 4 + q;
+      const double a = (m < DT) ? (TRANS ? V[k * DVL + m] : V[m * DVL + k]) : 0.0;
+#pragma unroll
+      for (int t = 0; t < NT; ++t) dmma(acc[b][t][0], acc[b][t][1], a, Xr[k * XL + t * 8 + g]);
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int b = 0; b < 2; ++b) {
+    const int ml = w * 8 + g;
+    if (ml < DB) {
+#pragma unroll
+      for (int t = 0; t < NT; ++t) {
+        epi(b * DB + ml, t * 8 + 2 * q, acc[b][t][0]);
+        epi(b * DB + ml, t * 8 + 2 * q + 1, acc[b][t][1]);
+      }
+    }
+  }
+}
+
+// RIGHT product  X <- X V'  with V'(k, n) = TRANS ? V[n][k] : V[k][n], block diagonal in
+// the columns.  Real rows r = (m, part) read X[m][k NP + part].  Warp w owns column tiles
+// (b, w) for b = 0, 1 and all NT real-row tiles.  EPI(m, part, n, v) stores one element.
+template <int NP, bool TRANS, typename EPI>
+__device__ __forceinline__ void dmma_right(double* Xr, const double* V, EPI epi) {
+  constexpr int XL = DmmaDims<NP>::XL, NT = DmmaDims<NP>::NT;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int g = lane >> 2, q = lane & 3;
+  double acc[2][NT][2];
+#pragma unroll
+  for (int b = 0; b < 2; ++b)
+#pragma unroll
+    for (int t = 0; t < NT; ++t) acc[b][t][0] = acc[b][t][1] = 0.0;
+#pragma unroll
+  for (int b = 0; b < 2; ++b) {
+    const int n = b * DB + w * 8 + g;  // B column of this lane
+#pragma unroll
+    for (int ks = 0; ks < DB / 4; ++ks) {
+      const int k = b * DB + ks * 4 + q;
+      const double bv = (n < DT) ? (TRANS ? V[n * DVL + k] : V[k * DVL + n]) : 0.0;
+#pragma unroll
+      for (int t = 0; t < NT; ++t) {
+        const int r = t * 8 + g;  // A row (real row) of this lane
+        dmma(acc[b][t][0], acc[b][t][1], Xr[(r / NP) * XL + k * NP + (r % NP)], bv);
+      }
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int b = 0; b < 2; ++b) {
+#pragma unroll
+    for (int t = 0; t < NT; ++t) {
+      const int r = t * 8 + g;
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int nl = w * 8 + 2 * q + e;
+        if (nl < DB) epi(r / NP, r % NP, b * DB + nl, acc[b][t][e]);
+      }
+    }
+  }
+}
+
+template <typename S>
+__global__ void __launch_bounds__(DTH) local_fdm_dmma_kernel(const S* __restrict__ x, const S* __restrict__ base,
+                                                             S* __restrict__ y, S* __restrict__ ovl,
+                                                             const int* __restrict__ boxes,
+                                                             const double* __restrict__ classVf,
+                                                             const double* __restrict__ classInvden, int ncls,
+                                                             LocalArgs a) {
+  constexpr int NP = Sc<S>::cplx ? 2 : 1;
+  constexpr int XL = DmmaDims<NP>::XL;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double* Xr = reinterpret_cast<double*>(smem_raw);  // [DT][XL]
+  double* Vy = Xr + DT * XL;                           // [DT][DVL]
+  double* Vx = Vy + DT * DVL;
+  int* meta = reinterpret_cast<int*>(Vx + DT * DVL);  // [2][3][DT]: multiplicity, first box, band per row / column
+  const int sid = boxes[blockIdx.x];
+  const int ay = sid / a.p, ax = sid % a.p;
+  const int nu = a.nu;
+  const size_t N = (size_t)nu * nu;
+  const int b = blockIdx.y;
+  const int cy = a.box_class[ay], cx = a.box_class[ax];
+  const int y0 = a.box_start[ay], Ly = a.box_len[ay];
+  const int x0 = a.box_start[ax], Lx = a.box_len[ax];
+  const int hy = Ly / 2, hpy = (Ly + 1) / 2, hx = Lx / 2, hpx = (Lx + 1) / 2;
+  const S* xb = x + (size_t)b * N;
+  const S* bb = base ? base + (size_t)b * N : nullptr;
+  S* yb = y + (size_t)b * N;
+  S* ob = ovl + (size_t)b * 6 * a.nbands * nu;
+  // gather + fold both axes: pair (i, j) of the half-box -> the 4 folded entries
+  // (s_y s_x) [i][j], (s_y d_x) [i][DB+j], (d_y s_x) [DB+i][j], (d_y d_x) [DB+i][DB+j]
+  const bool wb = a.weighted && a.wbs;
+  auto ld = [&](int r, int q) {
+    S v = xb[(size_t)(y0 + r) * nu + x0 + q];
+    if (wb) v = scale(v, 1.0 / (a.node_mult[y0 + r] * a.node_mult[x0 + q]));
+    return v;
+  };
+  constexpr int PPT = (DB * DB + DTH - 1) / DTH;  // pairs per thread
+  S f4[PPT][4];
+#pragma unroll
+  for (int u = 0; u < PPT; ++u) {
+    const int e = threadIdx.x + u * DTH;
+    const int i = e / DB, j = e % DB;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) f4[u][c] = Sc<S>::zero();
+    if (e < DB * DB && i < hpy && j < hpx) {
+      const bool ci = i == hy, cj = j == hx;  // centre row / column (odd length)
+      const S a00 = ld(i, j);
+      const S a10 = ci ? Sc<S>::zero() : ld(Ly - 1 - i, j);
+      const S a01 = cj ? Sc<S>::zero() : ld(i, Lx - 1 - j);
+      const S a11 = (ci || cj) ? Sc<S>::zero() : ld(Ly - 1 - i, Lx - 1 - j);
+      const S sy0 = add(a00, a10), dy0 = sub(a00, a10), sy1 = add(a01, a11), dy1 = sub(a01, a11);
+      f4[u][0] = add(sy0, sy1);
+      f4[u][1] = cj ? Sc<S>::zero() : sub(sy0, sy1);
+      f4[u][2] = ci ? Sc<S>::zero() : add(dy0, dy1);
+      f4[u][3] = (ci || cj) ? Sc<S>::zero() : sub(dy0, dy1);
+    }
+  }
+  {  // folded V tables (zero padded by the plan)
+    const double* vyg = classVf + (size_t)cy * DT * DT;
+    const double* vxg = classVf + (size_t)cx * DT * DT;
+    for (int r = threadIdx.x / 8; r < DT; r += DTH / 8)
+      for (int c = threadIdx.x % 8; c < DT; c += 8) {
+        Vy[r * DVL + c] = vyg[r * DT + c];
+        Vx[r * DVL + c] = vxg[r * DT + c];
+      }
+    // the box's per-row / per-column overlap bookkeeping (decomposition.py:111-134)
+    for (int e = threadIdx.x; e < DT; e += DTH) {
+      const int iy = y0 + (e < Ly ? e : 0), ix = x0 + (e < Lx ? e : 0);
+      meta[0 * DT + e] = a.node_mult[iy];
+      meta[1 * DT + e] = a.node_first_box[iy];
+      meta[2 * DT + e] = a.node_band[iy];
+      meta[3 * DT + e] = a.node_mult[ix];
+      meta[4 * DT + e] = a.node_first_box[ix];
+      meta[5 * DT + e] = a.node_band[ix];
+    }
+  }
+  const double* invden = classInvden + (size_t)(cy * ncls + cx) * DT * DT;
+  auto put_s = [&](int i, int j, S v) {
+    if constexpr (NP == 2) {
+      Xr[i * XL + 2 * j] = v.x;
+      Xr[i * XL + 2 * j + 1] = v.y;
+    } else {
+      Xr[i * XL + j] = v;
+    }
+  };
+#pragma unroll
+  for (int u = 0; u < PPT; ++u) {
+    const int e = threadIdx.x + u * DTH;
+    if (e < DB * DB) {
+      const int i = e / DB, j = e % DB;
+      put_s(i, j, f4[u][0]);
+      put_s(i, DB + j, f4[u][1]);
+      put_s(DB + i, j, f4[u][2]);
+      put_s(DB + i, DB + j, f4[u][3]);
+    }
+  }
+  __syncthreads();
+  // X <- Vfy^T X
+  dmma_left<NP, true>(Xr, Vy, [&](int m, int c, double v) { Xr[m * XL + c] = v; });
+  __syncthreads();
+  // X <- (X Vfx) ./ (lfy (+) lfx - k^2)
+  dmma_right<NP, false>(Xr, Vx, [&](int m, int part, int n, double v) {
+    Xr[m * XL + n * NP + part] = v * invden[m * DT + n];  // 1 / (lfy[m] + lfx[n] - k^2), plan table
+  });
+  __syncthreads();
+  // X <- Vfy X
+  dmma_left<NP, false>(Xr, Vy, [&](int m, int c, double v) { Xr[m * XL + c] = v; });
+  __syncthreads();
+  // X <- X Vfx^T
+  dmma_right<NP, true>(Xr, Vx, [&](int m, int part, int n, double v) { Xr[m * XL + n * NP + part] = v; });
+  __syncthreads();
+  // unfold into a natural-order tile (the V tables are dead now: reuse their space),
+  // x_i = e_i + o_i, x_{L-1-i} = e_i - o_i on both axes ...
+  S* Y = reinterpret_cast<S*>(Vy);  // [Ly][Lx]
+  auto get = [&](int i, int j) -> S {
+    if constexpr (NP == 2) return mk(Xr[i * XL + 2 * j], Xr[i * XL + 2 * j + 1]);
+    else return Xr[i * XL + j];
+  };
+  for (int e = threadIdx.x; e < hpy * hpx; e += DTH) {
+    const int i = e / hpx, j = e % hpx;
+    const bool ci = i == hy, cj = j == hx;
+    const S ee = get(i, j);
+    const S eo = cj ? Sc<S>::zero() : get(i, DB + j);
+    const S oe = ci ? Sc<S>::zero() : get(DB + i, j);
+    const S oo = (ci || cj) ? Sc<S>::zero() : get(DB + i, DB + j);
+    const S ry0 = add(ee, oe), ry1 = sub(ee, oe);  // row i / row L-1-i, still split in x
+    const S rz0 = add(eo, oo), rz1 = sub(eo, oo);
+    Y[i * Lx + j] = add(ry0, rz0);
+    if (!cj) Y[i * Lx + Lx - 1 - j] = sub(ry0, rz0);
+    if (!ci) Y[(Ly - 1 - i) * Lx + j] = add(ry1, rz1);
+    if (!ci && !cj) Y[(Ly - 1 - i) * Lx + Lx - 1 - j] = sub(ry1, rz1);
+  }
+  __syncthreads();
+  // ... then weight and write row by row (coalesced; the overlap rows / columns of the
+  // box go to their slot of the scratch that the combine kernels sum)
+  for (int e = threadIdx.x; e < Ly * Lx; e += DTH) {
+    const int r = e / Lx, q = e % Lx;
+    S acc = Y[e];
+    const int my = meta[r], mx = meta[3 * DT + q];
+    if (a.weighted && !a.wbs) acc = scale(acc, 1.0 / (my * mx));
+    const int iy = y0 + r, ix = x0 + q;
+    const size_t pidx = (size_t)iy * nu + ix;
+    if (my == 1 && mx == 1) {
+      yb[pidx] = bb ? add(bb[pidx], acc) : acc;
+    } else if (my == 2) {
+      const int ry = ay - meta[DT + r], rx = ax - meta[4 * DT + q];
+      ob[((size_t)(ry * 2 + rx) * a.nbands + meta[2 * DT + r]) * nu + ix] = acc;
+    } else {
+      const int rx = ax - meta[4 * DT + q];
+      ob[(size_t)4 * a.nbands * nu + ((size_t)rx * nu + iy) * a.nbands + meta[5 * DT + q]] = acc;
+    }
+  }
+}
+
+template <typename S>
+void launch_local_dmma(const helm_plan* P, const S* x, const S* base, S* y, S* ovl, const LocalArgs& a, int batch,
+                       cudaStream_t st) {
+  const PlanDev& d = P->dev;
+  if (d.n_ff == 0) return;
+  constexpr int NP = Sc<S>::cplx ? 2 : 1;
+  const size_t smem = (size_t)(DT * DmmaDims<NP>::XL + 2 * DT * DVL) * sizeof(double) + 6 * DT * sizeof(int);
+  static bool attr = false;
+  if (!attr) {
+    HELM_CUDA(cudaFuncSetAttribute(local_fdm_dmma_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)smem));
+    attr = true;
+  }
+  dim3 grd(d.n_ff, batch);
+  local_fdm_dmma_kernel<S><<<grd, DTH, smem, st>>>(x, base, y, ovl, d.box_ff, d.class_Vf, d.class_invden,
+                                                   d.n_classes, a);
+  HELM_LAUNCH_CHECK();
+}
+
+template void launch_local_dmma<double>(const helm_plan*, const double*, const double*, double*, double*,
+                                        const LocalArgs&, int, cudaStream_t);
+template void launch_local_dmma<double2>(const helm_plan*, const double2*, const double2*, double2*, double2*,
+                                         const LocalArgs&, int, cudaStream_t);
+
+}  // namespace helm

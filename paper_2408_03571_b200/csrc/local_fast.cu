@@ -186,226 +186,6 @@ __global__ void __launch_bounds__(LTH) local_fdm_fast_kernel(const S* __restrict
   }
 }
 
-// ----------------------------------------------------------------------------
-// Folded FDM for boxes whose two classes are symmetric (V[L-1-j][k] = +-V[j][k]):
-// the middle class (DST-like eigenvectors) and every MP-1 class.  With
-// s_j = x_j + x_{L-1-j}, d_j = x_j - x_{L-1-j} (and s_c = x_c for odd L) the
-// even modes see only s and the odd modes only d, so each 1-D transform is a
-// block-diagonal product with two (L/2)-sized blocks: half the FP64 work and
-// half the shared-memory traffic of the plain product.  Layout of a folded
-// axis in the tile: s / even modes at [0, HB), d / odd modes at [HB, 2 HB).
-// Vf[j'][k'] (LT x LT, zero padded) and lamf[k'] are built once per class by
-// helm_plan_create.
-// ----------------------------------------------------------------------------
-constexpr int HB = LT / 2;
-
-// out(m, n) = sum_k A(m, k) B(k, n) with the k range of the block that owns m (LEFT)
-// or n (right); the thread's rows tm + 9i (cols tn + 9j) with i (j) in {0,1} lie in
-// block 0 and {2,3} in block 1.
-template <bool LEFT, typename TO, typename GA, typename GB, typename PUT>
-__device__ __forceinline__ void tile_product_fold(int k0n, int k1n, GA ga, GB gb, PUT put) {
-  const int t = threadIdx.x;
-  const int tm = LEFT ? t % 9 : t / 9, tn = LEFT ? t / 9 : t % 9;  // warp layout as in tile_product
-  const bool act = t < 81;
-  TO acc[4][4];
-#pragma unroll
-  for (int i = 0; i < 4; ++i)
-#pragma unroll
-    for (int j = 0; j < 4; ++j) acc[i][j] = Sc<TO>::zero();
-  if (act) {
-#pragma unroll
-    for (int blk = 0; blk < 2; ++blk) {
-      // full HB-length blocks (the padding of Vf and of the folded tile is zero):
-      // a compile-time trip count, unrolled by 3
-      const int kb = blk * HB;
-#pragma unroll 3
-      for (int kk = 0; kk < HB; ++kk) {
-        const int k = kb + kk;
-        if constexpr (LEFT) {  // rows of block blk: i = 2 blk, 2 blk + 1; all 4 columns
-          decltype(ga(0, 0)) av[2];
-          decltype(gb(0, 0)) bv[4];
-#pragma unroll
-          for (int i = 0; i < 2; ++i) av[i] = ga(tm + 9 * (2 * blk + i), k);
-#pragma unroll
-          for (int j = 0; j < 4; ++j) bv[j] = gb(k, tn + 9 * j);
-#pragma unroll
-          for (int i = 0; i < 2; ++i)
-#pragma unroll
-            for (int j = 0; j < 4; ++j) acc[2 * blk + i][j] = fma_(av[i], bv[j], acc[2 * blk + i][j]);
-        } else {  // columns of block blk: j = 2 blk, 2 blk + 1; all 4 rows
-          decltype(ga(0, 0)) av[4];
-          decltype(gb(0, 0)) bv[2];
-#pragma unroll
-          for (int i = 0; i < 4; ++i) av[i] = ga(tm + 9 * i, k);
-#pragma unroll
-          for (int j = 0; j < 2; ++j) bv[j] = gb(k, tn + 9 * (2 * blk + j));
-#pragma unroll
-          for (int i = 0; i < 4; ++i)
-#pragma unroll
-            for (int j = 0; j < 2; ++j) acc[i][2 * blk + j] = fma_(av[i], bv[j], acc[i][2 * blk + j]);
-        }
-      }
-    }
-  }
-  __syncthreads();
-  if (act) {
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-      for (int j = 0; j < 4; ++j) put(tm + 9 * i, tn + 9 * j, acc[i][j]);
-  }
-}
-
-template <typename S>
-__global__ void __launch_bounds__(LTH) local_fdm_fold_kernel(const S* __restrict__ x, const S* __restrict__ base,
-                                                             S* __restrict__ y, S* __restrict__ ovl,
-                                                             const int* __restrict__ boxes,
-                                                             const double* __restrict__ classVf,
-                                                             const double* __restrict__ classLamf, LocalArgs a) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  S* X = reinterpret_cast<S*>(smem_raw);
-  double* Vy = reinterpret_cast<double*>(X + LT * LTD);
-  double* Vx = Vy + LT * LTD;
-  double* ly = Vx + LT * LTD;
-  double* lx = ly + LT;
-  const int sid = boxes[blockIdx.x];
-  const int ay = sid / a.p, ax = sid % a.p;
-  const int nu = a.nu;
-  const size_t N = (size_t)nu * nu;
-  const int b = blockIdx.y;
-  const int cy = a.box_class[ay], cx = a.box_class[ax];
-  const int y0 = a.box_start[ay], Ly = a.box_len[ay];
-  const int x0 = a.box_start[ax], Lx = a.box_len[ax];
-  const int hy = Ly / 2, hpy = (Ly + 1) / 2, hx = Lx / 2, hpx = (Lx + 1) / 2;
-  const S* xb = x + (size_t)b * N;
-  const S* bb = base ? base + (size_t)b * N : nullptr;
-  S* yb = y + (size_t)b * N;
-  S* ob = ovl + (size_t)b * 6 * a.nbands * nu;
-  {
-    const double* vyg = classVf + (size_t)cy * LT * LT;
-    const double* vxg = classVf + (size_t)cx * LT * LT;
-    for (int e = threadIdx.x; e < LT * LT; e += LTH) {
-      Vy[(e / LT) * LTD + e % LT] = vyg[e];
-      Vx[(e / LT) * LTD + e % LT] = vxg[e];
-    }
-    for (int e = threadIdx.x; e < LT; e += LTH) {
-      ly[e] = classLamf[cy * LT + e];
-      lx[e] = classLamf[cx * LT + e];
-    }
-  }
-  // gather + fold both axes: pair (i, j) of the half-box -> the 4 folded entries
-  // (s_y s_x) [i][j], (s_y d_x) [i][HB+j], (d_y s_x) [HB+i][j], (d_y d_x) [HB+i][HB+j]
-  const bool wb = a.weighted && a.wbs;
-  auto ld = [&](int r, int q) {
-    S v = xb[(size_t)(y0 + r) * nu + x0 + q];
-    if (wb) v = scale(v, 1.0 / (a.node_mult[y0 + r] * a.node_mult[x0 + q]));
-    return v;
-  };
-  constexpr int PPT = (HB * HB + LTH - 1) / LTH;  // pairs per thread
-  S f4[PPT][4];
-#pragma unroll
-  for (int u = 0; u < PPT; ++u) {
-    const int e = threadIdx.x + u * LTH;
-    const int i = e / HB, j = e % HB;
-#pragma unroll
-    for (int c = 0; c < 4; ++c) f4[u][c] = Sc<S>::zero();
-    if (e < HB * HB && i < hpy && j < hpx) {
-      const bool ci = i == hy, cj = j == hx;  // centre row / column (odd length)
-      const S a00 = ld(i, j);
-      const S a10 = ci ? Sc<S>::zero() : ld(Ly - 1 - i, j);
-      const S a01 = cj ? Sc<S>::zero() : ld(i, Lx - 1 - j);
-      const S a11 = (ci || cj) ? Sc<S>::zero() : ld(Ly - 1 - i, Lx - 1 - j);
-      const S sy0 = add(a00, a10), dy0 = sub(a00, a10), sy1 = add(a01, a11), dy1 = sub(a01, a11);
-      // the d components of a centre row / column are exactly zero (the padded K range reads them)
-      f4[u][0] = add(sy0, sy1);
-      f4[u][1] = cj ? Sc<S>::zero() : sub(sy0, sy1);
-      f4[u][2] = ci ? Sc<S>::zero() : add(dy0, dy1);
-      f4[u][3] = (ci || cj) ? Sc<S>::zero() : sub(dy0, dy1);
-    }
-  }
-  __syncthreads();  // (X is not read before here; the barrier orders the V loads too)
-#pragma unroll
-  for (int u = 0; u < PPT; ++u) {
-    const int e = threadIdx.x + u * LTH;
-    if (e < HB * HB) {
-      const int i = e / HB, j = e % HB;
-      X[i * LTD + j] = f4[u][0];
-      X[i * LTD + HB + j] = f4[u][1];
-      X[(HB + i) * LTD + j] = f4[u][2];
-      X[(HB + i) * LTD + HB + j] = f4[u][3];
-    }
-  }
-  __syncthreads();
-  // X <- Vfy^T X   (block rows: even modes from s_y, odd modes from d_y)
-  tile_product_fold<true, S>(hpy, hy, [&](int m, int k) { return Vy[k * LTD + m]; },
-                             [&](int k, int n) { return X[k * LTD + n]; },
-                             [&](int m, int n, S v) { X[m * LTD + n] = v; });
-  __syncthreads();
-  // X <- (X Vfx) ./ (lfy (+) lfx - k^2)
-  tile_product_fold<false, S>(hpx, hx, [&](int m, int k) { return X[m * LTD + k]; },
-                              [&](int k, int n) { return Vx[k * LTD + n]; }, [&](int m, int n, S v) {
-                                X[m * LTD + n] = scale(v, 1.0 / (ly[m] + lx[n] - a.k2));
-                              });
-  __syncthreads();
-  // X <- Vfy X
-  tile_product_fold<true, S>(hpy, hy, [&](int m, int k) { return Vy[m * LTD + k]; },
-                             [&](int k, int n) { return X[k * LTD + n]; },
-                             [&](int m, int n, S v) { X[m * LTD + n] = v; });
-  __syncthreads();
-  // X <- X Vfx^T
-  tile_product_fold<false, S>(hpx, hx, [&](int m, int k) { return X[m * LTD + k]; },
-                              [&](int k, int n) { return Vx[n * LTD + k]; },
-                              [&](int m, int n, S v) { X[m * LTD + n] = v; });
-  __syncthreads();
-  // unfold + weight + scatter: x_i = e_i + o_i, x_{L-1-i} = e_i - o_i on both axes
-  auto put = [&](int r, int q, S acc) {
-    const int iy = y0 + r, ix = x0 + q;
-    const int my = a.node_mult[iy], mx = a.node_mult[ix];
-    if (a.weighted && !a.wbs) acc = scale(acc, 1.0 / (my * mx));
-    const size_t pidx = (size_t)iy * nu + ix;
-    if (my == 1 && mx == 1) {
-      yb[pidx] = bb ? add(bb[pidx], acc) : acc;
-    } else if (my == 2) {
-      const int ry = ay - a.node_first_box[iy], rx = ax - a.node_first_box[ix];
-      ob[((size_t)(ry * 2 + rx) * a.nbands + a.node_band[iy]) * nu + ix] = acc;
-    } else {
-      const int rx = ax - a.node_first_box[ix];
-      ob[(size_t)4 * a.nbands * nu + ((size_t)rx * nu + iy) * a.nbands + a.node_band[ix]] = acc;
-    }
-  };
-  for (int e = threadIdx.x; e < hpy * hpx; e += LTH) {
-    const int i = e / hpx, j = e % hpx;
-    const bool ci = i == hy, cj = j == hx;
-    const S ee = X[i * LTD + j];
-    const S eo = cj ? Sc<S>::zero() : X[i * LTD + HB + j];
-    const S oe = ci ? Sc<S>::zero() : X[(HB + i) * LTD + j];
-    const S oo = (ci || cj) ? Sc<S>::zero() : X[(HB + i) * LTD + HB + j];
-    const S ry0 = add(ee, oe), ry1 = sub(ee, oe);  // row i / row L-1-i, still split in x
-    const S rz0 = add(eo, oo), rz1 = sub(eo, oo);
-    put(i, j, add(ry0, rz0));
-    if (!cj) put(i, Lx - 1 - j, sub(ry0, rz0));
-    if (!ci) put(Ly - 1 - i, j, add(ry1, rz1));
-    if (!ci && !cj) put(Ly - 1 - i, Lx - 1 - j, sub(ry1, rz1));
-  }
-}
-
-template <typename S>
-static void fold_launch(const helm_plan* P, const S* x, const S* base, S* y, S* ovl, const LocalArgs& a, int batch,
-                        cudaStream_t st) {
-  const PlanDev& d = P->dev;
-  if (d.n_ff == 0) return;
-  const size_t smem = (size_t)LT * LTD * (sizeof(S) + 2 * sizeof(double)) + 2 * LT * sizeof(double);
-  static bool attr = false;
-  if (!attr) {
-    HELM_CUDA(cudaFuncSetAttribute(local_fdm_fold_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)smem));
-    attr = true;
-  }
-  dim3 grd(d.n_ff, batch);
-  local_fdm_fold_kernel<S><<<grd, LTH, smem, st>>>(x, base, y, ovl, d.box_ff, d.class_Vf, d.class_lamf, a);
-  HELM_LAUNCH_CHECK();
-}
-
 template <typename S, bool RR>
 static void fast_launch(const helm_plan* P, const S* x, const S* base, S* y, S* ovl, const LocalArgs& a,
                         const int* boxes, int nbox, int batch, cudaStream_t st) {
@@ -430,7 +210,7 @@ bool launch_local_fast(const helm_plan* P, const S* x, const S* base, S* y, S* o
                        cudaStream_t st) {
   const PlanDev& d = P->dev;
   if (d.max_len > LT) return false;
-  fold_launch<S>(P, x, base, y, ovl, a, batch, st);
+  launch_local_dmma<S>(P, x, base, y, ovl, a, batch, st);  // folded real classes: FP64 tensor pipe
   fast_launch<S, true>(P, x, base, y, ovl, a, d.box_rr, d.n_rr, batch, st);
   fast_launch<S, false>(P, x, base, y, ovl, a, d.box_mix, d.n_mix, batch, st);
   return true;
