@@ -21,7 +21,7 @@ namespace helm {
 
 constexpr int DB = 20;      // folded block (even / odd modes)
 constexpr int DT = 2 * DB;  // tile side
-constexpr int DVL = 41;     // V leading dimension (doubles)
+constexpr int DVL = DT;     // V leading dimension (doubles): the plan's global tables, read through L1
 constexpr int DTH = 96;     // 3 warps
 
 template <int NP> struct DmmaDims {
@@ -36,87 +36,78 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
 }
 
 // LEFT product  X <- V' X  with V'(m, k) = TRANS ? V[k][m] : V[m][k], block diagonal:
-// rows of block b use k in [b DB, b DB + DB).  Warp w owns row tiles (b, w) for b = 0, 1
-// and all NT real-column tiles.  EPI(m, c, v) stores one result element.
+// rows of block b read and write only rows of block b, so the blocks run one after
+// the other (one set of accumulators live at a time), each in place across a barrier.
+// Warp w owns row tile (b, w) and all NT real-column tiles.  EPI(m, c, v) stores.
 template <int NP, bool TRANS, typename EPI>
-__device__ __forceinline__ void dmma_left(double* Xr, const double* V, EPI epi) {
+__device__ __forceinline__ void dmma_left(double* Xr, const double* __restrict__ V, EPI epi) {
   constexpr int XL = DmmaDims<NP>::XL, NT = DmmaDims<NP>::NT;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int g = lane >> 2, q = lane & 3;
-  double acc[2][NT][2];
-#pragma unroll
-  for (int b = 0; b < 2; ++b)
-#pragma unroll
-    for (int t = 0; t < NT; ++t) acc[b][t][0] = acc[b][t][1] = 0.0;
 #pragma unroll
   for (int b = 0; b < 2; ++b) {
+    double acc[NT][2];
+#pragma unroll
+    for (int t = 0; t < NT; ++t) acc[t][0] = acc[t][1] = 0.0;
     const int m = b * DB + w * 8 + g;  // A row of this lane (may run into the next block: discarded)
 #pragma unroll
     for (int ks = 0; ks < DB / 4; ++ks) {
       const int k = b * DB + ks * 4 + q;
-      const double a = (m < DT) ? (TRANS ? V[k * DVL + m] : V[m * DVL + k]) : 0.0;
+      const double a = (m < DT) ? __ldg(TRANS ? &V[k * DVL + m] : &V[m * DVL + k]) : 0.0;
 #pragma unroll
-      for (int t = 0; t < NT; ++t) dmma(acc[b][t][0], acc[b][t][1], a, Xr[k * XL + t * 8 + g]);
+      for (int t = 0; t < NT; ++t) dmma(acc[t][0], acc[t][1], a, Xr[k * XL + t * 8 + g]);
     }
-  }
-  __syncthreads();
-#pragma unroll
-  for (int b = 0; b < 2; ++b) {
+    __syncthreads();
     const int ml = w * 8 + g;
     if (ml < DB) {
 #pragma unroll
       for (int t = 0; t < NT; ++t) {
-        epi(b * DB + ml, t * 8 + 2 * q, acc[b][t][0]);
-        epi(b * DB + ml, t * 8 + 2 * q + 1, acc[b][t][1]);
+        epi(b * DB + ml, t * 8 + 2 * q, acc[t][0]);
+        epi(b * DB + ml, t * 8 + 2 * q + 1, acc[t][1]);
       }
     }
   }
 }
 
 // RIGHT product  X <- X V'  with V'(k, n) = TRANS ? V[n][k] : V[k][n], block diagonal in
-// the columns.  Real rows r = (m, part) read X[m][k NP + part].  Warp w owns column tiles
-// (b, w) for b = 0, 1 and all NT real-row tiles.  EPI(m, part, n, v) stores one element.
+// the columns (blocks one after the other as above).  Real rows r = (m, part) read
+// X[m][k NP + part].  Warp w owns column tile (b, w) and all NT real-row tiles.
 template <int NP, bool TRANS, typename EPI>
-__device__ __forceinline__ void dmma_right(double* Xr, const double* V, EPI epi) {
+__device__ __forceinline__ void dmma_right(double* Xr, const double* __restrict__ V, EPI epi) {
   constexpr int XL = DmmaDims<NP>::XL, NT = DmmaDims<NP>::NT;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int g = lane >> 2, q = lane & 3;
-  double acc[2][NT][2];
-#pragma unroll
-  for (int b = 0; b < 2; ++b)
-#pragma unroll
-    for (int t = 0; t < NT; ++t) acc[b][t][0] = acc[b][t][1] = 0.0;
 #pragma unroll
   for (int b = 0; b < 2; ++b) {
+    double acc[NT][2];
+#pragma unroll
+    for (int t = 0; t < NT; ++t) acc[t][0] = acc[t][1] = 0.0;
     const int n = b * DB + w * 8 + g;  // B column of this lane
 #pragma unroll
     for (int ks = 0; ks < DB / 4; ++ks) {
       const int k = b * DB + ks * 4 + q;
-      const double bv = (n < DT) ? (TRANS ? V[n * DVL + k] : V[k * DVL + n]) : 0.0;
+      const double bv = (n < DT) ? __ldg(TRANS ? &V[n * DVL + k] : &V[k * DVL + n]) : 0.0;
 #pragma unroll
       for (int t = 0; t < NT; ++t) {
         const int r = t * 8 + g;  // A row (real row) of this lane
-        dmma(acc[b][t][0], acc[b][t][1], Xr[(r / NP) * XL + k * NP + (r % NP)], bv);
+        dmma(acc[t][0], acc[t][1], Xr[(r / NP) * XL + k * NP + (r % NP)], bv);
       }
     }
-  }
-  __syncthreads();
-#pragma unroll
-  for (int b = 0; b < 2; ++b) {
+    __syncthreads();
 #pragma unroll
     for (int t = 0; t < NT; ++t) {
       const int r = t * 8 + g;
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         const int nl = w * 8 + 2 * q + e;
-        if (nl < DB) epi(r / NP, r % NP, b * DB + nl, acc[b][t][e]);
+        if (nl < DB) epi(r / NP, r % NP, b * DB + nl, acc[t][e]);
       }
     }
   }
 }
 
 template <typename S>
-__global__ void __launch_bounds__(DTH) local_fdm_dmma_kernel(const S* __restrict__ x, const S* __restrict__ base,
+__global__ void __launch_bounds__(DTH, 5) local_fdm_dmma_kernel(const S* __restrict__ x, const S* __restrict__ base,
                                                              S* __restrict__ y, S* __restrict__ ovl,
                                                              const int* __restrict__ boxes,
                                                              const double* __restrict__ classVf,
@@ -126,9 +117,7 @@ __global__ void __launch_bounds__(DTH) local_fdm_dmma_kernel(const S* __restrict
   constexpr int XL = DmmaDims<NP>::XL;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double* Xr = reinterpret_cast<double*>(smem_raw);  // [DT][XL]
-  double* Vy = Xr + DT * XL;                           // [DT][DVL]
-  double* Vx = Vy + DT * DVL;
-  int* meta = reinterpret_cast<int*>(Vx + DT * DVL);  // [2][3][DT]: multiplicity, first box, band per row / column
+  int* meta = reinterpret_cast<int*>(Xr + DT * XL);  // [2][3][DT]: multiplicity, first box, band per row / column
   const int sid = boxes[blockIdx.x];
   const int ay = sid / a.p, ax = sid % a.p;
   const int nu = a.nu;
@@ -150,35 +139,38 @@ __global__ void __launch_bounds__(DTH) local_fdm_dmma_kernel(const S* __restrict
     if (wb) v = scale(v, 1.0 / (a.node_mult[y0 + r] * a.node_mult[x0 + q]));
     return v;
   };
-  constexpr int PPT = (DB * DB + DTH - 1) / DTH;  // pairs per thread
-  S f4[PPT][4];
-#pragma unroll
-  for (int u = 0; u < PPT; ++u) {
-    const int e = threadIdx.x + u * DTH;
+  auto put_s = [&](int i, int j, S v) {
+    if constexpr (NP == 2) {
+      Xr[i * XL + 2 * j] = v.x;
+      Xr[i * XL + 2 * j + 1] = v.y;
+    } else {
+      Xr[i * XL + j] = v;
+    }
+  };
+  for (int e = threadIdx.x; e < DB * DB; e += DTH) {
     const int i = e / DB, j = e % DB;
-#pragma unroll
-    for (int c = 0; c < 4; ++c) f4[u][c] = Sc<S>::zero();
-    if (e < DB * DB && i < hpy && j < hpx) {
+    S f0 = Sc<S>::zero(), f1 = f0, f2 = f0, f3 = f0;
+    if (i < hpy && j < hpx) {
       const bool ci = i == hy, cj = j == hx;  // centre row / column (odd length)
       const S a00 = ld(i, j);
       const S a10 = ci ? Sc<S>::zero() : ld(Ly - 1 - i, j);
       const S a01 = cj ? Sc<S>::zero() : ld(i, Lx - 1 - j);
       const S a11 = (ci || cj) ? Sc<S>::zero() : ld(Ly - 1 - i, Lx - 1 - j);
       const S sy0 = add(a00, a10), dy0 = sub(a00, a10), sy1 = add(a01, a11), dy1 = sub(a01, a11);
-      f4[u][0] = add(sy0, sy1);
-      f4[u][1] = cj ? Sc<S>::zero() : sub(sy0, sy1);
-      f4[u][2] = ci ? Sc<S>::zero() : add(dy0, dy1);
-      f4[u][3] = (ci || cj) ? Sc<S>::zero() : sub(dy0, dy1);
+      // the d components of a centre row / column are exactly zero (the padded blocks read them)
+      f0 = add(sy0, sy1);
+      f1 = cj ? Sc<S>::zero() : sub(sy0, sy1);
+      f2 = ci ? Sc<S>::zero() : add(dy0, dy1);
+      f3 = (ci || cj) ? Sc<S>::zero() : sub(dy0, dy1);
     }
+    put_s(i, j, f0);
+    put_s(i, DB + j, f1);
+    put_s(DB + i, j, f2);
+    put_s(DB + i, DB + j, f3);
   }
-  {  // folded V tables (zero padded by the plan)
-    const double* vyg = classVf + (size_t)cy * DT * DT;
-    const double* vxg = classVf + (size_t)cx * DT * DT;
-    for (int r = threadIdx.x / 8; r < DT; r += DTH / 8)
-      for (int c = threadIdx.x % 8; c < DT; c += 8) {
-        Vy[r * DVL + c] = vyg[r * DT + c];
-        Vx[r * DVL + c] = vxg[r * DT + c];
-      }
+  const double* Vy = classVf + (size_t)cy * DT * DT;  // folded V tables (zero padded by the plan)
+  const double* Vx = classVf + (size_t)cx * DT * DT;
+  {
     // the box's per-row / per-column overlap bookkeeping (decomposition.py:111-134)
     for (int e = threadIdx.x; e < DT; e += DTH) {
       const int iy = y0 + (e < Ly ? e : 0), ix = x0 + (e < Lx ? e : 0);
@@ -191,25 +183,6 @@ __global__ void __launch_bounds__(DTH) local_fdm_dmma_kernel(const S* __restrict
     }
   }
   const double* invden = classInvden + (size_t)(cy * ncls + cx) * DT * DT;
-  auto put_s = [&](int i, int j, S v) {
-    if constexpr (NP == 2) {
-      Xr[i * XL + 2 * j] = v.x;
-      Xr[i * XL + 2 * j + 1] = v.y;
-    } else {
-      Xr[i * XL + j] = v;
-    }
-  };
-#pragma unroll
-  for (int u = 0; u < PPT; ++u) {
-    const int e = threadIdx.x + u * DTH;
-    if (e < DB * DB) {
-      const int i = e / DB, j = e % DB;
-      put_s(i, j, f4[u][0]);
-      put_s(i, DB + j, f4[u][1]);
-      put_s(DB + i, j, f4[u][2]);
-      put_s(DB + i, DB + j, f4[u][3]);
-    }
-  }
   __syncthreads();
   // X <- Vfy^T X
   dmma_left<NP, true>(Xr, Vy, [&](int m, int c, double v) { Xr[m * XL + c] = v; });
@@ -225,33 +198,12 @@ __global__ void __launch_bounds__(DTH) local_fdm_dmma_kernel(const S* __restrict
   // X <- X Vfx^T
   dmma_right<NP, true>(Xr, Vx, [&](int m, int part, int n, double v) { Xr[m * XL + n * NP + part] = v; });
   __syncthreads();
-  // unfold into a natural-order tile (the V tables are dead now: reuse their space),
-  // x_i = e_i + o_i, x_{L-1-i} = e_i - o_i on both axes ...
-  S* Y = reinterpret_cast<S*>(Vy);  // [Ly][Lx]
+  // unfold + weight + scatter: x_i = e_i + o_i, x_{L-1-i} = e_i - o_i on both axes
   auto get = [&](int i, int j) -> S {
     if constexpr (NP == 2) return mk(Xr[i * XL + 2 * j], Xr[i * XL + 2 * j + 1]);
     else return Xr[i * XL + j];
   };
-  for (int e = threadIdx.x; e < hpy * hpx; e += DTH) {
-    const int i = e / hpx, j = e % hpx;
-    const bool ci = i == hy, cj = j == hx;
-    const S ee = get(i, j);
-    const S eo = cj ? Sc<S>::zero() : get(i, DB + j);
-    const S oe = ci ? Sc<S>::zero() : get(DB + i, j);
-    const S oo = (ci || cj) ? Sc<S>::zero() : get(DB + i, DB + j);
-    const S ry0 = add(ee, oe), ry1 = sub(ee, oe);  // row i / row L-1-i, still split in x
-    const S rz0 = add(eo, oo), rz1 = sub(eo, oo);
-    Y[i * Lx + j] = add(ry0, rz0);
-    if (!cj) Y[i * Lx + Lx - 1 - j] = sub(ry0, rz0);
-    if (!ci) Y[(Ly - 1 - i) * Lx + j] = add(ry1, rz1);
-    if (!ci && !cj) Y[(Ly - 1 - i) * Lx + Lx - 1 - j] = sub(ry1, rz1);
-  }
-  __syncthreads();
-  // ... then weight and write row by row (coalesced; the overlap rows / columns of the
-  // box go to their slot of the scratch that the combine kernels sum)
-  for (int e = threadIdx.x; e < Ly * Lx; e += DTH) {
-    const int r = e / Lx, q = e % Lx;
-    S acc = Y[e];
+  auto put = [&](int r, int q, S acc) {
     const int my = meta[r], mx = meta[3 * DT + q];
     if (a.weighted && !a.wbs) acc = scale(acc, 1.0 / (my * mx));
     const int iy = y0 + r, ix = x0 + q;
@@ -265,6 +217,20 @@ __global__ void __launch_bounds__(DTH) local_fdm_dmma_kernel(const S* __restrict
       const int rx = ax - meta[4 * DT + q];
       ob[(size_t)4 * a.nbands * nu + ((size_t)rx * nu + iy) * a.nbands + meta[5 * DT + q]] = acc;
     }
+  };
+  for (int e = threadIdx.x; e < hpy * hpx; e += DTH) {
+    const int i = e / hpx, j = e % hpx;
+    const bool ci = i == hy, cj = j == hx;
+    const S ee = get(i, j);
+    const S eo = cj ? Sc<S>::zero() : get(i, DB + j);
+    const S oe = ci ? Sc<S>::zero() : get(DB + i, j);
+    const S oo = (ci || cj) ? Sc<S>::zero() : get(DB + i, DB + j);
+    const S ry0 = add(ee, oe), ry1 = sub(ee, oe);  // row i / row L-1-i, still split in x
+    const S rz0 = add(eo, oo), rz1 = sub(eo, oo);
+    put(i, j, add(ry0, rz0));
+    if (!cj) put(i, Lx - 1 - j, sub(ry0, rz0));
+    if (!ci) put(Ly - 1 - i, j, add(ry1, rz1));
+    if (!ci && !cj) put(Ly - 1 - i, Lx - 1 - j, sub(ry1, rz1));
   }
 }
 
@@ -274,7 +240,7 @@ void launch_local_dmma(const helm_plan* P, const S* x, const S* base, S* y, S* o
   const PlanDev& d = P->dev;
   if (d.n_ff == 0) return;
   constexpr int NP = Sc<S>::cplx ? 2 : 1;
-  const size_t smem = (size_t)(DT * DmmaDims<NP>::XL + 2 * DT * DVL) * sizeof(double) + 6 * DT * sizeof(int);
+  const size_t smem = (size_t)(DT * DmmaDims<NP>::XL) * sizeof(double) + 6 * DT * sizeof(int);
   static bool attr = false;
   if (!attr) {
     HELM_CUDA(cudaFuncSetAttribute(local_fdm_dmma_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
