@@ -45,7 +45,7 @@
 extern "C" {
 #endif
 
-#define HELM_ABI_VERSION 2
+#define HELM_ABI_VERSION 3
 
 enum helm_bc { HELM_DIRICHLET = 0, HELM_SOMMERFELD = 1 };
 enum helm_kind { HELM_AS2 = 0, HELM_SAS2 = 1, HELM_SHS2 = 2 };
@@ -97,7 +97,16 @@ typedef struct helm_desc {
   const void* cap_left;       /* S [m0][m0]  V^T M0 (V: y-pencil eigenvectors)   */
   const void* cap_right;      /* S [m0][m0]  M0 V                                */
   const void* cap_mode;       /* S [m0][n_strip][n_strip]                        */
-  int32_t refine_steps;       /* iterative-refinement steps of the coarse solve  */
+  /* strip-space refinement: after the second band pass the exact strip residual
+   * rho = c_S - C_U y_S is formed from the band-pass strip values and one more band
+   * pass applies B^{-1} of (I - H G) rho (the eigen-space H, G are only ~1e-12
+   * accurate; the band passes are exact), see coarse.cu                          */
+  const void* cap_vt;         /* S [m0][m0]  V^T                                 */
+  const void* cap_hg;         /* S [m0][n_strip][n_strip]  cap_mode_b Gamma_b     */
+  const void* strip_lt;       /* S [n_strip][n_strip]  (T0 - T~) on the strips    */
+  const void* strip_lm;       /* S [n_strip][n_strip]  (M0 - M~) on the strips    */
+  int32_t strip_refine;       /* strip-refinement steps (Sommerfeld; 0..4)        */
+  int32_t refine_steps;       /* full iterative-refinement steps r = c - A0 y    */
 } helm_desc;
 
 typedef struct helm_gmres_report {

@@ -15,7 +15,7 @@ LIB_PATH = os.path.join(_HERE, "libhelmb200.so")
 
 HELM_DIRICHLET, HELM_SOMMERFELD = 0, 1
 KINDS = {"AS2": 0, "SAS2": 1, "SHS2": 2}
-ABI_VERSION = 2
+ABI_VERSION = 3
 
 c_int32_p = ctypes.POINTER(ctypes.c_int32)
 
@@ -55,6 +55,11 @@ class HelmDesc(ctypes.Structure):
         ("cap_left", ctypes.c_void_p),
         ("cap_right", ctypes.c_void_p),
         ("cap_mode", ctypes.c_void_p),
+        ("cap_vt", ctypes.c_void_p),
+        ("cap_hg", ctypes.c_void_p),
+        ("strip_lt", ctypes.c_void_p),
+        ("strip_lm", ctypes.c_void_p),
+        ("strip_refine", ctypes.c_int32),
         ("refine_steps", ctypes.c_int32),
     ]
 

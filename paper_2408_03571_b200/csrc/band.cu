@@ -1,8 +1,11 @@
 // Pivoted pentadiagonal solves along y, one per x-mode (part of K5, the Sommerfeld
 // coarse solve; algorithm and reference lines in coarse.cu):
 //
-//   (T0 + s_a M0) out[b][:, a] = in[b][:, a] - sig_a * sum_i corr[y][b*4+i] q[a][i]
+//   (T0 + s_a M0) X[b][:, a] = in[b][:, a] - sig_a * sum_i corr[y][b*4+i] q[a][i],   out = X (+ add)
 //
+// `in` may be null (right-hand side = the strip term alone: the strip refinement);
+// `add` (may be null) is summed into the backward sweep's stores, read one chunk
+// ahead into registers so its latency stays off the recurrence.
 // A CTA owns 32 consecutive modes a (lane = mode: the factors and the vectors are
 // stored [row][a], so every access is a coalesced 512-byte row segment) and NW*RB
 // right-hand sides: warp w carries RB independent recurrences per lane, which gives
@@ -58,7 +61,8 @@ __global__ void __launch_bounds__(BW* NW) band_solve_kernel(const double2* __res
                                                             const double2* __restrict__ U, int m0, int batch,
                                                             const double2* __restrict__ corr,
                                                             const double* __restrict__ q,
-                                                            const double* __restrict__ sig, int ldc) {
+                                                            const double* __restrict__ sig, int ldc,
+                                                            const double2* __restrict__ add) {
   extern __shared__ __align__(16) unsigned char sraw[];
   const int t = threadIdx.x & (BW - 1), w = threadIdx.x / BW;
   const int a0 = blockIdx.x * BW;
@@ -98,10 +102,12 @@ __global__ void __launch_bounds__(BW* NW) band_solve_kernel(const double2* __res
     for (int rr = 0; rr < R; ++rr) {
       const int jr = c * R + rr + 3;
       const size_t fr = (size_t)(jr < m0 ? jr : 0) * m0 + (va ? a : 0);
+      if (in) {
 #pragma unroll
-      for (int r = 0; r < RB; ++r) {
-        const bool okb = b0 + r < batch;
-        cp_async16(&S.rhs[w][r][rr][t], in + (size_t)(okb ? b0 + r : 0) * N0 + fr, va && jr < m0 && okb);
+        for (int r = 0; r < RB; ++r) {
+          const bool okb = b0 + r < batch;
+          cp_async16(&S.rhs[w][r][rr][t], in + (size_t)(okb ? b0 + r : 0) * N0 + fr, va && jr < m0 && okb);
+        }
       }
       if (corr && t < 4 * RB) {
         const int r = t >> 2, i = t & 3;
@@ -117,13 +123,13 @@ __global__ void __launch_bounds__(BW* NW) band_solve_kernel(const double2* __res
   for (int r = 0; r < RB; ++r) {
     const int b = b0 + r;
     const bool ok = va && b < batch;
-    const double2* col = in + (size_t)(ok ? b : 0) * N0 + (va ? a : 0);
+    const double2* col = in ? in + (size_t)(ok ? b : 0) * N0 + (va ? a : 0) : nullptr;
     double2 c4[4];
     double2 v3[3];
     for (int jj = 0; jj < 3; ++jj) {
       double2 v = mk(0.0, 0.0);
       if (ok && jj < m0) {
-        v = col[(size_t)jj * m0];
+        if (in) v = col[(size_t)jj * m0];
         if (corr) {
           for (int i = 0; i < 4; ++i) c4[i] = corr[(size_t)jj * ldc + (size_t)b * 4 + i];
           v = corrected(v, c4);
@@ -158,7 +164,7 @@ __global__ void __launch_bounds__(BW* NW) band_solve_kernel(const double2* __res
         x1 = fms_(l0, x0, x1);
         x2 = fms_(l1, x0, x2);
         if (va && b0 + r < batch) out[(size_t)(b0 + r) * N0 + (size_t)j * m0 + a] = x0;
-        double2 nx = S.rhs[w][r][rr][t];
+        double2 nx = in ? S.rhs[w][r][rr][t] : mk(0.0, 0.0);
         if (corr) nx = corrected(nx, S.corr[w][r][rr]);
         r0[r] = x1;
         r1[r] = x2;
@@ -200,14 +206,29 @@ __global__ void __launch_bounds__(BW* NW) band_solve_kernel(const double2* __res
   double2 y1[RB], y2[RB], y3[RB], y4[RB];
 #pragma unroll
   for (int r = 0; r < RB; ++r) y1[r] = y2[r] = y3[r] = y4[r] = mk(0.0, 0.0);
+  double2 acur[RB][R], anxt[RB][R];
+  auto load_add = [&](int c, double2 (&dst)[RB][R]) {
+#pragma unroll
+    for (int rr = 0; rr < R; ++rr) {
+      const int j = m0 - 1 - (c * R + rr);
+#pragma unroll
+      for (int r = 0; r < RB; ++r)
+        dst[r][rr] = (va && j >= 0 && b0 + r < batch) ? __ldg(add + (size_t)(b0 + r) * N0 + (size_t)j * m0 + a)
+                                                       : mk(0.0, 0.0);
+    }
+  };
+  if (add) load_add(0, acur);
   for (int c = 0; c < nch; ++c) {
     cp_wait<ST - 2>();
     __syncthreads();
     if (c + ST - 1 < nch) issue_bwd(c + ST - 1);
     else cp_commit();
+    if (add && c + 1 < nch) load_add(c + 1, anxt);
     const BS& S = bs[c % ST];
     const int rows = min(R, m0 - c * R);
-    for (int rr = 0; rr < rows; ++rr) {
+#pragma unroll
+    for (int rr = 0; rr < R; ++rr) {
+      if (rr >= rows) break;
       const int j = m0 - 1 - (c * R + rr);
       const double2 u0 = S.U[rr][t][0], u1 = S.U[rr][t][1], u2 = S.U[rr][t][2], u3 = S.U[rr][t][3],
                     u4 = S.U[rr][t][4];
@@ -219,12 +240,19 @@ __global__ void __launch_bounds__(BW* NW) band_solve_kernel(const double2* __res
         v = fms_(u3, y3[r], v);
         v = fms_(u4, y4[r], v);
         v = mul(v, u0);
-        if (va && b0 + r < batch) out[(size_t)(b0 + r) * N0 + (size_t)j * m0 + a] = v;
+        if (va && b0 + r < batch)
+          out[(size_t)(b0 + r) * N0 + (size_t)j * m0 + a] = add ? ::helm::add(v, acur[r][rr]) : v;
         y4[r] = y3[r];
         y3[r] = y2[r];
         y2[r] = y1[r];
         y1[r] = v;
       }
+    }
+    if (add) {
+#pragma unroll
+      for (int rr = 0; rr < R; ++rr)
+#pragma unroll
+        for (int r = 0; r < RB; ++r) acur[r][rr] = anxt[r][rr];
     }
   }
   cp_wait<0>();
@@ -232,7 +260,7 @@ __global__ void __launch_bounds__(BW* NW) band_solve_kernel(const double2* __res
 
 template <int RB, int NW, int R, int ST>
 static void band_launch(const helm_plan* P, const double2* in, double2* out, const double2* corr, int batch,
-                        cudaStream_t st) {
+                        cudaStream_t st, const double2* add) {
   const PlanDev& d = P->dev;
   constexpr size_t smem = band_smem_bytes<RB, NW, R, ST>();
   static_assert(smem <= 227 * 1024, "band-solve stages exceed shared memory");
@@ -245,20 +273,22 @@ static void band_launch(const helm_plan* P, const double2* in, double2* out, con
   dim3 grd((d.m0 + BW - 1) / BW, (batch + RB * NW - 1) / (RB * NW));
   band_solve_kernel<RB, NW, R, ST><<<grd, BW * NW, smem, st>>>(in, out, d.band_piv, (const double2*)d.band_l,
                                                                (const double2*)d.band_u, d.m0, batch, corr,
-                                                               d.strip_q, d.coarse_scale, batch * 4);
+                                                               d.strip_q, d.coarse_scale, batch * 4, add);
   HELM_LAUNCH_CHECK();
 }
 
 void launch_band_solve(const helm_plan* P, const double2* in, double2* out, const double2* corr, int batch,
-                       cudaStream_t st) {
+                       cudaStream_t st, const double2* add) {
   HELM_CHECK(P->dev.band_piv != nullptr, "plan has no band factors");
-  HELM_CHECK((const void*)in != (const void*)out, "band solve: input and output must not alias");
+  HELM_CHECK((const void*)in != (const void*)out && (const void*)add != (const void*)out,
+             "band solve: input and output must not alias");
+  HELM_CHECK(in != nullptr || corr != nullptr, "band solve: no right-hand side");
   if (batch == 1)
-    band_launch<1, 1, 8, 4>(P, in, out, corr, batch, st);  // latency-bound recurrence
+    band_launch<1, 1, 8, 4>(P, in, out, corr, batch, st, add);  // latency-bound recurrence
   else if (batch <= 4)
-    band_launch<2, 2, 8, 3>(P, in, out, corr, batch, st);
+    band_launch<2, 2, 8, 3>(P, in, out, corr, batch, st, add);
   else
-    band_launch<1, 8, 8, 3>(P, in, out, corr, batch, st);  // 8 warps (8 right-hand sides) share each factor read
+    band_launch<1, 8, 8, 3>(P, in, out, corr, batch, st, add);  // 8 warps (8 right-hand sides) share each factor read
 }
 
 }  // namespace helm

@@ -237,6 +237,7 @@ static void build_plan(const helm_desc* d, helm_plan* P) {
   // p == 0 (no boxes) and coarse_V == NULL (no coarse solver) give an operator-only plan
   HELM_CHECK(d->p == 0 || (d->p >= 1 && (d->n - 1) % d->p == 0), "p must divide the cell count n-1");
   HELM_CHECK(d->refine_steps >= 0 && d->refine_steps <= 8, "refine_steps out of range");
+  HELM_CHECK(d->strip_refine >= 0 && d->strip_refine <= 4, "strip_refine out of range");
   P->desc = *d;
   P->elem = d->is_complex ? sizeof(double2) : sizeof(double);
   Geo& g = P->geo;
@@ -291,6 +292,15 @@ static void build_plan(const helm_desc* d, helm_plan* P) {
       dv.cap_left = upload_bytes(d->cap_left, m0 * m0 * P->elem);
       dv.cap_right = upload_bytes(d->cap_right, m0 * m0 * P->elem);
       dv.cap_mode = upload_bytes(d->cap_mode, m0 * ns * ns * P->elem);
+      dv.strip_refine = d->strip_refine;
+      if (d->strip_refine) {
+        HELM_CHECK(d->cap_vt && d->cap_hg && d->strip_lt && d->strip_lm,
+                   "strip refinement needs cap_vt, cap_hg, strip_lt and strip_lm");
+        dv.cap_vt = upload_bytes(d->cap_vt, m0 * m0 * P->elem);
+        dv.cap_hg = upload_bytes(d->cap_hg, m0 * ns * ns * P->elem);
+        std::memcpy(dv.strip_lt, d->strip_lt, 16 * sizeof(double2));
+        std::memcpy(dv.strip_lm, d->strip_lm, 16 * sizeof(double2));
+      }
     }
   }
   if (p == 0) return;
@@ -432,7 +442,8 @@ static void finish_desc(helm_plan* P) {
   P->desc.class_V = P->desc.class_lambda = nullptr;
   P->desc.coarse_scale = P->desc.strip_q = P->desc.coarse_lamT = P->desc.coarse_lamM = nullptr;
   P->desc.t0_band = P->desc.m0_band = P->desc.band_l = P->desc.band_u = nullptr;
-  P->desc.cap_left = P->desc.cap_right = P->desc.cap_mode = nullptr;
+  P->desc.cap_left = P->desc.cap_right = P->desc.cap_mode = P->desc.cap_vt = P->desc.cap_hg = nullptr;
+  P->desc.strip_lt = P->desc.strip_lm = nullptr;
   P->desc.band_piv = nullptr;
 }
 
@@ -442,7 +453,7 @@ static void free_plan(helm_plan* P) {
                   dv.class_V, dv.class_lambda, dv.class_real, dv.class_Vr, dv.box_ff, dv.class_Vf, dv.class_lamf, dv.class_invden, dv.box_rr, dv.box_mix,
                   dv.node_first_box, dv.node_mult, dv.node_band, dv.band_node,
                   dv.coarse_scale, dv.twiddle, dv.coarse_lamT, dv.coarse_lamM, dv.t0_band, dv.m0_band, dv.band_piv, dv.band_l, dv.band_u, dv.strip_q,
-                  dv.cap_left, dv.cap_right, dv.cap_mode};
+                  dv.cap_left, dv.cap_right, dv.cap_mode, dv.cap_vt, dv.cap_hg};
   for (void* q : ptrs)
     if (q) cudaFree(q);
 }
@@ -506,7 +517,7 @@ int helm_workspace_create(const helm_plan* P, int32_t max_batch, helm_workspace*
     for (void** q : coarse) HELM_CUDA(cudaMalloc(q, B * P->N0 * e));
     const size_t novl = std::max<size_t>(1, B * 6 * (size_t)P->dev.nbands * P->geo.nu);
     HELM_CUDA(cudaMalloc(&w->ovl, novl * e));
-    for (int s = 0; s < 4; ++s)
+    for (int s = 0; s < 6; ++s)
       if (P->dev.n_strip)
         HELM_CUDA(cudaMalloc(&w->strip[s], (size_t)(s == 3 ? 4 : 1) * P->dev.m0 * B * P->dev.n_strip * e));
     w->red_bytes = krylov_scratch_bytes(4096);
@@ -520,7 +531,7 @@ int helm_workspace_destroy(helm_workspace* w) {
   return guarded([&] {
     if (!w) return;
     void* ptrs[] = {w->z, w->d, w->c, w->g, w->y0, w->r0, w->e0, w->f0, w->ovl, w->red, w->strip[0], w->strip[1],
-                    w->strip[2], w->strip[3]};
+                    w->strip[2], w->strip[3], w->strip[4], w->strip[5]};
     for (void* q : ptrs)
       if (q) cudaFree(q);
     if (w->pinned) cudaFreeHost(w->pinned);

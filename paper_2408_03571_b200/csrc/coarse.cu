@@ -111,7 +111,8 @@ __global__ void __launch_bounds__(256) strip_gemm_part_kernel(const S* __restric
 
 template <typename S>
 __global__ void __launch_bounds__(256) strip_gemm_reduce_kernel(const S* __restrict__ part, S* __restrict__ out,
-                                                                const S* __restrict__ Hm, int m0, int ngroups) {
+                                                                const S* __restrict__ Hm, const S* __restrict__ minus,
+                                                                int m0, int ngroups) {
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= m0 * ngroups) return;
   const int m = e / ngroups, g = e % ngroups;
@@ -124,6 +125,7 @@ __global__ void __launch_bounds__(256) strip_gemm_reduce_kernel(const S* __restr
     t[i] = s;
   }
   S* o = out + (size_t)m * ldz + (size_t)g * 4;
+  S res[4];
   if (Hm) {
     const S* h = Hm + (size_t)m * 16;
 #pragma unroll
@@ -131,18 +133,22 @@ __global__ void __launch_bounds__(256) strip_gemm_reduce_kernel(const S* __restr
       S s = Sc<S>::zero();
 #pragma unroll
       for (int j = 0; j < 4; ++j) s = fma_(h[i * 4 + j], t[j], s);
-      o[i] = s;
+      res[i] = s;
     }
   } else {
 #pragma unroll
-    for (int i = 0; i < 4; ++i) o[i] = t[i];
+    for (int i = 0; i < 4; ++i) res[i] = t[i];
   }
+  const S* mi = minus ? minus + (size_t)m * ldz + (size_t)g * 4 : nullptr;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) o[i] = mi ? sub(res[i], mi[i]) : res[i];
 }
 
 // Warp-per-row form for few columns (batch <= 4): lanes stride over y.
 template <typename S, int NG>
 __global__ void __launch_bounds__(256) strip_gemm_rows_kernel(const S* __restrict__ A, const S* __restrict__ Z,
-                                                              S* __restrict__ out, const S* __restrict__ Hm, int m0) {
+                                                              S* __restrict__ out, const S* __restrict__ Hm,
+                                                              const S* __restrict__ minus, int m0) {
   const int m = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (m >= m0) return;
@@ -171,27 +177,80 @@ __global__ void __launch_bounds__(256) strip_gemm_rows_kernel(const S* __restric
       } else {
         s = acc[g * 4 + i];
       }
+      if (minus) s = sub(s, minus[(size_t)m * NC + g * 4 + i]);
       out[(size_t)m * NC + g * 4 + i] = s;
     }
   }
 }
 
+// out = [Hm] (A Z) [- minus]
 template <typename S>
-static void strip_gemm(const S* A, const S* Z, S* out, const S* Hm, int m0, int batch, S* part, cudaStream_t st) {
+static void strip_gemm(const S* A, const S* Z, S* out, const S* Hm, int m0, int batch, S* part, cudaStream_t st,
+                       const S* minus = nullptr) {
   const int rows_blocks = (m0 * 32 + 255) / 256;
   switch (batch) {
-    case 1: strip_gemm_rows_kernel<S, 1><<<rows_blocks, 256, 0, st>>>(A, Z, out, Hm, m0); break;
-    case 2: strip_gemm_rows_kernel<S, 2><<<rows_blocks, 256, 0, st>>>(A, Z, out, Hm, m0); break;
-    case 3: strip_gemm_rows_kernel<S, 3><<<rows_blocks, 256, 0, st>>>(A, Z, out, Hm, m0); break;
-    case 4: strip_gemm_rows_kernel<S, 4><<<rows_blocks, 256, 0, st>>>(A, Z, out, Hm, m0); break;
+    case 1: strip_gemm_rows_kernel<S, 1><<<rows_blocks, 256, 0, st>>>(A, Z, out, Hm, minus, m0); break;
+    case 2: strip_gemm_rows_kernel<S, 2><<<rows_blocks, 256, 0, st>>>(A, Z, out, Hm, minus, m0); break;
+    case 3: strip_gemm_rows_kernel<S, 3><<<rows_blocks, 256, 0, st>>>(A, Z, out, Hm, minus, m0); break;
+    case 4: strip_gemm_rows_kernel<S, 4><<<rows_blocks, 256, 0, st>>>(A, Z, out, Hm, minus, m0); break;
     default: {
       dim3 grd((batch + GT_G - 1) / GT_G, (m0 + GT_M - 1) / GT_M, GT_KS);
       strip_gemm_part_kernel<S><<<grd, 256, 0, st>>>(A, Z, part, m0, batch);
       HELM_LAUNCH_CHECK();
-      strip_gemm_reduce_kernel<S><<<(m0 * batch + 255) / 256, 256, 0, st>>>(part, out, Hm, m0, batch);
+      strip_gemm_reduce_kernel<S><<<(m0 * batch + 255) / 256, 256, 0, st>>>(part, out, Hm, minus, m0, batch);
     }
   }
   HELM_LAUNCH_CHECK();
+}
+
+// --- strip refinement ----------------------------------------------------------
+// rho[y][b*4+i] = cS[y][b*4+i] - sum_j ((T0 yS_j)[y] LM[i][j] + (M0 yS_j)[y] (LT[i][j] - k^2 LM[i][j]))
+// the exact residual A0 y - F on the strip columns of y = B^{-1}(F - ext(cS))
+// (A0 - B is supported on the strip x strip block of the x-pencil).
+struct StripCoupling {
+  double2 lm[16];
+  double2 lk[16];  // LT - k^2 LM
+};
+__global__ void __launch_bounds__(256) strip_rho_kernel(const double2* __restrict__ cS, const double2* __restrict__ yS,
+                                                        double2* __restrict__ rho, const double2* __restrict__ t0b,
+                                                        const double2* __restrict__ m0b, StripCoupling cp, int m0,
+                                                        int batch) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= m0 * batch) return;
+  const int y = e / batch, b = e % batch;
+  const size_t ldz = (size_t)batch * 4;
+  double2 ty[4], my[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) ty[j] = my[j] = mk(0.0, 0.0);
+#pragma unroll
+  for (int d = 0; d < 5; ++d) {
+    const int yy = y + d - 2;
+    if (yy < 0 || yy >= m0) continue;
+    const double2 tb = t0b[y * 5 + d], mb = m0b[y * 5 + d];
+    const double2* v = yS + (size_t)yy * ldz + (size_t)b * 4;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      ty[j] = fma_(tb, v[j], ty[j]);
+      my[j] = fma_(mb, v[j], my[j]);
+    }
+  }
+  const double2* c = cS + (size_t)y * ldz + (size_t)b * 4;
+  double2* o = rho + (size_t)y * ldz + (size_t)b * 4;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    double2 s = mk(0.0, 0.0);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      s = fma_(cp.lm[i * 4 + j], ty[j], s);
+      s = fma_(cp.lk[i * 4 + j], my[j], s);
+    }
+    o[i] = sub(c[i], s);
+  }
+}
+
+__global__ void strip_axpy_kernel(double2* __restrict__ c, const double2* __restrict__ w, size_t n) {
+  const size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e < n) c[e] = add(c[e], w[e]);
 }
 
 // --- r = c - A0 y  (25-point Kronecker-sum stencil from the 1-D bands) ------
@@ -297,6 +356,33 @@ static void fast_solve(const helm_plan* P, helm_workspace* ws, const S* in, S* o
     strip_gemm<S>((const S*)d.cap_left, Z, Ch, (const S*)d.cap_mode, d.m0, batch, part, st);
     strip_gemm<S>((const S*)d.cap_right, Ch, Cs, nullptr, d.m0, batch, part, st);
     launch_band_solve(P, T1, T2, Cs, batch, st);
+    // strip refinement: rho = cS - C_U y_S from this pass's strip values (exact), the
+    // correction W = H G rho - rho from the eigen-space operators (only ~1e-12 accurate,
+    // enough for a correction of a ~1e-12 quantity), then Y^ += B^{-1}(-ext(W)).
+    S* T3 = (S*)ws->e0;
+    S* R = (S*)ws->strip[4];
+    S* W = (S*)ws->strip[5];
+    StripCoupling cp;
+    for (int i = 0; i < 16; ++i) {
+      cp.lm[i] = d.strip_lm[i];
+      cp.lk[i] = sub(d.strip_lt[i], scale(d.strip_lm[i], P->geo.k2));
+    }
+    for (int it = 0; it < d.strip_refine; ++it) {
+      strip_reduce_kernel<S><<<grd, 256, 0, st>>>(T2, d.strip_q, Z, d.m0, batch * 4);
+      HELM_LAUNCH_CHECK();
+      strip_rho_kernel<<<(d.m0 * batch + 255) / 256, 256, 0, st>>>(Cs, Z, R, (const double2*)d.t0_band,
+                                                                  (const double2*)d.m0_band, cp, d.m0, batch);
+      HELM_LAUNCH_CHECK();
+      strip_gemm<S>((const S*)d.cap_vt, R, Ch, (const S*)d.cap_hg, d.m0, batch, part, st);
+      strip_gemm<S>((const S*)d.cap_right, Ch, W, nullptr, d.m0, batch, part, st, R);
+      launch_band_solve(P, nullptr, T3, W, batch, st, T2);  // T3 = T2 + B^{-1}(-ext(W))
+      if (it + 1 < d.strip_refine) {
+        const size_t ns = (size_t)d.m0 * batch * 4;
+        strip_axpy_kernel<<<(unsigned)((ns + 255) / 256), 256, 0, st>>>(Cs, W, ns);
+        HELM_LAUNCH_CHECK();
+      }
+      std::swap(T2, T3);
+    }
     launch_xform<S>(P, T2, out, nullptr, false, batch, st, accumulate);
   }
 }

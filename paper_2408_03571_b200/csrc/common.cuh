@@ -180,6 +180,11 @@ struct PlanDev {
   void* cap_left;
   void* cap_right;
   void* cap_mode;
+  void* cap_vt;         // strip refinement (coarse.cu)
+  void* cap_hg;
+  double2 strip_lt[16]; // (T0 - T~), (M0 - M~) on the strip columns [i][j]
+  double2 strip_lm[16];
+  int strip_refine;
 };
 
 }  // namespace helm
@@ -206,7 +211,7 @@ struct helm_workspace {
   void* e0;       // [B][N0]
   void* f0;       // [B][N0]
   void* ovl;      // overlap scratch [B][6][nbands][nu]
-  void* strip[4]; // coarse Woodbury scratch [m0][B * n_strip] x3, split-K partials x4
+  void* strip[6]; // coarse Woodbury scratch [m0][B * n_strip]: Z, C^, C_S, split-K partials (x4), rho, W
   void* red;      // reduction scratch (doubles)
   size_t red_bytes;
   void* pinned;   // small pinned host buffer for scalar read-back

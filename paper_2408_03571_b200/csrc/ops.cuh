@@ -21,7 +21,7 @@ void launch_xform(const helm_plan* P, const S* in, S* out, const double* sig, bo
                   cudaStream_t st, bool accumulate = false);
 template <typename S> void launch_transpose(const S* in, S* out, int m, int batch, cudaStream_t st);
 void launch_band_solve(const helm_plan* P, const double2* in, double2* out, const double2* corr, int batch,
-                       cudaStream_t st);
+                       cudaStream_t st, const double2* add = nullptr);
 
 // composite operators (capi.cu)
 template <typename S> void op_apply_A(const helm_plan* P, const S* x, S* y, int batch, cudaStream_t st);

@@ -55,7 +55,27 @@ def _general_pencil_eig(T0: np.ndarray, M0: np.ndarray):
     lam, U = np.linalg.eig(S)
     nrm = np.sqrt(np.einsum("ij,ij->j", U, U))
     U = U / nrm[None, :]
-    return lam, Li.T @ U
+    return _refine_eig(S, lam, U, Li.T)
+
+
+def _refine_eig(S: np.ndarray, lam: np.ndarray, U: np.ndarray, back: np.ndarray):
+    """One Newton step on S U = U diag(lam), U^T U = I for complex-symmetric S
+    (the Ogita-Aishima update with the bilinear form in place of the inner product).
+
+    LAPACK's non-symmetric eig leaves residuals ~1e-14 |S| that the Woodbury strip step
+    amplifies to ~4e-12 in the coarse solve at m0 = 513; one step brings the residual to
+    ~2e-15 (near-degenerate pairs, whose gap is below 1e-8 |S|, are left unmixed)."""
+    R = np.eye(len(S)) - U.T @ U
+    SU = U.T @ (S @ U)
+    lt = np.diag(SU) / (1.0 - np.diag(R))
+    gap = lt[None, :] - lt[:, None]
+    tiny = np.abs(gap) < 1e-8 * np.abs(lt).max()
+    E = np.where(tiny, 0.0, (SU + lt[None, :] * R) / np.where(tiny, 1.0, gap))
+    np.fill_diagonal(E, np.diag(R) / 2)
+    U = U + U @ E
+    nrm = np.sqrt(np.einsum("ij,ij->j", U, U))
+    U = U / nrm[None, :]
+    return lt, back @ U
 
 
 def _bands(A: np.ndarray) -> np.ndarray:
@@ -187,6 +207,12 @@ class CoarseFast:
     cap_left: np.ndarray    # [m0][m0]  V^T M0  (y-pencil eigenbasis, V^T M0 V = I)
     cap_right: np.ndarray   # [m0][m0]  M0 V
     cap_mode: np.ndarray    # [m0][ns][ns]  G_b (I + Gamma_b G_b)^{-1}
+    # strip-space refinement (coarse.cu): the exact coupling on the strips and the
+    # eigen-space approximation of (I + C_U G)^{-1} = I - H G used for the correction
+    cap_vt: np.ndarray      # [m0][m0]  V^T
+    cap_hg: np.ndarray      # [m0][ns][ns]  cap_mode_b Gamma_b
+    strip_lt: np.ndarray    # [ns][ns]  (T0 - T~) on the strip columns
+    strip_lm: np.ndarray    # [ns][ns]  (M0 - M~) on the strip columns
 
 
 def _dense_from_bands(b: np.ndarray) -> np.ndarray:
@@ -205,6 +231,31 @@ def coarse_pencil(grid: Grid, k: float):
     T0 = P @ T @ P.T
     M0 = P @ (w[:, None] * P.T)
     return 0.5 * (T0 + T0.T), 0.5 * (M0 + M0.T), P, T, w
+
+
+def _transform_eigs(A: np.ndarray, dct: bool) -> np.ndarray:
+    """diag(Q^{-1} W^{-1} A Q) of a pentadiagonal A in extended precision.
+
+    The low modes of the stiffness pencil are tiny differences of O(1/h) entries: in
+    fp64 they carry relative errors up to ~1e-11 (eps |T| / lambda_min), which the
+    fast solve turns into a ~3e-12 solution error; long double (64-bit mantissa)
+    sums bring them to the last fp64 bit."""
+    m = len(A)
+    ld = np.longdouble
+    pi = ld("3.14159265358979323846264338327950288")
+    I = np.arange(m, dtype=ld)
+    if dct:
+        Q = np.cos(np.outer(I, I) * (pi / (m - 1)))
+        qn = np.full(m, ld(2) / (m - 1))
+        qn[0] = qn[-1] = ld(1) / (m - 1)
+    else:
+        Q = np.sin(np.outer(I + 1, I + 1) * (pi / (m + 1)))
+        qn = np.full(m, ld(2) / (m + 1))
+    AQ = np.zeros((m, m), dtype=ld)
+    for d in range(-2, 3):
+        i = np.arange(max(0, -d), min(m, m - d))
+        AQ[i] += A[i, i + d].astype(ld)[:, None] * Q[i + d]
+    return ((Q * AQ).sum(axis=0) * qn).astype(np.float64)
 
 
 def coarse_fast(grid: Grid, k: float) -> CoarseFast:
@@ -232,8 +283,8 @@ def coarse_fast(grid: Grid, k: float) -> CoarseFast:
         Tt, Mt = T0.real, M0.real
         strip = np.zeros(0, dtype=np.int32)
     Qi = qnorm[:, None] * Q.T                 # Q^{-1} W^{-1}
-    lamT = np.einsum("aj,ja->a", Qi, Tt @ Q).real
-    lamM = np.einsum("aj,ja->a", Qi, Mt @ Q).real
+    lamT = _transform_eigs(Tt.real, grid.bc == "sommerfeld")
+    lamM = _transform_eigs(Mt.real, grid.bc == "sommerfeld")
     if np.any(lamM <= 0):
         raise SingularMatrixError("coarse mass pencil is not positive definite")
     shifts = lamT / lamM - k**2
@@ -263,11 +314,14 @@ def coarse_fast(grid: Grid, k: float) -> CoarseFast:
         K = np.eye(ns)[None] + Gam @ G
         cap_mode = G @ np.linalg.inv(K)
         cap_left, cap_right = V.T @ M0, M0 @ V
+        cap_vt, cap_hg = V.T, cap_mode @ Gam
     else:
-        cap_mode = np.zeros((m, 0, 0), dt)
-        cap_left = cap_right = np.zeros((0, 0), dt)
+        cap_mode = cap_hg = np.zeros((m, 0, 0), dt)
+        cap_left = cap_right = cap_vt = np.zeros((0, 0), dt)
+        LT = LM = np.zeros((0, 0), dt)
     return CoarseFast(m, 1 if grid.bc == "sommerfeld" else 0, scale, lamT, lamM, float(qnorm[0]), float(k**2), shifts,
                       t0b,
                       m0b.astype(dt), piv,
                       L.astype(dt), U.astype(dt), strip, strip_q, cap_left.astype(dt), cap_right.astype(dt),
-                      cap_mode.astype(dt))
+                      cap_mode.astype(dt), np.ascontiguousarray(cap_vt.astype(dt)), cap_hg.astype(dt),
+                      np.asarray(LT, dt), np.asarray(LM, dt))

@@ -192,7 +192,7 @@ class _Plan:
 
     @staticmethod
     def create(grid: Grid, k: float, kind: str, dec: Decomposition, cf, weights_before_solve=False,
-               max_batch: int = 1, refine_steps: int = 1):
+               max_batch: int = 1, refine_steps: int = 0, strip_refine: int = 1):
         lib = _lib.load()
         cplx = grid.bc == "sommerfeld"
         dt = np.complex128 if cplx else np.float64
@@ -219,7 +219,8 @@ class _Plan:
             arrays = dict(scale=(cf.scale, np.float64), lamT=(cf.lamT, np.float64), lamM=(cf.lamM, np.float64),
                           t0b=(cf.t0b, dt), m0b=(cf.m0b, dt), piv=(cf.piv, np.uint8),
                           L=(cf.L, dt), U=(cf.U, dt), q=(cf.strip_q, np.float64), cl=(cf.cap_left, dt),
-                          cr=(cf.cap_right, dt), cm=(cf.cap_mode, dt))
+                          cr=(cf.cap_right, dt), cm=(cf.cap_mode, dt), vt=(cf.cap_vt, dt), hg=(cf.cap_hg, dt),
+                          lt=(cf.strip_lt, np.complex128), lm=(cf.strip_lm, np.complex128))
             for key, (v, t) in arrays.items():
                 keep[key] = np.ascontiguousarray(v, dtype=t)
             d.coarse_scale = vp(keep["scale"])
@@ -232,6 +233,9 @@ class _Plan:
             if d.n_strip:
                 d.strip_q, d.cap_left, d.cap_right = vp(keep["q"]), vp(keep["cl"]), vp(keep["cr"])
                 d.cap_mode = vp(keep["cm"])
+                d.cap_vt, d.cap_hg = vp(keep["vt"]), vp(keep["hg"])
+                d.strip_lt, d.strip_lm = vp(keep["lt"]), vp(keep["lm"])
+                d.strip_refine = int(strip_refine)
         d.refine_steps = int(refine_steps)
         h = ctypes.c_void_p()
         _lib.check(lib.helm_plan_create(ctypes.byref(d), ctypes.byref(h)))
@@ -291,7 +295,7 @@ class SchwarzPreconditioner:
     KINDS = ("AS2", "SAS2", "SHS2")
 
     def __init__(self, kind, A, decomposition, coarse_space, weights_before_solve=False,
-                 local_factorizations=None, max_batch: int = 1, refine_steps: int = 1):
+                 local_factorizations=None, max_batch: int = 1, refine_steps: int = 0, strip_refine: int = 1):
         if kind not in self.KINDS:
             raise ValueError(f"unknown preconditioner {kind!r}, expected one of {self.KINDS}")
         grid = _grid_of(decomposition)
@@ -309,7 +313,7 @@ class SchwarzPreconditioner:
         self.weights_before_solve = bool(weights_before_solve)
         self.max_batch = int(max_batch)
         self.plan = _Plan.create(grid, self.A.k, kind, self.decomposition, cf, weights_before_solve,
-                                 max_batch=max_batch, refine_steps=refine_steps)
+                                 max_batch=max_batch, refine_steps=refine_steps, strip_refine=strip_refine)
         self.N = self.plan.N
         self.N0 = self.plan.N0
 

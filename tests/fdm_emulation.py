@@ -67,9 +67,25 @@ def x_transform(cf, X):
     return X @ Q
 
 
-def fast_solve(cf, R):
+def _dense_bands(b):
+    m = len(b)
+    A = np.zeros((m, m), dtype=b.dtype)
+    for d in range(-2, 3):
+        i = np.arange(max(0, -d), min(m, m - d))
+        A[i, i + d] = b[i, d + 2]
+    return A
+
+
+def strip_coupling(cf, YS):
+    """C_U y_S = (A0 - B) restricted to the strip columns (strip_rho_kernel)."""
+    T0, M0 = _dense_bands(cf.t0b), _dense_bands(cf.m0b)
+    return T0 @ YS @ cf.strip_lm.T + M0 @ YS @ (cf.strip_lt - cf.k2 * cf.strip_lm).T
+
+
+def fast_solve(cf, R, strip_refine=0):
     """One pass of the device coarse solve (coarse.cu): x-transform, band solves + Woodbury strip
-    step (Sommerfeld) or the separable 2-D DST scaling (Dirichlet), inverse transform."""
+    step (Sommerfeld) or the separable 2-D DST scaling (Dirichlet), inverse transform.
+    strip_refine: Newton steps on the strip coupling (Sommerfeld), each one more band pass."""
     Fh = x_transform(cf, R) * cf.scale[None, :]
     if cf.transform == 0:
         lT, lM = cf.lamT, cf.lamM
@@ -82,17 +98,25 @@ def fast_solve(cf, R):
         yh = cf.cap_left @ Y0S                          # y-eigen coordinates
         ch = np.einsum("bij,bj->bi", cf.cap_mode, yh)   # per-mode 4x4
         cS = cf.cap_right @ ch
-        Fh = Fh - (cS @ cf.strip_q.T) * cf.scale[None, :]
+        Yh = band_solve(cf.piv, cf.L, cf.U, Fh - (cS @ cf.strip_q.T) * cf.scale[None, :])
+        for _ in range(strip_refine):
+            # true residual on the strips, rho = c - C_U y_S (exact: y_S from the band pass)
+            rho = cS - strip_coupling(cf, Yh @ cf.strip_q)
+            t = np.einsum("bij,bj->bi", cf.cap_hg, cf.cap_vt @ rho)
+            w = cf.cap_right @ t - rho               # -(I - H G) rho
+            Yh = Yh + band_solve(cf.piv, cf.L, cf.U, -(w @ cf.strip_q.T) * cf.scale[None, :])
+            cS = cS + w
+        return x_transform(cf, Yh)
     Yh = band_solve(cf.piv, cf.L, cf.U, Fh)
     return x_transform(cf, Yh)
 
 
-def coarse_solve(cf, k, c, refine=1):
+def coarse_solve(cf, k, c, refine=0, strip_refine=1):
     m = cf.m0
     C = c.reshape(m, m)
-    Y = fast_solve(cf, C)
+    Y = fast_solve(cf, C, strip_refine)
     for _ in range(refine):
-        Y = Y + fast_solve(cf, C - a0_apply(cf, k, Y))
+        Y = Y + fast_solve(cf, C - a0_apply(cf, k, Y), strip_refine)
     return Y.ravel()
 
 
