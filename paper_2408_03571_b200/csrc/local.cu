@@ -88,7 +88,7 @@ __global__ void __launch_bounds__(256) local_fdm_kernel(const S* __restrict__ x,
   smem_gemm<S, false, false>(Ly, Lx, Ly, Vy, ld, X, ld, T, ld);
   __syncthreads();
   // Y = T Vx^T, weighted, written out
-  const S* bb = base ? base + (size_t)b * N : nullptr;
+  const S* bb = base ? base + (size_t)b * base_stride(a) : nullptr;
   S* yb = y + (size_t)b * N;
   S* ob = ovl + (size_t)b * 6 * a.nbands * nu;
   for (int e = threadIdx.x; e < Ly * Lx; e += blockDim.x) {
@@ -100,7 +100,7 @@ __global__ void __launch_bounds__(256) local_fdm_kernel(const S* __restrict__ x,
     if (a.weighted && !a.wbs) acc = scale(acc, 1.0 / (my * mx));
     const size_t pidx = (size_t)iy * nu + ix;
     if (my == 1 && mx == 1) {
-      yb[pidx] = bb ? add(bb[pidx], acc) : acc;
+      yb[pidx] = bb ? add(base_at(bb, a, iy, ix), acc) : acc;
     } else if (my == 2) {
       const int ry = ay - a.node_first_box[iy], rx = ax - a.node_first_box[ix];
       ob[((size_t)(ry * 2 + rx) * a.nbands + a.node_band[iy]) * nu + ix] = acc;
@@ -116,7 +116,7 @@ __global__ void __launch_bounds__(256) local_fdm_kernel(const S* __restrict__ x,
 template <typename S>
 __global__ void combine_rows_kernel(const S* __restrict__ base, S* __restrict__ y, const S* __restrict__ ovl,
                                     const int* __restrict__ band_node, const int* __restrict__ node_mult,
-                                    int nu, int nbands) {
+                                    int nu, int nbands, LocalArgs a) {
   const int ix = blockIdx.x * blockDim.x + threadIdx.x;
   const int bi = blockIdx.y;
   if (ix >= nu) return;
@@ -132,13 +132,13 @@ __global__ void combine_rows_kernel(const S* __restrict__ base, S* __restrict__ 
     acc = add(acc, ob[((size_t)3 * nbands + bi) * nu + ix]);
   }
   const size_t pidx = (size_t)iy * nu + ix;
-  y[b * N + pidx] = base ? add(base[b * N + pidx], acc) : acc;
+  y[b * N + pidx] = base ? add(base_at(base + b * base_stride(a), a, iy, ix), acc) : acc;
 }
 
 template <typename S>
 __global__ void combine_cols_kernel(const S* __restrict__ base, S* __restrict__ y, const S* __restrict__ ovl,
                                     const int* __restrict__ band_node, const int* __restrict__ node_mult,
-                                    int nu, int nbands) {
+                                    int nu, int nbands, LocalArgs a) {
   const int bi = blockIdx.x * blockDim.x + threadIdx.x;
   const int iy = blockIdx.y;
   if (bi >= nbands || node_mult[iy] != 1) return;
@@ -148,7 +148,7 @@ __global__ void combine_cols_kernel(const S* __restrict__ base, S* __restrict__ 
   S acc = add(ob[((size_t)0 * nu + iy) * nbands + bi], ob[((size_t)1 * nu + iy) * nbands + bi]);
   const int ix = band_node[bi];
   const size_t pidx = (size_t)iy * nu + ix;
-  y[b * N + pidx] = base ? add(base[b * N + pidx], acc) : acc;
+  y[b * N + pidx] = base ? add(base_at(base + b * base_stride(a), a, iy, ix), acc) : acc;
 }
 
 
@@ -156,11 +156,14 @@ size_t local_smem_bytes(int ld, size_t elem) { return (size_t)(4 * ld * ld + 2 *
 
 template <typename S>
 void launch_local_sum(const helm_plan* P, const S* x, const S* base, S* y, S* ovl, int weighted, int batch,
-                      const int* band_node, cudaStream_t st) {
+                      const int* band_node, cudaStream_t st, bool coarse_base) {
   const PlanDev& d = P->dev;
   HELM_CHECK(d.p > 0, "plan was created without subdomains");
   LocalArgs a;
   a.nu = P->geo.nu;
+  a.coarse_base = coarse_base ? 1 : 0;
+  a.m0 = P->geo.m0;
+  a.off = P->geo.off;
   a.p = d.p;
   a.nbands = d.nbands;
   a.k2 = P->geo.k2;
@@ -190,17 +193,17 @@ void launch_local_sum(const helm_plan* P, const S* x, const S* base, S* y, S* ov
   }
   if (d.nbands > 0) {
     dim3 g1((a.nu + 127) / 128, d.nbands, batch);
-    combine_rows_kernel<S><<<g1, 128, 0, st>>>(base, y, ovl, band_node, d.node_mult, a.nu, d.nbands);
+    combine_rows_kernel<S><<<g1, 128, 0, st>>>(base, y, ovl, band_node, d.node_mult, a.nu, d.nbands, a);
     HELM_LAUNCH_CHECK();
     dim3 g2((d.nbands + 127) / 128, a.nu, batch);
-    combine_cols_kernel<S><<<g2, 128, 0, st>>>(base, y, ovl, band_node, d.node_mult, a.nu, d.nbands);
+    combine_cols_kernel<S><<<g2, 128, 0, st>>>(base, y, ovl, band_node, d.node_mult, a.nu, d.nbands, a);
     HELM_LAUNCH_CHECK();
   }
 }
 
 template void launch_local_sum<double>(const helm_plan*, const double*, const double*, double*, double*, int, int,
-                                       const int*, cudaStream_t);
+                                       const int*, cudaStream_t, bool);
 template void launch_local_sum<double2>(const helm_plan*, const double2*, const double2*, double2*, double2*, int,
-                                        int, const int*, cudaStream_t);
+                                        int, const int*, cudaStream_t, bool);
 
 }  // namespace helm

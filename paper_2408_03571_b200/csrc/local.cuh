@@ -6,6 +6,9 @@ namespace helm {
 
 struct LocalArgs {
   int nu;
+  int coarse_base;  // 1: `base` is a coarse vector c [B][m0][m0]; the base value of a node is (R0^T c)
+  int m0;
+  int off;          // grid offset of the prolongation (Geo::off)
   int p;
   int nbands;
   double k2;
@@ -21,6 +24,81 @@ struct LocalArgs {
   const int* node_mult;
   const int* node_band;
 };
+
+// Base value of fine node (iy, ix): base[pidx] or, in coarse-base mode, the prolongation
+// R0^T c at that node -- the same taps and summation order as prolong_kernel (stencil.cu),
+// so z is never written to / read back from HBM (bb = this right-hand side's base).
+__device__ __forceinline__ void prolong_taps_off(int u, int off, int& U0, int& cnt, double w[3]) {
+  const int t = u - off;  // t = 2U + d
+  if ((t & 1) == 0) {
+    U0 = t / 2 - 1;
+    w[0] = 0.125; w[1] = 0.75; w[2] = 0.125;
+    cnt = 3;
+  } else {
+    U0 = (t - 1) >> 1;
+    w[0] = 0.5; w[1] = 0.5; w[2] = 0.0;
+    cnt = 2;
+  }
+}
+template <typename S>
+__device__ __forceinline__ S base_at(const S* __restrict__ bb, const LocalArgs& a, int iy, int ix) {
+  if (!a.coarse_base) return bb[(size_t)iy * a.nu + ix];
+  int Uy, ny, Ux, nx;
+  double wy[3], wx[3];
+  prolong_taps_off(iy, a.off, Uy, ny, wy);
+  prolong_taps_off(ix, a.off, Ux, nx, wx);
+  S acc = Sc<S>::zero();
+  for (int p = 0; p < ny; ++p) {
+    const int U = Uy + p;
+    if (U < 0 || U >= a.m0) continue;
+    S row = Sc<S>::zero();
+    for (int q = 0; q < nx; ++q) {
+      const int V = Ux + q;
+      if (V < 0 || V >= a.m0) continue;
+      row = fma_(wx[q], __ldg(bb + (size_t)U * a.m0 + V), row);
+    }
+    acc = fma_(wy[p], row, acc);
+  }
+  return acc;
+}
+// Coarse-base mode inside a box kernel: the box's window of c (WIN x WIN, zero outside
+// [0, m0)) is copied to shared memory with cp.async at the start and prolongated from
+// there in the epilogue (same taps and order as prolong_kernel).
+constexpr int WIN = 23;  // >= max box side / 2 + 3 for boxes up to 40 nodes
+template <typename S>
+__device__ __forceinline__ void window_load(S* cw, const S* __restrict__ bb, const LocalArgs& a, int Uby, int Ubx,
+                                            int nthreads) {
+  for (int e = threadIdx.x; e < WIN * WIN; e += nthreads) {
+    const int U = Uby + e / WIN, V = Ubx + e % WIN;
+    const bool in = U >= 0 && U < a.m0 && V >= 0 && V < a.m0;
+    const S* src = bb + (in ? (size_t)U * a.m0 + V : 0);
+    if constexpr (Sc<S>::cplx) cp_async16(&cw[e], src, in);
+    else cp_async8(&cw[e], src, in);
+  }
+  cp_commit();
+}
+__device__ __forceinline__ int window_base(int y0, int off) { return ((y0 - off) >> 1) - 1; }
+template <typename S>
+__device__ __forceinline__ S window_prolong(const S* cw, int off, int Uby, int Ubx, int iy, int ix) {
+  const int ty = iy - off, tx = ix - off;
+  const bool ey = (ty & 1) == 0, ex = (tx & 1) == 0;
+  const int U0 = (ey ? ty / 2 - 1 : (ty - 1) >> 1) - Uby, V0 = (ex ? tx / 2 - 1 : (tx - 1) >> 1) - Ubx;
+  const double wy[3] = {ey ? 0.125 : 0.5, ey ? 0.75 : 0.5, ey ? 0.125 : 0.0};
+  const double wx[3] = {ex ? 0.125 : 0.5, ex ? 0.75 : 0.5, ex ? 0.125 : 0.0};
+  S acc = Sc<S>::zero();
+#pragma unroll
+  for (int p = 0; p < 3; ++p) {
+    S row = Sc<S>::zero();
+#pragma unroll
+    for (int q = 0; q < 3; ++q) row = fma_(wx[q], cw[(U0 + p) * WIN + V0 + q], row);
+    acc = fma_(wy[p], row, acc);
+  }
+  return acc;
+}
+
+__host__ __device__ __forceinline__ size_t base_stride(const LocalArgs& a) {
+  return a.coarse_base ? (size_t)a.m0 * a.m0 : (size_t)a.nu * a.nu;
+}
 
 // Register-blocked FDM for boxes of at most 36 nodes per side (local_fast.cu).
 // Returns false (nothing launched) when the plan's boxes are larger.

@@ -118,6 +118,7 @@ __global__ void __launch_bounds__(DTH, 5) local_fdm_dmma_kernel(const S* __restr
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double* Xr = reinterpret_cast<double*>(smem_raw);  // [DT][XL]
   int* meta = reinterpret_cast<int*>(Xr + DT * XL);  // [2][3][DT]: multiplicity, first box, band per row / column
+  S* cw = reinterpret_cast<S*>(meta + 6 * DT);       // [WIN][WIN] coarse window (coarse-base mode)
   const int sid = boxes[blockIdx.x];
   const int ay = sid / a.p, ax = sid % a.p;
   const int nu = a.nu;
@@ -128,9 +129,12 @@ __global__ void __launch_bounds__(DTH, 5) local_fdm_dmma_kernel(const S* __restr
   const int x0 = a.box_start[ax], Lx = a.box_len[ax];
   const int hy = Ly / 2, hpy = (Ly + 1) / 2, hx = Lx / 2, hpx = (Lx + 1) / 2;
   const S* xb = x + (size_t)b * N;
-  const S* bb = base ? base + (size_t)b * N : nullptr;
+  const S* bb = base ? base + (size_t)b * base_stride(a) : nullptr;
   S* yb = y + (size_t)b * N;
   S* ob = ovl + (size_t)b * 6 * a.nbands * nu;
+  // coarse-base mode: the box's window of c streams into shared memory behind the products
+  const int Uby = window_base(y0, a.off), Ubx = window_base(x0, a.off);
+  if (bb && a.coarse_base) window_load(cw, bb, a, Uby, Ubx, DTH);
   // gather + fold both axes: pair (i, j) of the half-box -> the 4 folded entries
   // (s_y s_x) [i][j], (s_y d_x) [i][DB+j], (d_y s_x) [DB+i][j], (d_y d_x) [DB+i][DB+j]
   const bool wb = a.weighted && a.wbs;
@@ -197,6 +201,7 @@ __global__ void __launch_bounds__(DTH, 5) local_fdm_dmma_kernel(const S* __restr
   __syncthreads();
   // X <- X Vfx^T
   dmma_right<NP, true>(Xr, Vx, [&](int m, int part, int n, double v) { Xr[m * XL + n * NP + part] = v; });
+  cp_wait<0>();
   __syncthreads();
   // unfold + weight + scatter: x_i = e_i + o_i, x_{L-1-i} = e_i - o_i on both axes
   auto get = [&](int i, int j) -> S {
@@ -209,7 +214,7 @@ __global__ void __launch_bounds__(DTH, 5) local_fdm_dmma_kernel(const S* __restr
     const int iy = y0 + r, ix = x0 + q;
     const size_t pidx = (size_t)iy * nu + ix;
     if (my == 1 && mx == 1) {
-      yb[pidx] = bb ? add(bb[pidx], acc) : acc;
+      yb[pidx] = bb ? add(a.coarse_base ? window_prolong(cw, a.off, Uby, Ubx, iy, ix) : bb[pidx], acc) : acc;
     } else if (my == 2) {
       const int ry = ay - meta[DT + r], rx = ax - meta[4 * DT + q];
       ob[((size_t)(ry * 2 + rx) * a.nbands + meta[2 * DT + r]) * nu + ix] = acc;
@@ -240,11 +245,14 @@ void launch_local_dmma(const helm_plan* P, const S* x, const S* base, S* y, S* o
   const PlanDev& d = P->dev;
   if (d.n_ff == 0) return;
   constexpr int NP = Sc<S>::cplx ? 2 : 1;
-  const size_t smem = (size_t)(DT * DmmaDims<NP>::XL) * sizeof(double) + 6 * DT * sizeof(int);
+  const size_t smem = (size_t)(DT * DmmaDims<NP>::XL) * sizeof(double) + 6 * DT * sizeof(int) +
+                      (a.coarse_base ? WIN * WIN * sizeof(S) : 0);
   static bool attr = false;
   if (!attr) {
+    const size_t smax = (size_t)(DT * DmmaDims<NP>::XL) * sizeof(double) + 6 * DT * sizeof(int) +
+                        WIN * WIN * sizeof(S);
     HELM_CUDA(cudaFuncSetAttribute(local_fdm_dmma_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)smem));
+                                   (int)smax));
     attr = true;
   }
   dim3 grd(d.n_ff, batch);

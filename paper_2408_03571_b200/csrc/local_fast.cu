@@ -88,9 +88,12 @@ __device__ __forceinline__ void fdm_box(const S* __restrict__ xb, const S* __res
   VX* Vx = reinterpret_cast<VX*>(Vy + LT * LTD);
   S* ly = reinterpret_cast<S*>(Vx + LT * LTD);
   S* lx = ly + LT;
+  S* cw = lx + LT;  // [WIN][WIN] coarse window (coarse-base mode)
   const int nu = a.nu;
   const int y0 = a.box_start[ay], Ly = a.box_len[ay];
   const int x0 = a.box_start[ax], Lx = a.box_len[ax];
+  const int Uby = window_base(y0, a.off), Ubx = window_base(x0, a.off);
+  if (bb && a.coarse_base) window_load(cw, bb, a, Uby, Ubx, LTH);
   // gather the box (weights first when weights_before_solve, schwarz.py:69-70)
   constexpr int U = 7;
   for (int e0 = threadIdx.x; e0 < Ly * Lx; e0 += U * LTH) {
@@ -128,6 +131,7 @@ __device__ __forceinline__ void fdm_box(const S* __restrict__ xb, const S* __res
   // X <- Vy X
   tile_product<true, S>(Ly, Lx, Ly, [&](int m, int k) { return Vy[m * LTD + k]; },
                   [&](int k, int n) { return X[k * LTD + n]; }, [&](int m, int n, S v) { X[m * LTD + n] = v; });
+  cp_wait<0>();
   __syncthreads();
   // Y = X Vx^T, weighted, written out (overlap nodes into their slot of the scratch)
   tile_product<false, S>(Ly, Lx, Lx, [&](int m, int k) { return X[m * LTD + k]; },
@@ -137,7 +141,8 @@ __device__ __forceinline__ void fdm_box(const S* __restrict__ xb, const S* __res
                     if (a.weighted && !a.wbs) acc = scale(acc, 1.0 / (my * mx));
                     const size_t pidx = (size_t)iy * nu + ix;
                     if (my == 1 && mx == 1) {
-                      yb[pidx] = bb ? add(bb[pidx], acc) : acc;
+                      yb[pidx] = bb ? add(a.coarse_base ? window_prolong(cw, a.off, Uby, Ubx, iy, ix) : bb[pidx], acc)
+                                    : acc;
                     } else if (my == 2) {
                       const int ry = ay - a.node_first_box[iy], rx = ax - a.node_first_box[ix];
                       ob[((size_t)(ry * 2 + rx) * a.nbands + a.node_band[iy]) * nu + ix] = acc;
@@ -164,7 +169,7 @@ __global__ void __launch_bounds__(LTH) local_fdm_fast_kernel(const S* __restrict
   const int b = blockIdx.y;
   const int cy = a.box_class[ay], cx = a.box_class[ax];
   const S* xb = x + (size_t)b * N;
-  const S* bb = base ? base + (size_t)b * N : nullptr;
+  const S* bb = base ? base + (size_t)b * base_stride(a) : nullptr;
   S* yb = y + (size_t)b * N;
   S* ob = ovl + (size_t)b * 6 * a.nbands * a.nu;
   const S* ly = classLam + a.class_off_lam[cy];
@@ -192,7 +197,7 @@ static void fast_launch(const helm_plan* P, const S* x, const S* base, S* y, S* 
   if (nbox == 0) return;
   const PlanDev& d = P->dev;
   const size_t vsz = RR ? sizeof(double) : sizeof(S);
-  const size_t smem = (size_t)LT * LTD * (sizeof(S) + 2 * vsz) + 2 * LT * sizeof(S);
+  const size_t smem = (size_t)LT * LTD * (sizeof(S) + 2 * vsz) + 2 * LT * sizeof(S) + WIN * WIN * sizeof(S);
   static bool attr = false;
   if (!attr) {
     HELM_CUDA(cudaFuncSetAttribute(local_fdm_fast_kernel<S, RR>, cudaFuncAttributeMaxDynamicSharedMemorySize,

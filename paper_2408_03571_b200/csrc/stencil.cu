@@ -276,7 +276,7 @@ __global__ void __launch_bounds__(256) prolong_deflate_kernel(const S* __restric
     const S az = stencil_point<S>(g, vx, u, zc, zs[rr][threadIdx.x + 1], zs[rr + 2][threadIdx.x + 1],
                                   zs[rr + 1][threadIdx.x], zs[rr + 1][threadIdx.x + 2]);
     const size_t p = boff + (size_t)u * nu + vx;
-    z[p] = zc;
+    if (z) z[p] = zc;  // z may be left implicit (coarse-base local sum)
     d[p] = sub(xv[i], az);
   }
 }
