@@ -45,7 +45,7 @@
 extern "C" {
 #endif
 
-#define HELM_ABI_VERSION 3
+#define HELM_ABI_VERSION 4
 
 enum helm_bc { HELM_DIRICHLET = 0, HELM_SOMMERFELD = 1 };
 enum helm_kind { HELM_AS2 = 0, HELM_SAS2 = 1, HELM_SHS2 = 2 };
@@ -94,14 +94,21 @@ typedef struct helm_desc {
   const void* band_u;         /* S [m0][m0][5] {1/U_jj, U_j,j+1 .. U_j,j+4}      */
   int32_t n_strip;            /* 0 (Dirichlet) or 4 (Sommerfeld)                 */
   const double* strip_q;      /* [m0][n_strip]  Q[strip_x[i], a]                 */
-  const void* cap_left;       /* S [m0][m0]  V^T M0 (V: y-pencil eigenvectors)   */
-  const void* cap_right;      /* S [m0][m0]  M0 V                                */
+  /* The y-pencil is reflection symmetric, so its modes are even (first he = (m0+1)/2)
+   * or odd (last ho = m0/2); the three mode matrices are passed as packed half-size
+   * blocks [A_e (he x he) row-major, A_o (ho x ho) row-major]:
+   *   left  (V^T M0, V^T): A_e acts on Z[y] + Z[m0-1-y] (Z[h] alone when m0 is odd),
+   *                        A_o on Z[y] - Z[m0-1-y]  (y < he / ho);
+   *   right (M0 V):        E = A_e c_even, O = A_o c_odd, out[y] = E + O,
+   *                        out[m0-1-y] = E - O.                                     */
+  const void* cap_left;       /* S packed  V^T M0 (V: y-pencil eigenvectors)     */
+  const void* cap_right;      /* S packed  M0 V                                  */
   const void* cap_mode;       /* S [m0][n_strip][n_strip]                        */
   /* strip-space refinement: after the second band pass the exact strip residual
    * rho = c_S - C_U y_S is formed from the band-pass strip values and one more band
    * pass applies B^{-1} of (I - H G) rho (the eigen-space H, G are only ~1e-12
    * accurate; the band passes are exact), see coarse.cu                          */
-  const void* cap_vt;         /* S [m0][m0]  V^T                                 */
+  const void* cap_vt;         /* S packed  V^T                                   */
   const void* cap_hg;         /* S [m0][n_strip][n_strip]  cap_mode_b Gamma_b     */
   const void* strip_lt;       /* S [n_strip][n_strip]  (T0 - T~) on the strips    */
   const void* strip_lm;       /* S [n_strip][n_strip]  (M0 - M~) on the strips    */

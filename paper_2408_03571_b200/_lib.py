@@ -15,7 +15,7 @@ LIB_PATH = os.path.join(_HERE, "libhelmb200.so")
 
 HELM_DIRICHLET, HELM_SOMMERFELD = 0, 1
 KINDS = {"AS2": 0, "SAS2": 1, "SHS2": 2}
-ABI_VERSION = 3
+ABI_VERSION = 4
 
 c_int32_p = ctypes.POINTER(ctypes.c_int32)
 

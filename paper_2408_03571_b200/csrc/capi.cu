@@ -293,14 +293,15 @@ static void build_plan(const helm_desc* d, helm_plan* P) {
     if (d->n_strip) {
       const size_t ns = d->n_strip;
       dv.strip_q = upload<double>(d->strip_q, m0 * ns);
-      dv.cap_left = upload_bytes(d->cap_left, m0 * m0 * P->elem);
-      dv.cap_right = upload_bytes(d->cap_right, m0 * m0 * P->elem);
+      const size_t he = (m0 + 1) / 2, ho = m0 / 2, packed = he * he + ho * ho;
+      dv.cap_left = upload_bytes(d->cap_left, packed * P->elem);
+      dv.cap_right = upload_bytes(d->cap_right, packed * P->elem);
       dv.cap_mode = upload_bytes(d->cap_mode, m0 * ns * ns * P->elem);
       dv.strip_refine = d->strip_refine;
       if (d->strip_refine) {
         HELM_CHECK(d->cap_vt && d->cap_hg && d->strip_lt && d->strip_lm,
                    "strip refinement needs cap_vt, cap_hg, strip_lt and strip_lm");
-        dv.cap_vt = upload_bytes(d->cap_vt, m0 * m0 * P->elem);
+        dv.cap_vt = upload_bytes(d->cap_vt, packed * P->elem);
         dv.cap_hg = upload_bytes(d->cap_hg, m0 * ns * ns * P->elem);
         std::memcpy(dv.strip_lt, d->strip_lt, 16 * sizeof(double2));
         std::memcpy(dv.strip_lm, d->strip_lm, 16 * sizeof(double2));
@@ -521,9 +522,9 @@ int helm_workspace_create(const helm_plan* P, int32_t max_batch, helm_workspace*
     for (void** q : coarse) HELM_CUDA(cudaMalloc(q, B * P->N0 * e));
     const size_t novl = std::max<size_t>(1, B * 6 * (size_t)P->dev.nbands * P->geo.nu);
     HELM_CUDA(cudaMalloc(&w->ovl, novl * e));
-    for (int s = 0; s < 6; ++s)
+    for (int s = 0; s < 7; ++s)
       if (P->dev.n_strip)
-        HELM_CUDA(cudaMalloc(&w->strip[s], (size_t)(s == 3 ? 4 : 1) * P->dev.m0 * B * P->dev.n_strip * e));
+        HELM_CUDA(cudaMalloc(&w->strip[s], (size_t)(s == 3 ? 8 : 1) * P->dev.m0 * B * P->dev.n_strip * e));
     w->red_bytes = krylov_scratch_bytes(4096);
     HELM_CUDA(cudaMalloc(&w->red, w->red_bytes));
     HELM_CUDA(cudaMallocHost(&w->pinned, 64 * sizeof(double)));
@@ -535,7 +536,7 @@ int helm_workspace_destroy(helm_workspace* w) {
   return guarded([&] {
     if (!w) return;
     void* ptrs[] = {w->z, w->d, w->c, w->g, w->y0, w->r0, w->e0, w->f0, w->ovl, w->red, w->strip[0], w->strip[1],
-                    w->strip[2], w->strip[3], w->strip[4], w->strip[5]};
+                    w->strip[2], w->strip[3], w->strip[4], w->strip[5], w->strip[6]};
     for (void* q : ptrs)
       if (q) cudaFree(q);
     if (w->pinned) cudaFreeHost(w->pinned);

@@ -54,152 +54,235 @@ __global__ void __launch_bounds__(256) strip_reduce_kernel(const S* __restrict__
   if (lane < 4) Z[(size_t)y * ldz + (size_t)b * 4 + lane] = acc[lane];
 }
 
-// out[m][b*4+i] = (Hm)? sum_j Hm[m][i][j] t[j] : t[i],  t[j] = sum_y A[m][y] Z[y][b*4+j]
-// Tiled form for many columns: 64 rows x 8 column groups of 4 per CTA (2 rows x 1 group
-// per thread, register-blocked), K split GT_KS ways into a partial-sum scratch that a
-// second kernel reduces in a fixed order (deterministic) and applies the 4x4 epilogue.
-constexpr int GT_M = 64, GT_G = 8, GT_K = 16, GT_KS = 4;
-template <typename S>
-__global__ void __launch_bounds__(256) strip_gemm_part_kernel(const S* __restrict__ A, const S* __restrict__ Z,
-                                                              S* __restrict__ part, int m0, int ngroups) {
-  __shared__ S As[GT_M][GT_K + 1];
-  __shared__ S Zs[GT_K][GT_G * 4];
-  const int ldz = ngroups * 4;
-  const int tr = threadIdx.x / GT_G, tg = threadIdx.x % GT_G;
-  const int kchunk = ((m0 + GT_KS - 1) / GT_KS + GT_K - 1) / GT_K * GT_K;
-  const int kbeg = blockIdx.z * kchunk, kend = min(m0, kbeg + kchunk);
-  S acc[2][4];
-#pragma unroll
-  for (int q = 0; q < 2; ++q)
-#pragma unroll
-    for (int i = 0; i < 4; ++i) acc[q][i] = Sc<S>::zero();
-  for (int k0 = kbeg; k0 < kend; k0 += GT_K) {
-    for (int e = threadIdx.x; e < GT_M * GT_K; e += blockDim.x) {
-      const int r = e / GT_K, kk = e % GT_K;
-      const int mm = blockIdx.y * GT_M + r, k = k0 + kk;
-      As[r][kk] = (mm < m0 && k < kend) ? A[(size_t)mm * m0 + k] : Sc<S>::zero();
-    }
-    for (int e = threadIdx.x; e < GT_K * GT_G * 4; e += blockDim.x) {
-      const int kk = e / (GT_G * 4), c = e % (GT_G * 4);
-      const int k = k0 + kk, col = blockIdx.x * GT_G * 4 + c;
-      Zs[kk][c] = (k < kend && col < ldz) ? Z[(size_t)k * ldz + col] : Sc<S>::zero();
-    }
-    __syncthreads();
-#pragma unroll
-    for (int kk = 0; kk < GT_K; ++kk) {
-      const S a0 = As[2 * tr][kk], a1 = As[2 * tr + 1][kk];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const S zv = Zs[kk][tg * 4 + i];
-        acc[0][i] = fma_(a0, zv, acc[0][i]);
-        acc[1][i] = fma_(a1, zv, acc[1][i]);
-      }
-    }
-    __syncthreads();
-  }
-  const int g = blockIdx.x * GT_G + tg;
-  if (g >= ngroups) return;
-#pragma unroll
-  for (int q = 0; q < 2; ++q) {
-    const int m = blockIdx.y * GT_M + 2 * tr + q;
-    if (m >= m0) continue;
-    S* o = part + ((size_t)blockIdx.z * m0 + m) * ldz + (size_t)g * 4;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) o[i] = acc[q][i];
+// --- strip GEMMs on the folded (even / odd) mode blocks ------------------------
+// The y-pencil is reflection symmetric, so its modes are even (first he) or odd (last ho)
+// and every product with V^T M0, V^T or M0 V splits into two half-size blocks
+// (include/helmb200.h): half the FLOPs and half the matrix bytes of a dense product.
+//   left  (mode <- y):  Zf = [Z[y] + Z[m0-1-y] ; Z[y] - Z[m0-1-y]] (strip_fold_kernel), then
+//                       out[e] = A_e Zf_s, out[he+o] = A_o Zf_d, then the per-mode 4x4 epilogue;
+//   right (y <- mode):  E = A_e c_e, O = A_o c_o, out[y] = E + O, out[m0-1-y] = E - O.
+// Columns are the batch's 4 strip columns per right-hand side (ldn = 4 * batch).
+__global__ void __launch_bounds__(256) strip_fold_kernel(const double2* __restrict__ Z, double2* __restrict__ Zf,
+                                                         int m0, int ldn) {
+  const int he = (m0 + 1) / 2, ho = m0 / 2;
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= he * ldn) return;
+  const int y = e / ldn, c = e % ldn;
+  const double2 a = Z[(size_t)y * ldn + c];
+  if (y < ho) {
+    const double2 b = Z[(size_t)(m0 - 1 - y) * ldn + c];
+    Zf[(size_t)y * ldn + c] = add(a, b);
+    Zf[(size_t)(he + y) * ldn + c] = sub(a, b);
+  } else {
+    Zf[(size_t)y * ldn + c] = a;  // the centre row (odd m0) belongs to the even block only
   }
 }
 
-template <typename S>
-__global__ void __launch_bounds__(256) strip_gemm_reduce_kernel(const S* __restrict__ part, S* __restrict__ out,
-                                                                const S* __restrict__ Hm, const S* __restrict__ minus,
-                                                                int m0, int ngroups) {
-  const int e = blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= m0 * ngroups) return;
-  const int m = e / ngroups, g = e % ngroups;
-  const int ldz = ngroups * 4;
-  S t[4];
+// part[ks][rowoff_g + m][n] = sum_{k in chunk ks} A_g[m][k] B[rowoff_g + k][n], g = even / odd.
+// 64 x 64 complex outputs per CTA (256 threads, 4 x 4 each), K tiles of 16 double-buffered
+// through shared memory with cp.async; split-K over blockIdx.z into a partial-sum scratch
+// reduced in a fixed order (deterministic).
+constexpr int FG_M = 64, FG_N = 64, FG_K = 16, FG_KS = 8;
+struct FoldGemmSmem {
+  double2 A[2][FG_M][FG_K + 1];
+  double2 B[2][FG_K][FG_N];
+};
+__global__ void __launch_bounds__(256) strip_gemm_fold_kernel(const double2* __restrict__ A,
+                                                              const double2* __restrict__ B,
+                                                              double2* __restrict__ part, int m0, int ldn) {
+  extern __shared__ __align__(16) unsigned char sraw[];
+  FoldGemmSmem& sm = *reinterpret_cast<FoldGemmSmem*>(sraw);
+  const int he = (m0 + 1) / 2, ho = m0 / 2;
+  const int tiles_e = (he + FG_M - 1) / FG_M;
+  const int g = blockIdx.y < tiles_e ? 0 : 1;
+  const int Mg = g ? ho : he;
+  const int m0t = (g ? blockIdx.y - tiles_e : blockIdx.y) * FG_M;
+  const double2* Ag = A + (g ? (size_t)he * he : 0);
+  const int rowoff = g ? he : 0;
+  const int n0 = blockIdx.x * FG_N;
+  const int kchunk = ((Mg + FG_KS - 1) / FG_KS + FG_K - 1) / FG_K * FG_K;
+  const int kb = blockIdx.z * kchunk, ke = min(Mg, kb + kchunk);
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  auto issue = [&](int buf, int k0) {
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int e = tid + 256 * r;
+      const int mm = e >> 4, kk = e & 15;
+      const int m = m0t + mm, k = k0 + kk;
+      const bool ok = m < Mg && k < ke;
+      cp_async16(&sm.A[buf][mm][kk], Ag + (ok ? (size_t)m * Mg + k : 0), ok);
+      const int kk2 = e >> 6, nn = e & 63;
+      const int k2 = k0 + kk2, n = n0 + nn;
+      const bool ok2 = k2 < ke && n < ldn;
+      cp_async16(&sm.B[buf][kk2][nn], B + (ok2 ? (size_t)(rowoff + k2) * ldn + n : 0), ok2);
+    }
+    cp_commit();
+  };
+  double2 acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = mk(0.0, 0.0);
+  if (kb < ke) issue(0, kb);
+  int buf = 0;
+  for (int k0 = kb; k0 < ke; k0 += FG_K) {
+    if (k0 + FG_K < ke) {
+      issue(buf ^ 1, k0 + FG_K);
+      cp_wait<1>();
+    } else {
+      cp_wait<0>();
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < FG_K; ++kk) {
+      double2 av[4], bv[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) av[i] = sm.A[buf][ty + 16 * i][kk];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) bv[j] = sm.B[buf][kk][tx + 16 * j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fma_(av[i], bv[j], acc[i][j]);
+    }
+    __syncthreads();
+    buf ^= 1;
+  }
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
-    S s = Sc<S>::zero();
-    for (int ks = 0; ks < GT_KS; ++ks) s = add(s, part[((size_t)ks * m0 + m) * ldz + g * 4 + i]);
-    t[i] = s;
-  }
-  S* o = out + (size_t)m * ldz + (size_t)g * 4;
-  S res[4];
-  if (Hm) {
-    const S* h = Hm + (size_t)m * 16;
+    const int m = m0t + ty + 16 * i;
+    if (m >= Mg) continue;
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      S s = Sc<S>::zero();
-#pragma unroll
-      for (int j = 0; j < 4; ++j) s = fma_(h[i * 4 + j], t[j], s);
-      res[i] = s;
+    for (int j = 0; j < 4; ++j) {
+      const int n = n0 + tx + 16 * j;
+      if (n < ldn) part[((size_t)blockIdx.z * m0 + rowoff + m) * ldn + n] = acc[i][j];
     }
-  } else {
-#pragma unroll
-    for (int i = 0; i < 4; ++i) res[i] = t[i];
   }
-  const S* mi = minus ? minus + (size_t)m * ldz + (size_t)g * 4 : nullptr;
-#pragma unroll
-  for (int i = 0; i < 4; ++i) o[i] = mi ? sub(res[i], mi[i]) : res[i];
 }
 
-// Warp-per-row form for few columns (batch <= 4): lanes stride over y.
-template <typename S, int NG>
-__global__ void __launch_bounds__(256) strip_gemm_rows_kernel(const S* __restrict__ A, const S* __restrict__ Z,
-                                                              S* __restrict__ out, const S* __restrict__ Hm,
-                                                              const S* __restrict__ minus, int m0) {
-  const int m = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+// Warp-per-row form for few columns (batch <= 4): part[0][row][.] for the packed row.
+template <int NC>
+__global__ void __launch_bounds__(256) strip_gemm_fold_rows_kernel(const double2* __restrict__ A,
+                                                                   const double2* __restrict__ B,
+                                                                   double2* __restrict__ part, int m0) {
+  const int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
-  if (m >= m0) return;
-  constexpr int NC = NG * 4;
-  S acc[NC];
+  if (r >= m0) return;
+  const int he = (m0 + 1) / 2;
+  const int g = r < he ? 0 : 1;
+  const int Mg = g ? m0 / 2 : he, rowoff = g ? he : 0;
+  const double2* arow = A + (g ? (size_t)he * he : 0) + (size_t)(r - rowoff) * Mg;
+  double2 acc[NC];
 #pragma unroll
-  for (int c = 0; c < NC; ++c) acc[c] = Sc<S>::zero();
-  for (int y = lane; y < m0; y += 32) {
-    const S av = A[(size_t)m * m0 + y];
+  for (int c = 0; c < NC; ++c) acc[c] = mk(0.0, 0.0);
+  for (int k = lane; k < Mg; k += 32) {
+    const double2 av = arow[k];
 #pragma unroll
-    for (int c = 0; c < NC; ++c) acc[c] = fma_(av, Z[(size_t)y * NC + c], acc[c]);
+    for (int c = 0; c < NC; ++c) acc[c] = fma_(av, B[(size_t)(rowoff + k) * NC + c], acc[c]);
   }
 #pragma unroll
   for (int c = 0; c < NC; ++c) acc[c] = warp_sum(acc[c]);
-  if (lane != 0) return;
-  const S* h = Hm ? Hm + (size_t)m * 16 : nullptr;
+  if (lane < NC) {
+    double2 v = acc[0];
 #pragma unroll
-  for (int g = 0; g < NG; ++g) {
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      S s;
-      if (h) {
-        s = Sc<S>::zero();
-#pragma unroll
-        for (int j = 0; j < 4; ++j) s = fma_(h[i * 4 + j], acc[g * 4 + j], s);
-      } else {
-        s = acc[g * 4 + i];
-      }
-      if (minus) s = sub(s, minus[(size_t)m * NC + g * 4 + i]);
-      out[(size_t)m * NC + g * 4 + i] = s;
-    }
+    for (int c = 1; c < NC; ++c)
+      if (lane == c) v = acc[c];
+    part[(size_t)r * NC + lane] = v;
   }
 }
 
-// out = [Hm] (A Z) [- minus]
-template <typename S>
-static void strip_gemm(const S* A, const S* Z, S* out, const S* Hm, int m0, int batch, S* part, cudaStream_t st,
-                       const S* minus = nullptr) {
+// left epilogue: out[r][g*4+i] = sum_j H[r][i][j] t[j],  t = sum_ks part[ks][r][g*4+.]
+__global__ void __launch_bounds__(256) strip_reduce_left_kernel(const double2* __restrict__ part,
+                                                                double2* __restrict__ out,
+                                                                const double2* __restrict__ Hm, int m0,
+                                                                int ngroups, int nks) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= m0 * ngroups) return;
+  const int r = e / ngroups, g = e % ngroups;
+  const size_t ldn = (size_t)ngroups * 4;
+  double2 t[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    double2 s = mk(0.0, 0.0);
+    for (int ks = 0; ks < nks; ++ks) s = add(s, part[((size_t)ks * m0 + r) * ldn + g * 4 + i]);
+    t[i] = s;
+  }
+  const double2* h = Hm + (size_t)r * 16;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    double2 s = mk(0.0, 0.0);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) s = fma_(h[i * 4 + j], t[j], s);
+    out[(size_t)r * ldn + g * 4 + i] = s;
+  }
+}
+
+// right epilogue: E = rows [0, he), O = rows [he, m0) of the partials;
+// out[y] = E + O (- minus[y]), out[m0-1-y] = E - O (- minus[m0-1-y]), out[h] = E (odd m0)
+__global__ void __launch_bounds__(256) strip_reduce_right_kernel(const double2* __restrict__ part,
+                                                                 double2* __restrict__ out,
+                                                                 const double2* __restrict__ minus, int m0,
+                                                                 int ldn, int nks) {
+  const int he = (m0 + 1) / 2, ho = m0 / 2;
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= he * ldn) return;
+  const int y = e / ldn, c = e % ldn;
+  double2 E = mk(0.0, 0.0), O = mk(0.0, 0.0);
+  for (int ks = 0; ks < nks; ++ks) {
+    E = add(E, part[((size_t)ks * m0 + y) * ldn + c]);
+    if (y < ho) O = add(O, part[((size_t)ks * m0 + he + y) * ldn + c]);
+  }
+  if (y < ho) {
+    double2 lo = add(E, O), hi = sub(E, O);
+    const size_t pl = (size_t)y * ldn + c, ph = (size_t)(m0 - 1 - y) * ldn + c;
+    if (minus) {
+      lo = sub(lo, minus[pl]);
+      hi = sub(hi, minus[ph]);
+    }
+    out[pl] = lo;
+    out[ph] = hi;
+  } else {
+    const size_t pl = (size_t)y * ldn + c;
+    out[pl] = minus ? sub(E, minus[pl]) : E;
+  }
+}
+
+// out = fold-GEMM of Zin with the packed blocks A; left: + 4x4 epilogue Hm (Zin in y order,
+// folded here into Zf); right: unfolded, minus subtracted (Zin in mode order).
+static void strip_gemm_fold(const double2* A, const double2* Zin, double2* out, bool left, const double2* Hm,
+                            const double2* minus, int m0, int batch, double2* Zf, double2* part, cudaStream_t st) {
+  const int ldn = 4 * batch, he = (m0 + 1) / 2, ho = m0 / 2;
+  const double2* B = Zin;
+  if (left) {
+    strip_fold_kernel<<<(he * ldn + 255) / 256, 256, 0, st>>>(Zin, Zf, m0, ldn);
+    HELM_LAUNCH_CHECK();
+    B = Zf;
+  }
+  int nks = 1;
   const int rows_blocks = (m0 * 32 + 255) / 256;
   switch (batch) {
-    case 1: strip_gemm_rows_kernel<S, 1><<<rows_blocks, 256, 0, st>>>(A, Z, out, Hm, minus, m0); break;
-    case 2: strip_gemm_rows_kernel<S, 2><<<rows_blocks, 256, 0, st>>>(A, Z, out, Hm, minus, m0); break;
-    case 3: strip_gemm_rows_kernel<S, 3><<<rows_blocks, 256, 0, st>>>(A, Z, out, Hm, minus, m0); break;
-    case 4: strip_gemm_rows_kernel<S, 4><<<rows_blocks, 256, 0, st>>>(A, Z, out, Hm, minus, m0); break;
+    case 1: strip_gemm_fold_rows_kernel<4><<<rows_blocks, 256, 0, st>>>(A, B, part, m0); break;
+    case 2: strip_gemm_fold_rows_kernel<8><<<rows_blocks, 256, 0, st>>>(A, B, part, m0); break;
+    case 3: strip_gemm_fold_rows_kernel<12><<<rows_blocks, 256, 0, st>>>(A, B, part, m0); break;
+    case 4: strip_gemm_fold_rows_kernel<16><<<rows_blocks, 256, 0, st>>>(A, B, part, m0); break;
     default: {
-      dim3 grd((batch + GT_G - 1) / GT_G, (m0 + GT_M - 1) / GT_M, GT_KS);
-      strip_gemm_part_kernel<S><<<grd, 256, 0, st>>>(A, Z, part, m0, batch);
-      HELM_LAUNCH_CHECK();
-      strip_gemm_reduce_kernel<S><<<(m0 * batch + 255) / 256, 256, 0, st>>>(part, out, Hm, minus, m0, batch);
+      static bool attr = false;
+      if (!attr) {
+        HELM_CUDA(cudaFuncSetAttribute(strip_gemm_fold_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)sizeof(FoldGemmSmem)));
+        attr = true;
+      }
+      const int tiles = (he + FG_M - 1) / FG_M + (ho + FG_M - 1) / FG_M;
+      dim3 grd((ldn + FG_N - 1) / FG_N, tiles, FG_KS);
+      strip_gemm_fold_kernel<<<grd, 256, sizeof(FoldGemmSmem), st>>>(A, B, part, m0, ldn);
+      nks = FG_KS;
     }
   }
+  HELM_LAUNCH_CHECK();
+  if (left)
+    strip_reduce_left_kernel<<<(m0 * batch + 255) / 256, 256, 0, st>>>(part, out, Hm, m0, batch, nks);
+  else
+    strip_reduce_right_kernel<<<(he * ldn + 255) / 256, 256, 0, st>>>(part, out, minus, m0, ldn, nks);
   HELM_LAUNCH_CHECK();
 }
 
@@ -353,8 +436,10 @@ static void fast_solve(const helm_plan* P, helm_workspace* ws, const S* in, S* o
     strip_reduce_kernel<S><<<grd, 256, 0, st>>>(T2, d.strip_q, Z, d.m0, batch * 4);
     HELM_LAUNCH_CHECK();
     S* part = (S*)ws->strip[3];
-    strip_gemm<S>((const S*)d.cap_left, Z, Ch, (const S*)d.cap_mode, d.m0, batch, part, st);
-    strip_gemm<S>((const S*)d.cap_right, Ch, Cs, nullptr, d.m0, batch, part, st);
+    S* Zf = (S*)ws->strip[6];
+    strip_gemm_fold((const double2*)d.cap_left, Z, Ch, true, (const double2*)d.cap_mode, nullptr, d.m0, batch, Zf,
+                    part, st);
+    strip_gemm_fold((const double2*)d.cap_right, Ch, Cs, false, nullptr, nullptr, d.m0, batch, Zf, part, st);
     launch_band_solve(P, T1, T2, Cs, batch, st);
     // strip refinement: rho = cS - C_U y_S from this pass's strip values (exact), the
     // correction W = H G rho - rho from the eigen-space operators (only ~1e-12 accurate,
@@ -373,8 +458,9 @@ static void fast_solve(const helm_plan* P, helm_workspace* ws, const S* in, S* o
       strip_rho_kernel<<<(d.m0 * batch + 255) / 256, 256, 0, st>>>(Cs, Z, R, (const double2*)d.t0_band,
                                                                   (const double2*)d.m0_band, cp, d.m0, batch);
       HELM_LAUNCH_CHECK();
-      strip_gemm<S>((const S*)d.cap_vt, R, Ch, (const S*)d.cap_hg, d.m0, batch, part, st);
-      strip_gemm<S>((const S*)d.cap_right, Ch, W, nullptr, d.m0, batch, part, st, R);
+      strip_gemm_fold((const double2*)d.cap_vt, R, Ch, true, (const double2*)d.cap_hg, nullptr, d.m0, batch, Zf,
+                      part, st);
+      strip_gemm_fold((const double2*)d.cap_right, Ch, W, false, nullptr, R, d.m0, batch, Zf, part, st);
       launch_band_solve(P, nullptr, T3, W, batch, st, T2);  // T3 = T2 + B^{-1}(-ext(W))
       if (it + 1 < d.strip_refine) {
         const size_t ns = (size_t)d.m0 * batch * 4;

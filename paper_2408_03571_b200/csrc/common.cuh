@@ -232,7 +232,7 @@ struct helm_workspace {
   void* e0;       // [B][N0]
   void* f0;       // [B][N0]
   void* ovl;      // overlap scratch [B][6][nbands][nu]
-  void* strip[6]; // coarse Woodbury scratch [m0][B * n_strip]: Z, C^, C_S, split-K partials (x4), rho, W
+  void* strip[7]; // coarse Woodbury scratch [m0][B * n_strip]: Z, C^, C_S, split-K partials (x8), rho, W, Zf
   void* red;      // reduction scratch (doubles)
   size_t red_bytes;
   void* pinned;   // small pinned host buffer for scalar read-back

@@ -58,6 +58,53 @@ def _general_pencil_eig(T0: np.ndarray, M0: np.ndarray):
     return _refine_eig(S, lam, U, Li.T)
 
 
+def fold_bases(m: int):
+    """Bases of the reflection-even / -odd subspaces of R^m (y -> m-1-y): Pe [m][he], Po [m][ho]."""
+    he, ho = (m + 1) // 2, m // 2
+    Pe = np.zeros((m, he))
+    Po = np.zeros((m, ho))
+    j = np.arange(ho)
+    Pe[j, j] = Pe[m - 1 - j, j] = 1.0
+    if he > ho:
+        Pe[ho, ho] = 1.0
+    Po[j, j] = 1.0
+    Po[m - 1 - j, j] = -1.0
+    return Pe, Po
+
+
+def folded_pencil_eig(T0: np.ndarray, M0: np.ndarray):
+    """T0 V = M0 V diag(lam), V^T M0 V = I for a reflection-symmetric pencil (J T0 J = T0,
+    J M0 J = M0, J the y-reversal), solved on the even and odd subspaces separately: the
+    modes come out exactly even (first he) or odd (last ho), so every product with V or
+    V^T M0 folds to two half-size blocks (coarse.cu strip GEMMs)."""
+    m = len(M0)
+    J = np.arange(m)[::-1]
+    if np.any(T0[np.ix_(J, J)] != T0) or np.any(M0[np.ix_(J, J)] != M0):
+        raise ValueError("coarse y-pencil is not reflection symmetric")
+    Pe, Po = fold_bases(m)
+    lams, Vs = [], []
+    for Pb in (Pe, Po):
+        lb, Ub = _general_pencil_eig(Pb.T @ T0 @ Pb, Pb.T @ M0 @ Pb)
+        lams.append(lb)
+        Vs.append(Pb @ Ub)
+    return np.concatenate(lams), np.concatenate(Vs, axis=1)
+
+
+def fold_blocks(A: np.ndarray, kind: str) -> np.ndarray:
+    """Packed half-size blocks of a mode/space matrix with reflection-parity structure:
+    kind "left" (rows = modes [even; odd], columns = y: V^T M0, V^T) -> [A_e (he x he), A_o (ho x ho)]
+    acting on Z_s = Z[y] + Z[m-1-y] (Z[h] alone for odd m) and Z_d = Z[y] - Z[m-1-y];
+    kind "right" (rows = y, columns = modes: M0 V) -> [A_e, A_o] giving E[y] (y < he) and O[y]
+    (y < ho), unfolded as out[y] = E + O, out[m-1-y] = E - O."""
+    m = len(A)
+    he, ho = (m + 1) // 2, m // 2
+    if kind == "left":
+        Ae, Ao = A[:he, :he], A[he:, :ho]
+    else:
+        Ae, Ao = A[:he, :he], A[:ho, he:]
+    return np.concatenate([np.ascontiguousarray(Ae).ravel(), np.ascontiguousarray(Ao).ravel()])
+
+
 def _refine_eig(S: np.ndarray, lam: np.ndarray, U: np.ndarray, back: np.ndarray):
     """One Newton step on S U = U diag(lam), U^T U = I for complex-symmetric S
     (the Ogita-Aishima update with the bilinear form in place of the inner product).
@@ -306,7 +353,7 @@ def coarse_fast(grid: Grid, k: float) -> CoarseFast:
     if ns:
         LT = (T0 - Tt)[np.ix_(strip, strip)]
         LM = (M0 - Mt)[np.ix_(strip, strip)]
-        lam, V = _general_pencil_eig(T0, M0)
+        lam, V = folded_pencil_eig(T0, M0)
         den = lamM[None, :] * lam[:, None] + (lamT - k**2 * lamM)[None, :]  # [b][a]
         # Gamma_b[i][j] = sum_a Q[x_i,a] (Q^{-1}W^{-1})[a,x_j] / den[b,a]
         Gam = np.einsum("ai,aj,ba->bij", strip_q, Qi[:, strip], 1.0 / den)

@@ -22,7 +22,7 @@ import torch
 
 from . import _lib
 from .discretization import CoarseSpace, Decomposition, Grid, PROBLEMS, build_hocs, extend, partition
-from .fdm_setup import SingularMatrixError, coarse_fast, local_classes
+from .fdm_setup import SingularMatrixError, coarse_fast, fold_blocks, local_classes
 
 __all__ = [
     "HelmholtzOperator",
@@ -218,9 +218,11 @@ class _Plan:
         if cf is not None:  # fast-transform + Woodbury coarse solver
             arrays = dict(scale=(cf.scale, np.float64), lamT=(cf.lamT, np.float64), lamM=(cf.lamM, np.float64),
                           t0b=(cf.t0b, dt), m0b=(cf.m0b, dt), piv=(cf.piv, np.uint8),
-                          L=(cf.L, dt), U=(cf.U, dt), q=(cf.strip_q, np.float64), cl=(cf.cap_left, dt),
-                          cr=(cf.cap_right, dt), cm=(cf.cap_mode, dt), vt=(cf.cap_vt, dt), hg=(cf.cap_hg, dt),
+                          L=(cf.L, dt), U=(cf.U, dt), q=(cf.strip_q, np.float64), cm=(cf.cap_mode, dt), hg=(cf.cap_hg, dt),
                           lt=(cf.strip_lt, np.complex128), lm=(cf.strip_lm, np.complex128))
+            if len(cf.strip_x):  # packed even/odd blocks (include/helmb200.h)
+                arrays.update(cl=(fold_blocks(cf.cap_left, "left"), dt), cr=(fold_blocks(cf.cap_right, "right"), dt),
+                              vt=(fold_blocks(cf.cap_vt, "left"), dt))
             for key, (v, t) in arrays.items():
                 keep[key] = np.ascontiguousarray(v, dtype=t)
             d.coarse_scale = vp(keep["scale"])
