@@ -15,6 +15,8 @@
 // cp.async in chunks of R rows, ST chunks in flight, so HBM latency hides behind
 // the FP64 recurrence.  The forward sweep writes the eliminated right-hand side to
 // `out`; the backward sweep streams it back with U.
+#include <cstdlib>
+
 #include "ops.cuh"
 
 namespace helm {
@@ -262,13 +264,24 @@ static void band_launch(const helm_plan* P, const double2* in, double2* out, con
   HELM_LAUNCH_CHECK();
 }
 
+// batches up to this size use the segmented solve (HELM_BAND_SEG_MAX overrides; 0 disables)
+static int band_seg_max_batch() {
+  static int v = [] {
+    const char* e = std::getenv("HELM_BAND_SEG_MAX");
+    return e ? std::atoi(e) : 4;
+  }();
+  return v;
+}
+
 void launch_band_solve(const helm_plan* P, const double2* in, double2* out, const double2* corr, int batch,
                        cudaStream_t st, const double2* add) {
   HELM_CHECK(P->dev.band_piv != nullptr, "plan has no band factors");
   HELM_CHECK((const void*)in != (const void*)out && (const void*)add != (const void*)out,
              "band solve: input and output must not alias");
   HELM_CHECK(in != nullptr || corr != nullptr, "band solve: no right-hand side");
-  if (batch == 1)
+  if (batch <= band_seg_max_batch() && P->dev.band_seg)
+    band_seg_launch(P, in, out, corr, batch, st, add);  // segmented recurrence: latency-bound regime
+  else if (batch == 1)
     band_launch<1, 1, 8, 4>(P, in, out, corr, batch, st, add);  // latency-bound recurrence
   else if (batch <= 4)
     band_launch<2, 2, 8, 3>(P, in, out, corr, batch, st, add);

@@ -1,0 +1,282 @@
+// Segmented band solves for small batches (part of K5, the Sommerfeld coarse solve;
+// the recurrence and its factors are described in band.cu).
+//
+// band.cu runs each mode's 2*m0-step row recurrence (forward elimination with the
+// pivoted L, backward substitution with U) on one lane: at batch 1 that is 33 warps on
+// the whole GPU, each waiting on ~2000 dependent steps (0.38 ms per solve at m0=1025).
+// Here the m0 rows of a mode are cut into SEG segments and the recurrence is solved as
+// a linear recurrence with a carried state:
+//
+//   forward  state (r0, r1) (the two pending eliminated rows):  s_out = Phi_k s_in + p_k
+//   backward state (x[j+1..j+4]) (the last four solution rows): t_out = Psi_k t_in + q_k
+//
+// Phi_k (2x2) and Psi_k (4x4) depend on the factors only; they are computed once per plan
+// (band_seg_setup_kernel).  Per solve, every (mode, segment) thread
+//   F1  runs its segment's forward recurrence from a zero state  -> p_k
+//   --  the CTA chains the segments:  s_{k+1} = Phi_k s_k + p_k  (one thread per mode)
+//   F3  re-runs the segment from its true state, keeping the eliminated rows in shared memory
+//   B1  runs the backward recurrence over those rows from a zero state -> q_k
+//   --  chains downwards:  t_{k-1} = Psi_k t_k + q_k
+//   B3  re-runs from the true state and writes x (+ add).
+// Exact in exact arithmetic (the same linear recurrence, associated differently); 1025-row
+// modes become 32-row segments, so the dependent chain is ~130 steps instead of ~2050.
+// Right-hand side handling (in, corr/q/sig, add) is the same contract as band_solve_kernel.
+#include "ops.cuh"
+
+namespace helm {
+
+constexpr int SEG = 32;  // segments per mode
+constexpr int SMB = 8;   // modes per CTA (8 consecutive modes = one 128-byte row segment)
+constexpr int SEG_THREADS = SEG * SMB;
+
+struct SegRhs {
+  const double2* in;
+  const double2* corr;
+  int ldc;
+  int b;
+  double qa[4];
+  double sa;
+  size_t col;  // b * N0 + a
+  int m0;
+  __device__ __forceinline__ double2 operator()(int y) const {
+    if (y >= m0) return mk(0.0, 0.0);
+    double2 v = in ? __ldg(in + col + (size_t)y * m0) : mk(0.0, 0.0);
+    if (corr) {
+      const double2* c4 = corr + (size_t)y * ldc + (size_t)b * 4;
+      double2 c = mk(0.0, 0.0);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) c = fma_(qa[i], __ldg(c4 + i), c);
+      v = sub(v, scale(c, sa));
+    }
+    return v;
+  }
+};
+
+__device__ __forceinline__ void fwd_step(int pv, double2 l0, double2 l1, double2& r0, double2& r1, double2 f,
+                                         double2& out) {
+  double2 x0 = r0, x1 = r1, x2 = f;
+  if (pv == 1) {
+    const double2 t = x0; x0 = x1; x1 = t;
+  } else if (pv == 2) {
+    const double2 t = x0; x0 = x2; x2 = t;
+  }
+  x1 = fms_(l0, x0, x1);
+  x2 = fms_(l1, x0, x2);
+  out = x0;
+  r0 = x1;
+  r1 = x2;
+}
+
+__device__ __forceinline__ double2 bwd_step(const double2* __restrict__ u, double2 v, double2 (&y)[4]) {
+  v = fms_(__ldg(u + 1), y[0], v);
+  v = fms_(__ldg(u + 2), y[1], v);
+  v = fms_(__ldg(u + 3), y[2], v);
+  v = fms_(__ldg(u + 4), y[3], v);
+  v = mul(v, __ldg(u));
+  y[3] = y[2];
+  y[2] = y[1];
+  y[1] = y[0];
+  y[0] = v;
+  return v;
+}
+
+// forward pass over rows [j0, j1) with state (r0, r1); writes eliminated rows to sm (if non-null)
+template <bool STORE>
+__device__ __forceinline__ void fwd_run(const SegRhs& rhs, const int* __restrict__ piv, const double2* __restrict__ L,
+                                        int m0, int a, int j0, int j1, double2& r0, double2& r1, double2* sm,
+                                        int sm_stride) {
+  constexpr int C = 4;
+  int j = j0;
+  for (; j + C <= j1; j += C) {
+    int pv[C];
+    double2 l0[C], l1[C], f[C];
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+      const size_t e = (size_t)(j + c) * m0 + a;
+      pv[c] = __ldg(piv + e);
+      l0[c] = __ldg(L + 2 * e);
+      l1[c] = __ldg(L + 2 * e + 1);
+      f[c] = rhs(j + c + 2);
+    }
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+      double2 o;
+      fwd_step(pv[c], l0[c], l1[c], r0, r1, f[c], o);
+      if (STORE) sm[(j + c - j0) * sm_stride] = o;
+    }
+  }
+  for (; j < j1; ++j) {
+    const size_t e = (size_t)j * m0 + a;
+    double2 o;
+    fwd_step(__ldg(piv + e), __ldg(L + 2 * e), __ldg(L + 2 * e + 1), r0, r1, rhs(j + 2), o);
+    if (STORE) sm[(j - j0) * sm_stride] = o;
+  }
+}
+
+template <typename Emit>
+__device__ __forceinline__ void bwd_run(const double2* __restrict__ U, int m0, int a, int j0, int j1,
+                                        double2 (&y)[4], const double2* sm, int sm_stride, Emit&& emit) {
+#pragma unroll 4
+  for (int j = j1 - 1; j >= j0; --j) {
+    const double2 v = bwd_step(U + 5 * ((size_t)j * m0 + a), sm ? sm[(j - j0) * sm_stride] : mk(0.0, 0.0), y);
+    emit(j, v);
+  }
+}
+
+// Phi [SEG][4][m0], Psi [SEG][16][m0]: exit state of segment k for unit entry states
+__global__ void band_seg_setup_kernel(const int* __restrict__ piv, const double2* __restrict__ L,
+                                      const double2* __restrict__ U, int m0, int ls, double2* __restrict__ phi,
+                                      double2* __restrict__ psi) {
+  const int a = blockIdx.x * blockDim.x + threadIdx.x;
+  const int k = blockIdx.y;
+  if (a >= m0) return;
+  const int j0 = min(k * ls, m0), j1 = min(j0 + ls, m0);
+  SegRhs zero{nullptr, nullptr, 0, 0, {0, 0, 0, 0}, 0.0, 0, m0};
+  for (int c = 0; c < 2; ++c) {
+    double2 r0 = mk(c == 0 ? 1.0 : 0.0, 0.0), r1 = mk(c == 1 ? 1.0 : 0.0, 0.0);
+    fwd_run<false>(zero, piv, L, m0, a, j0, j1, r0, r1, nullptr, 0);
+    phi[((size_t)k * 4 + 0 * 2 + c) * m0 + a] = r0;
+    phi[((size_t)k * 4 + 1 * 2 + c) * m0 + a] = r1;
+  }
+  for (int c = 0; c < 4; ++c) {
+    double2 y[4];
+    for (int i = 0; i < 4; ++i) y[i] = mk(i == c ? 1.0 : 0.0, 0.0);
+    bwd_run(U, m0, a, j0, j1, y, nullptr, 0, [](int, double2) {});
+    for (int r = 0; r < 4; ++r) psi[((size_t)k * 16 + r * 4 + c) * m0 + a] = y[r];
+  }
+}
+
+__global__ void __launch_bounds__(SEG_THREADS) band_seg_kernel(
+    const double2* __restrict__ in, double2* __restrict__ out, const int* __restrict__ piv,
+    const double2* __restrict__ L, const double2* __restrict__ U, const double2* __restrict__ phi,
+    const double2* __restrict__ psi, int m0, int ls, const double2* __restrict__ corr, const double* __restrict__ q,
+    const double* __restrict__ sig, int ldc, const double2* __restrict__ addv) {
+  extern __shared__ __align__(16) unsigned char sraw[];
+  double2* rows = reinterpret_cast<double2*>(sraw);  // [ls][SEG][SMB] eliminated rows
+  __shared__ double2 fst[SEG + 1][SMB][2];           // forward states at segment starts
+  __shared__ double2 bst[SEG + 1][SMB][4];           // backward states at segment tops
+  const int al = threadIdx.x % SMB, k = threadIdx.x / SMB;
+  const int a = blockIdx.x * SMB + al;
+  const int b = blockIdx.y;
+  const bool va = a < m0;
+  const size_t N0 = (size_t)m0 * m0;
+  const int j0 = min(k * ls, m0), j1 = min(j0 + ls, m0);
+  SegRhs rhs{in, corr, ldc, b, {0, 0, 0, 0}, 0.0, (size_t)b * N0 + (va ? a : 0), m0};
+  if (corr && va) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) rhs.qa[i] = __ldg(q + (size_t)a * 4 + i);
+    rhs.sa = __ldg(sig + a);
+  }
+  const int ac = va ? a : 0;
+  const int sstride = SEG * SMB;
+  double2* mysm = rows + k * SMB + al;
+
+  // F1: zero-state forward pass (segment 0 starts from the true rows 0, 1)
+  double2 r0 = mk(0.0, 0.0), r1 = mk(0.0, 0.0);
+  if (k == 0) {
+    r0 = rhs(0);
+    r1 = rhs(1);
+  }
+  fwd_run<false>(rhs, piv, L, m0, ac, j0, j1, r0, r1, nullptr, 0);
+  fst[k + 1][al][0] = r0;
+  fst[k + 1][al][1] = r1;
+  __syncthreads();
+  // chain: s_{k+1} = Phi_k s_k + p_k (s_1 = p_0)
+  if (k == 0 && va) {
+    double2 s0 = fst[1][al][0], s1 = fst[1][al][1];
+    for (int kk = 1; kk < SEG; ++kk) {
+      const double2* P = phi + (size_t)kk * 4 * m0 + a;
+      const double2 n0 = add(fst[kk + 1][al][0], add(mul(__ldg(P), s0), mul(__ldg(P + m0), s1)));
+      const double2 n1 = add(fst[kk + 1][al][1], add(mul(__ldg(P + 2 * m0), s0), mul(__ldg(P + 3 * m0), s1)));
+      fst[kk][al][0] = s0;  // entry state of segment kk
+      fst[kk][al][1] = s1;
+      s0 = n0;
+      s1 = n1;
+    }
+  }
+  __syncthreads();
+  // F3: true forward pass, eliminated rows kept in shared memory
+  if (k == 0) {
+    r0 = rhs(0);
+    r1 = rhs(1);
+  } else {
+    r0 = fst[k][al][0];
+    r1 = fst[k][al][1];
+  }
+  fwd_run<true>(rhs, piv, L, m0, ac, j0, j1, r0, r1, mysm, sstride);
+  // B1: zero-state backward pass
+  double2 y[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) y[i] = mk(0.0, 0.0);
+  bwd_run(U, m0, ac, j0, j1, y, mysm, sstride, [](int, double2) {});
+#pragma unroll
+  for (int i = 0; i < 4; ++i) bst[k][al][i] = y[i];
+  __syncthreads();
+  // chain downwards: the state entering segment k is the exit state of segment k+1
+  if (k == 0 && va) {
+    double2 t[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) t[i] = bst[SEG - 1][al][i];  // the top segment starts from zeros
+    for (int kk = SEG - 2; kk >= 0; --kk) {
+      double2 n[4];
+      const double2* P = psi + (size_t)kk * 16 * m0 + a;
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        double2 s = bst[kk][al][r];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) s = fma_(__ldg(P + (r * 4 + c) * m0), t[c], s);
+        n[r] = s;
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        bst[kk + 1][al][i] = t[i];  // entry state of segment kk  (stored one slot up)
+        t[i] = n[i];
+      }
+    }
+  }
+  __syncthreads();
+  // B3: true backward pass
+#pragma unroll
+  for (int i = 0; i < 4; ++i) y[i] = k == SEG - 1 ? mk(0.0, 0.0) : bst[k + 1][al][i];
+  double2* o = out + (size_t)b * N0 + ac;
+  const double2* ad = addv ? addv + (size_t)b * N0 + ac : nullptr;
+  bwd_run(U, m0, ac, j0, j1, y, mysm, sstride, [&](int j, double2 v) {
+    if (va) o[(size_t)j * m0] = ad ? ::helm::add(v, __ldg(ad + (size_t)j * m0)) : v;
+  });
+}
+
+static int seg_len(int m0) { return (m0 + SEG - 1) / SEG; }
+
+size_t band_seg_table_elems(int m0) { return (size_t)SEG * 20 * m0; }
+
+bool band_seg_usable(int m0) { return m0 >= 4 * SEG && seg_len(m0) <= 48; }
+
+void band_seg_setup(const PlanDev& d, double2* tables, cudaStream_t st) {
+  const int m0 = d.m0;
+  double2* phi = tables;
+  double2* psi = tables + (size_t)SEG * 4 * m0;
+  band_seg_setup_kernel<<<dim3((m0 + 127) / 128, SEG), 128, 0, st>>>(
+      d.band_piv, (const double2*)d.band_l, (const double2*)d.band_u, m0, seg_len(m0), phi, psi);
+  HELM_LAUNCH_CHECK();
+}
+
+void band_seg_launch(const helm_plan* P, const double2* in, double2* out, const double2* corr, int batch,
+                     cudaStream_t st, const double2* add) {
+  const PlanDev& d = P->dev;
+  const int m0 = d.m0, ls = seg_len(m0);
+  const size_t smem = (size_t)ls * SEG * SMB * sizeof(double2);
+  static bool attr = false;
+  if (!attr) {
+    HELM_CUDA(cudaFuncSetAttribute(band_seg_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    attr = true;
+  }
+  HELM_CHECK(smem <= 200 * 1024, "segmented band solve: segment too long");
+  const double2* phi = d.band_seg;
+  const double2* psi = d.band_seg + (size_t)SEG * 4 * m0;
+  band_seg_kernel<<<dim3((m0 + SMB - 1) / SMB, batch), SEG_THREADS, smem, st>>>(
+      in, out, d.band_piv, (const double2*)d.band_l, (const double2*)d.band_u, phi, psi, m0, ls, corr, d.strip_q,
+      d.coarse_scale, batch * 4, add);
+  HELM_LAUNCH_CHECK();
+}
+
+}  // namespace helm

@@ -283,6 +283,11 @@ static void build_plan(const helm_desc* d, helm_plan* P) {
       dv.band_piv = upload<int>(piv32.data(), piv32.size());
       dv.band_l = upload_bytes(d->band_l, m0 * m0 * 2 * P->elem);
       dv.band_u = upload_bytes(d->band_u, m0 * m0 * 5 * P->elem);
+      if (band_seg_usable(m0)) {
+        HELM_CUDA(cudaMalloc(&dv.band_seg, band_seg_table_elems(m0) * sizeof(double2)));
+        band_seg_setup(dv, dv.band_seg, 0);
+        HELM_CUDA(cudaStreamSynchronize(0));
+      }
     } else {
       dv.coarse_lamT = upload<double>(d->coarse_lamT, m0);
       dv.coarse_lamM = upload<double>(d->coarse_lamM, m0);
@@ -457,7 +462,7 @@ static void free_plan(helm_plan* P) {
   void* ptrs[] = {dv.box_start, dv.box_len, dv.box_class, dv.class_len, dv.class_off_V, dv.class_off_lam,
                   dv.class_V, dv.class_lambda, dv.class_real, dv.class_Vr, dv.box_ff, dv.class_Vf, dv.class_lamf, dv.class_invden, dv.box_rr, dv.box_mix,
                   dv.node_first_box, dv.node_mult, dv.node_band, dv.band_node,
-                  dv.coarse_scale, dv.twiddle, dv.coarse_lamT, dv.coarse_lamM, dv.t0_band, dv.m0_band, dv.band_piv, dv.band_l, dv.band_u, dv.strip_q,
+                  dv.coarse_scale, dv.twiddle, dv.coarse_lamT, dv.coarse_lamM, dv.t0_band, dv.m0_band, dv.band_piv, dv.band_l, dv.band_u, dv.band_seg, dv.strip_q,
                   dv.cap_left, dv.cap_right, dv.cap_mode, dv.cap_vt, dv.cap_hg};
   for (void* q : ptrs)
     if (q) cudaFree(q);

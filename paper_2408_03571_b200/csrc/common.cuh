@@ -175,6 +175,7 @@ struct PlanDev {
   int* band_piv;        // Sommerfeld band LU (pivot offsets widened to int for 4-byte cp.async)
   void* band_l;
   void* band_u;
+  double2* band_seg;    // segment propagators of the small-batch band solve (band_seg.cu), or null
   int n_strip;
   double* strip_q;
   void* cap_left;

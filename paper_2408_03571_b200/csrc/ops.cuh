@@ -20,6 +20,11 @@ template <typename S>
 void launch_xform(const helm_plan* P, const S* in, S* out, const double* sig, bool scale2d, int batch,
                   cudaStream_t st, bool accumulate = false);
 template <typename S> void launch_transpose(const S* in, S* out, int m, int batch, cudaStream_t st);
+size_t band_seg_table_elems(int m0);
+bool band_seg_usable(int m0);
+void band_seg_setup(const PlanDev& d, double2* tables, cudaStream_t st);
+void band_seg_launch(const helm_plan* P, const double2* in, double2* out, const double2* corr, int batch,
+                     cudaStream_t st, const double2* add);
 void launch_band_solve(const helm_plan* P, const double2* in, double2* out, const double2* corr, int batch,
                        cudaStream_t st, const double2* add = nullptr);
 

@@ -176,3 +176,32 @@ def test_pipelined_host_apply_matches_device():
         hi = min(19, lo + M.PIPE_CHUNK)
         ref[lo:hi] = M(X[lo:hi].cuda())
     assert torch.equal(Yh, ref.cpu())
+
+
+@pytest.mark.parametrize("n,k,p", [(257, 50.0, 8), (513, 100.0, 16)])
+def test_segmented_band_solve_matches_lane_recurrence(n, k, p):
+    """Small batches run the coarse band solves as a segmented linear recurrence
+    (band_seg.cu), larger ones one lane per mode (band.cu): same solve, different
+    association.  Both must agree to rounding, and the coarse solve must satisfy A0 y = c."""
+    import paper_2408_03571_b200 as hb
+
+    grid = hb.Grid(n, "sommerfeld")
+    prob = hb.assemble(grid, k, "MP2")
+    dec = hb.extend(hb.partition(grid, p), 2)
+    cs = hb.galerkin(hb.build_hocs(grid, 2), prob.A)
+    M = hb.SchwarzPreconditioner("SHS2", prob.A, dec, cs, max_batch=8)
+    import scipy.sparse as sp
+    import helmdd_oracle as O  # checker only: A0 = R0 A R0^T
+
+    og = O.OGrid(n, "sommerfeld")
+    oprob = O.assemble(og, k, "MP2")
+    P1 = O.bezier_1d(og, 2)
+    r0 = sp.kron(P1, P1, format="csr").astype(complex)
+    a0 = (r0 @ oprob.A @ r0.T).tocsr()
+    rng = np.random.default_rng(3)
+    C = rng.standard_normal((8, M.N0)) + 1j * rng.standard_normal((8, M.N0))
+    Yb = M.coarse_solve(torch.from_numpy(C).cuda()).cpu().numpy()  # batch 8: lane recurrence
+    for i in (0, 5):
+        y1 = M.coarse_solve(C[i])  # batch 1: segmented recurrence
+        assert rel(y1, Yb[i]) <= 1e-13
+        assert np.linalg.norm(a0 @ y1 - C[i]) / np.linalg.norm(C[i]) <= 1e-12
