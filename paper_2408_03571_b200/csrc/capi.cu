@@ -113,23 +113,19 @@ static void gmres_impl(const helm_plan* P, helm_workspace* ws, const S* b, S* x,
   HELM_CHECK(side == 0 || side == 1, "side must be 0 (right) or 1 (left)");
   const size_t N = (size_t)P->N;
   const bool left = side == 1;
-  // The Krylov basis grows on demand (capacity doubling, contiguous so the CGS2
-  // kernels see one [vectors][N] array): the reference allocates (cap+1) N eagerly
-  // (gmres.py:88-89), which at n=2049 and cap 1000 would be 67 GB.
-  int vcap = std::min(mi + 1, 32);
-  DevBuf<S> V((size_t)vcap * N, st), H((size_t)(mi + 1) * mi, st), cs(mi, st), sn(mi, st), g(mi + 1, st),
-      y(mi + 1, st), u(N, st), r(N, st);
+  // The Krylov basis lives in the workspace (basis.cu): address space for the cap is
+  // reserved, physical memory is mapped in chunks of 16 vectors as j grows and kept for
+  // later solves; the reference allocates (cap+1) N eagerly (gmres.py:88-89), which at
+  // n=2049 and cap 1000 would be 67 GB.
+  const size_t vbytes = N * sizeof(S);
+  S* Vp = nullptr;
   auto ensure_basis = [&](int nvec) {
-    if (nvec <= vcap) return;
-    const int ncap = std::min(mi + 1, std::max(nvec, 2 * vcap));
-    S* np = nullptr;
-    HELM_CUDA(cudaMallocAsync((void**)&np, (size_t)ncap * N * sizeof(S), st));
-    HELM_CUDA(cudaMemcpyAsync(np, V.p, (size_t)vcap * N * sizeof(S), cudaMemcpyDeviceToDevice, st));
-    HELM_CUDA(cudaFreeAsync(V.p, st));
-    V.p = np;
-    vcap = ncap;
+    Vp = (S*)basis_ensure(ws, (size_t)nvec * vbytes, (size_t)(mi + 1) * vbytes, 16 * vbytes, st);
   };
-  DevBuf<char> scratch(krylov_scratch_bytes(mi + 1), st);
+  ensure_basis(2);
+  DevBuf<S> H((size_t)(mi + 1) * mi, st), cs(mi, st), sn(mi, st), g(mi + 1, st), y(mi + 1, st), u(N, st), r(N, st);
+  HELM_CHECK(krylov_scratch_bytes(mi + 1) <= ws->red_bytes, "iteration cap too large for the workspace scratch");
+  void* scratch = ws->red;
   DevBuf<double> scal(16, st);
   HELM_CUDA(cudaMemsetAsync(H.p, 0, (size_t)(mi + 1) * mi * sizeof(S), st));
   HELM_CUDA(cudaMemsetAsync(cs.p, 0, mi * sizeof(S), st));
@@ -158,19 +154,19 @@ static void gmres_impl(const helm_plan* P, helm_workspace* ws, const S* b, S* x,
   };
 
   // ||b||, r0 (gmres.py:77-86)
-  krylov_norm2<S>(b, N, scal.p, scratch.p, st);
+  krylov_norm2<S>(b, N, scal.p, scratch, st);
   if (left)
-    applyM(b, V.p);
+    applyM(b, Vp);
   else
-    HELM_CUDA(cudaMemcpyAsync(V.p, b, N * sizeof(S), cudaMemcpyDeviceToDevice, st));
-  krylov_norm2<S>(V.p, N, scal.p + 1, scratch.p, st);
+    HELM_CUDA(cudaMemcpyAsync(Vp, b, N * sizeof(S), cudaMemcpyDeviceToDevice, st));
+  krylov_norm2<S>(Vp, N, scal.p + 1, scratch, st);
   read_scalars(scal.p, 2);
   const double bnorm = std::sqrt(hp[0]), beta = std::sqrt(hp[1]);
   HELM_CHECK(bnorm != 0.0, "right-hand side must be nonzero");
   // V[0] = r0 / beta ; g[0] = beta
   double sc[2] = {1.0 / beta, beta};
   HELM_CUDA(cudaMemcpyAsync(scal.p + 6, sc, 2 * sizeof(double), cudaMemcpyHostToDevice, st));
-  krylov_scale<S>(V.p, V.p, scal.p + 6, 0, N, st);
+  krylov_scale<S>(Vp, Vp, scal.p + 6, 0, N, st);
   S g0 = Sc<S>::from_real(beta);
   HELM_CUDA(cudaMemcpyAsync(g.p, &g0, sizeof(S), cudaMemcpyHostToDevice, st));
   if (history) history[0] = 1.0;
@@ -178,15 +174,15 @@ static void gmres_impl(const helm_plan* P, helm_workspace* ws, const S* b, S* x,
   auto form_solution = [&](int j) {  // gmres.py:98-105
     krylov_backsolve<S>(H.p, mi, j, g.p, y.p, st);
     if (left) {
-      krylov_combine<S>(x, V.p, j + 1, N, y.p, N, st);
+      krylov_combine<S>(x, Vp, j + 1, N, y.p, N, st);
     } else {
-      krylov_combine<S>(r.p, V.p, j + 1, N, y.p, N, st);
+      krylov_combine<S>(r.p, Vp, j + 1, N, y.p, N, st);
       applyM(r.p, x);
     }
   };
   auto true_residual = [&]() {  // ||b - A x|| / ||b||  (gmres.py:153)
     launch_stencil<S>(P->geo, b, x, r.p, 1, st);
-    krylov_norm2<S>(r.p, N, scal.p + 8, scratch.p, st);
+    krylov_norm2<S>(r.p, N, scal.p + 8, scratch, st);
     read_scalars(scal.p + 8, 1);
     return std::sqrt(hp[0]) / bnorm;
   };
@@ -194,10 +190,11 @@ static void gmres_impl(const helm_plan* P, helm_workspace* ws, const S* b, S* x,
   bool done = false;
   for (int j = 0; j < mi && !done; ++j) {
     ensure_basis(j + 2);
-    S* vj = V.p + (size_t)j * N;
+    S* vj = Vp + (size_t)j * N;
     applyOp(vj, vj + N);
-    krylov_cgs2_impl<S>(V.p, j, N, N, H.p + j, (size_t)mi, scal.p + 2, scratch.p, st);
-    krylov_givens<S>(H.p, mi, j, cs.p, sn.p, g.p, beta, scal.p + 4, st);
+    // CGS2 (3 sweeps) with the Givens update of column j fused into its reducing block
+    krylov_cgs2_impl<S>(Vp, j, N, N, H.p + j, (size_t)mi, scal.p + 2, scratch, st, H.p, mi, cs.p, sn.p, g.p, beta,
+                        scal.p + 4);
     HELM_CUDA(cudaMemcpyAsync(hp, scal.p + 2, 3 * sizeof(double), cudaMemcpyDeviceToHost, st));
     HELM_CUDA(cudaStreamSynchronize(st));
     const bool brk = hp[1] != 0.0;
@@ -532,6 +529,7 @@ int helm_workspace_create(const helm_plan* P, int32_t max_batch, helm_workspace*
         HELM_CUDA(cudaMalloc(&w->strip[s], (size_t)(s == 3 ? 8 : 1) * P->dev.m0 * B * P->dev.n_strip * e));
     w->red_bytes = krylov_scratch_bytes(4096);
     HELM_CUDA(cudaMalloc(&w->red, w->red_bytes));
+    HELM_CUDA(cudaMemset(w->red, 0, w->red_bytes));  // the CGS2 completion counters start at zero
     HELM_CUDA(cudaMallocHost(&w->pinned, 64 * sizeof(double)));
     *out = w;
   });
@@ -540,6 +538,7 @@ int helm_workspace_create(const helm_plan* P, int32_t max_batch, helm_workspace*
 int helm_workspace_destroy(helm_workspace* w) {
   return guarded([&] {
     if (!w) return;
+    basis_free(w);
     void* ptrs[] = {w->z, w->d, w->c, w->g, w->y0, w->r0, w->e0, w->f0, w->ovl, w->red, w->strip[0], w->strip[1],
                     w->strip[2], w->strip[3], w->strip[4], w->strip[5], w->strip[6]};
     for (void* q : ptrs)

@@ -237,4 +237,5 @@ struct helm_workspace {
   void* red;      // reduction scratch (doubles)
   size_t red_bytes;
   void* pinned;   // small pinned host buffer for scalar read-back
+  void* basis;    // GMRES Krylov basis (basis.cu: reserved address range, physical chunks on demand)
 };

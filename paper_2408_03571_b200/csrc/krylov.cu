@@ -2,10 +2,10 @@
 // (reference gmres.py:108-148: MGS + one conditional re-orthogonalisation pass,
 // complex Givens rotations, residual estimate |g[j+1]| / ||r0||).
 //
-// B200 form: classical Gram-Schmidt run twice (CGS2).  Each pass is one
-// multi-dot sweep of the basis (h = V^H w, block + warp-shuffle reductions,
-// deterministic two-stage sum) and one fused update sweep (w -= V h, with the
-// squared norm of the result reduced in the same sweep).  In exact arithmetic
+// B200 form: classical Gram-Schmidt run twice (CGS2) in three sweeps of the
+// basis (the second pass's dots ride on the first pass's update sweep, the
+// norm comes from Pythagoras, the Givens update runs in the reducing block;
+// details below).  In exact arithmetic
 // CGS2 equals MGS + re-orthogonalisation; numerically both keep the basis
 // orthogonal to working precision, which is what fixes the iteration count.
 // H, the rotations and g stay on the device; the host reads one estimate.
@@ -15,52 +15,6 @@ namespace helm {
 
 constexpr int KB = 256;        // threads per block
 constexpr int KNB = 4 * 148;   // reduction blocks (4 per SM)
-constexpr int KG = 8;          // vectors per multi-dot group
-
-// partial[i * gridDim.x + block] = sum over the block's elements of conj(V_i) w
-template <typename S>
-__global__ void __launch_bounds__(KB) dots_kernel(const S* __restrict__ V, int nvec, size_t ldv,
-                                                  const S* __restrict__ w, size_t N, S* __restrict__ partial) {
-  __shared__ S red[KG][KB / 32];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const size_t stride = (size_t)gridDim.x * blockDim.x;
-  for (int i0 = 0; i0 < nvec; i0 += KG) {
-    const int ng = min(KG, nvec - i0);
-    S acc[KG];
-#pragma unroll
-    for (int g = 0; g < KG; ++g) acc[g] = Sc<S>::zero();
-    for (size_t n = blockIdx.x * (size_t)blockDim.x + threadIdx.x; n < N; n += stride) {
-      const S wn = w[n];
-#pragma unroll
-      for (int g = 0; g < KG; ++g)
-        if (g < ng) acc[g] = add(acc[g], cmul(V[(size_t)(i0 + g) * ldv + n], wn));
-    }
-#pragma unroll
-    for (int g = 0; g < KG; ++g) {
-      S s = warp_sum(acc[g]);
-      if (lane == 0) red[g][wid] = s;
-    }
-    __syncthreads();
-    if (threadIdx.x < ng) {
-      S s = Sc<S>::zero();
-      for (int q = 0; q < KB / 32; ++q) s = add(s, red[threadIdx.x][q]);
-      partial[(size_t)(i0 + threadIdx.x) * gridDim.x + blockIdx.x] = s;
-    }
-    __syncthreads();
-  }
-}
-
-// out[i] = sum_b partial[i * nb + b]   (one warp per output, fixed order)
-template <typename S>
-__global__ void reduce_rows_kernel(const S* __restrict__ partial, int nvec, int nb, S* __restrict__ out) {
-  const int i = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
-  const int lane = threadIdx.x & 31;
-  if (i >= nvec) return;
-  S s = Sc<S>::zero();
-  for (int b = lane; b < nb; b += 32) s = add(s, partial[(size_t)i * nb + b]);
-  s = warp_sum(s);
-  if (lane == 0) out[i] = s;
-}
 
 // w <- w + sign * sum_i h_i V_i ; optionally norm2 partial of the result per block
 template <typename S>
@@ -124,33 +78,6 @@ __global__ void sum_partials_kernel(const double* __restrict__ npart, int nb, do
   if (threadIdx.x == 0) *out = s;
 }
 
-// hcol[i] = h1[i] + h2[i] (i <= j), hcol[j+1] = ||w||, breakdown test of gmres.py:125,
-// inv[0] = 1/||w|| (0 on breakdown so the scaling pass is skipped)
-template <typename S>
-__global__ void cgs2_finalize_kernel(const S* __restrict__ h1, const S* __restrict__ h2, const double* __restrict__ n2,
-                                     int j, S* __restrict__ hcol, size_t hstride, double* __restrict__ inv) {
-  __shared__ double mx[32];
-  const double hn = sqrt(*n2);
-  double m = 0.0;
-  for (int i = threadIdx.x; i <= j; i += blockDim.x) {
-    const S v = add(h1[i], h2[i]);
-    hcol[(size_t)i * hstride] = v;
-    m = fmax(m, sqrt(abs2(v)));
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
-  if ((threadIdx.x & 31) == 0) mx[threadIdx.x >> 5] = m;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    for (int q = 1; q < (int)(blockDim.x / 32); ++q) m = fmax(m, mx[q]);
-    m = fmax(mx[0], m);
-    hcol[(size_t)(j + 1) * hstride] = Sc<S>::from_real(hn);
-    const bool brk = hn <= 1e-14 * fmax(fmax(m, hn), 1.0);
-    inv[0] = brk ? 0.0 : 1.0 / hn;
-    inv[1] = brk ? 1.0 : 0.0;
-  }
-}
-
 template <typename S>
 __global__ void scale_kernel(S* __restrict__ x, const S* __restrict__ src, const double* __restrict__ s, int invert,
                              size_t N) {
@@ -160,13 +87,190 @@ __global__ void scale_kernel(S* __restrict__ x, const S* __restrict__ src, const
     x[n] = scale(src[n], f);
 }
 
-// --- Givens update of column j (gmres.py:129-148), one thread --------------
+// --- y = R^{-1} g with R = H[:j+1, :j+1] upper triangular (gmres.py:98-103) -----
+template <typename S>
+__global__ void backsolve_kernel(const S* __restrict__ H, int ldh, int j, const S* __restrict__ g, S* __restrict__ y) {
+  extern __shared__ __align__(16) unsigned char sraw[];
+  S* rhs = reinterpret_cast<S*>(sraw);
+  __shared__ S yi_s;
+  for (int i = threadIdx.x; i <= j; i += blockDim.x) rhs[i] = g[i];
+  __syncthreads();
+  for (int i = j; i >= 0; --i) {
+    if (threadIdx.x == 0) {
+      const S d = H[(size_t)i * ldh + i];
+      // singular R: the reference falls back to lstsq; a zero component is used here
+      yi_s = abs2(d) == 0.0 ? Sc<S>::zero() : div_(rhs[i], d);
+      y[i] = yi_s;
+    }
+    __syncthreads();
+    const S yi = yi_s;
+    for (int k = threadIdx.x; k < i; k += blockDim.x) rhs[k] = fms_(H[(size_t)k * ldh + i], yi, rhs[k]);
+    __syncthreads();
+  }
+}
+
+// ----------------------------------------------------------------------------
+// CGS2 in three sweeps of the basis (B_o = (3(j+1) + 5) N s of HBM traffic)
+//
+//   K1  h1 = V^H w                                     (sweep 1: V, w)
+//   K2  w' = w - V h1 (stored), h2 = V^H w', ||w'||^2    (sweep 2: V from HBM for the
+//       update, the second read of the same chunk for the dots hits L2)
+//       last block: h2, ||w''|| = sqrt(||w'||^2 - ||h2||^2) (Pythagoras: w'' = w' - V h2
+//       with V^H w' = h2), H[:, j] = h1 + h2, breakdown test, 1/||w''||, optional Givens
+//   K3  V[j+1] = (w' - V h2) / ||w''||                  (sweep 3)
+// Block partials are combined by the last block to finish (threadfence + counter), in a
+// fixed order: the result is deterministic.
+// ----------------------------------------------------------------------------
+constexpr int CG = 8;  // vectors per reduction group
+
+// 8 complex/real values per lane -> lane l holds the warp total of value (l >> 2) & 7
+template <typename S> __device__ __forceinline__ S shfl_x(S v, int o);
+template <> __device__ __forceinline__ double shfl_x<double>(double v, int o) {
+  return __shfl_xor_sync(0xffffffffu, v, o);
+}
+template <> __device__ __forceinline__ double2 shfl_x<double2>(double2 v, int o) {
+  return mk(__shfl_xor_sync(0xffffffffu, v.x, o), __shfl_xor_sync(0xffffffffu, v.y, o));
+}
+template <typename S> __device__ __forceinline__ S reduce8(const S (&v)[CG], int lane) {
+  const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4;
+  S u[4], t[2];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) u[q] = add(b4 ? v[q + 4] : v[q], shfl_x(b4 ? v[q] : v[q + 4], 16));
+#pragma unroll
+  for (int q = 0; q < 2; ++q) t[q] = add(b3 ? u[q + 2] : u[q], shfl_x(b3 ? u[q] : u[q + 2], 8));
+  S s = add(b2 ? t[1] : t[0], shfl_x(b2 ? t[0] : t[1], 4));
+  s = add(s, shfl_x(s, 2));
+  s = add(s, shfl_x(s, 1));
+  return s;
+}
+
+// scratch layout (fixed offsets first: the counters must stay put and start at zero)
+//   [count 2 x u32 | pad][scal 8 doubles][npart KNB doubles][h1 nv S][h2 nv S][partial nv x KNB S]
+struct CgsScratch {
+  unsigned* count; // [2]
+  double* scal;    // [8]
+  double* npart;   // [KNB]
+  void* h1;        // [nvec] S
+  void* h2;        // [nvec] S
+  void* partial;   // [nvec][KNB] S
+};
+size_t krylov_scratch_bytes(int max_vec) {
+  const size_t nv = (size_t)((max_vec + CG - 1) / CG) * CG;
+  return 64 + 8 * sizeof(double) + KNB * sizeof(double) + 2 * nv * sizeof(double2) + nv * KNB * sizeof(double2);
+}
+static CgsScratch carve(void* scratch, int max_vec) {
+  const size_t nv = (size_t)((max_vec + CG - 1) / CG) * CG;
+  char* p = (char*)scratch;
+  CgsScratch k;
+  k.count = (unsigned*)p;
+  p += 64;
+  k.scal = (double*)p;
+  p += 8 * sizeof(double);
+  k.npart = (double*)p;
+  p += KNB * sizeof(double);
+  k.h1 = p;
+  p += nv * sizeof(double2);
+  k.h2 = p;
+  p += nv * sizeof(double2);
+  k.partial = p;
+  return k;
+}
+
+// Block-level accumulation of sum_n conj(V_i[n]) x[n] for i in [0, nvec): per chunk of
+// KB elements (one per thread) and group of CG vectors, each warp reduces its 8 sums
+// (reduce8) and warp totals are added to sacc in warp order.
+template <typename S, bool UPDATE>
+__device__ __forceinline__ void block_dots(const S* __restrict__ V, int nvec, size_t ldv, S* __restrict__ w, size_t N,
+                                           const S* hs, S* sacc, S (*red)[CG], double* nrm_out) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  double nrm = 0.0;
+  for (size_t base = (size_t)blockIdx.x * KB; base < N; base += (size_t)gridDim.x * KB) {
+    const size_t n = base + threadIdx.x;
+    const bool ok = n < N;
+    S x = ok ? w[n] : Sc<S>::zero();
+    if (UPDATE) {  // x <- x - V h1 (read V from HBM), store, then the dots re-read V (L2)
+      if (ok) {
+        int i = 0;
+        for (; i + 4 <= nvec; i += 4) {
+          const S v0 = V[(size_t)i * ldv + n], v1 = V[(size_t)(i + 1) * ldv + n];
+          const S v2 = V[(size_t)(i + 2) * ldv + n], v3 = V[(size_t)(i + 3) * ldv + n];
+          x = fms_(hs[i], v0, x);
+          x = fms_(hs[i + 1], v1, x);
+          x = fms_(hs[i + 2], v2, x);
+          x = fms_(hs[i + 3], v3, x);
+        }
+        for (; i < nvec; ++i) x = fms_(hs[i], V[(size_t)i * ldv + n], x);
+        w[n] = x;
+        nrm += abs2(x);
+      }
+    }
+    for (int i0 = 0; i0 < nvec; i0 += CG) {
+      S acc[CG];
+#pragma unroll
+      for (int g = 0; g < CG; ++g)
+        acc[g] = (ok && i0 + g < nvec) ? cmul(V[(size_t)(i0 + g) * ldv + n], x) : Sc<S>::zero();
+      const S s = reduce8(acc, lane);
+      if ((lane & 3) == 0) red[wid][lane >> 2] = s;
+      __syncthreads();
+      if (threadIdx.x < CG && i0 + threadIdx.x < nvec) {
+        S t = sacc[i0 + threadIdx.x];
+#pragma unroll
+        for (int q = 0; q < KB / 32; ++q) t = add(t, red[q][threadIdx.x]);
+        sacc[i0 + threadIdx.x] = t;
+      }
+      __syncthreads();
+    }
+  }
+  if (UPDATE) *nrm_out = nrm;
+}
+
+// last block to arrive? (threadfence + counter; the counter is reset for the next use)
+__device__ __forceinline__ bool last_block(unsigned* count) {
+  __shared__ bool last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned t = atomicAdd(count, 1u);
+    last = t == gridDim.x - 1;
+    if (last) *count = 0;
+  }
+  __syncthreads();
+  return last;
+}
+
+template <typename S>
+__device__ __forceinline__ void sum_partials(const S* __restrict__ partial, int nvec, S* out) {
+  // one warp per vector, fixed order
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int i = wid; i < nvec; i += KB / 32) {
+    S s = Sc<S>::zero();
+    for (int b = lane; b < (int)gridDim.x; b += 32) s = add(s, partial[(size_t)i * gridDim.x + b]);
+    s = warp_sum(s);
+    if (lane == 0) out[i] = s;
+  }
+}
+
+template <typename S>
+__global__ void __launch_bounds__(KB) cgs_dots_kernel(const S* __restrict__ V, int nvec, size_t ldv,
+                                                      const S* __restrict__ w, size_t N, S* __restrict__ partial,
+                                                      S* __restrict__ h, unsigned* __restrict__ count) {
+  extern __shared__ __align__(16) unsigned char sraw[];
+  S* sacc = reinterpret_cast<S*>(sraw);
+  __shared__ S red[KB / 32][CG];
+  for (int i = threadIdx.x; i < nvec; i += KB) sacc[i] = Sc<S>::zero();
+  __syncthreads();
+  block_dots<S, false>(V, nvec, ldv, const_cast<S*>(w), N, nullptr, sacc, red, nullptr);
+  for (int i = threadIdx.x; i < nvec; i += KB) partial[(size_t)i * gridDim.x + blockIdx.x] = sacc[i];
+  if (last_block(count)) sum_partials(partial, nvec, h);
+}
+
 __device__ __forceinline__ double cabs_(double a) { return fabs(a); }
 __device__ __forceinline__ double cabs_(double2 a) { return hypot(a.x, a.y); }
+
+// Givens update of column j (gmres.py:129-148), one thread
 template <typename S>
-__global__ void givens_kernel(S* __restrict__ H, int ldh, int j, S* __restrict__ cs, S* __restrict__ sn,
-                              S* __restrict__ g, double beta, double* __restrict__ est) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+__device__ void givens_apply(S* __restrict__ H, int ldh, int j, S* __restrict__ cs, S* __restrict__ sn,
+                             S* __restrict__ g, double beta, double* __restrict__ est) {
   for (int i = 0; i < j; ++i) {
     S hi = H[(size_t)i * ldh + j], hi1 = H[(size_t)(i + 1) * ldh + j];
     S t = add(mul(cs[i], hi), mul(sn[i], hi1));
@@ -197,98 +301,153 @@ __global__ void givens_kernel(S* __restrict__ H, int ldh, int j, S* __restrict__
   est[0] = cabs_(g[j + 1]) / beta;
 }
 
-// --- y = R^{-1} g with R = H[:j+1, :j+1] upper triangular (gmres.py:98-103) -----
-template <typename S>
-__global__ void backsolve_kernel(const S* __restrict__ H, int ldh, int j, const S* __restrict__ g, S* __restrict__ y) {
-  extern __shared__ __align__(16) unsigned char sraw[];
-  S* rhs = reinterpret_cast<S*>(sraw);
-  __shared__ S yi_s;
-  for (int i = threadIdx.x; i <= j; i += blockDim.x) rhs[i] = g[i];
-  __syncthreads();
-  for (int i = j; i >= 0; --i) {
-    if (threadIdx.x == 0) {
-      const S d = H[(size_t)i * ldh + i];
-      // singular R: the reference falls back to lstsq; a zero component is used here
-      yi_s = abs2(d) == 0.0 ? Sc<S>::zero() : div_(rhs[i], d);
-      y[i] = yi_s;
-    }
-    __syncthreads();
-    const S yi = yi_s;
-    for (int k = threadIdx.x; k < i; k += blockDim.x) rhs[k] = fms_(H[(size_t)k * ldh + i], yi, rhs[k]);
-    __syncthreads();
-  }
-}
-
-// ----------------------------------------------------------------------------
-// host launchers
-// scratch layout: [partial KG-rounded max_vec x KNB S][h1 max_vec S][h2 max_vec S][npart KNB][n2 4]
-// ----------------------------------------------------------------------------
-size_t krylov_scratch_bytes(int max_vec) {
-  const size_t nv = (size_t)((max_vec + KG - 1) / KG) * KG;
-  return nv * KNB * sizeof(double2) + 2 * nv * sizeof(double2) + KNB * sizeof(double) + 8 * sizeof(double);
-}
-struct KScratch {
-  void* partial;
-  void* h1;
-  void* h2;
-  double* npart;
-  double* n2;
+struct GivensArgs {
+  void* H;
+  int ldh;
+  void* cs;
+  void* sn;
+  void* g;
+  double beta;
+  double* est;
 };
-static KScratch carve(void* scratch, int max_vec) {
-  const size_t nv = (size_t)((max_vec + KG - 1) / KG) * KG;
-  char* p = (char*)scratch;
-  KScratch k;
-  k.partial = p;
-  p += nv * KNB * sizeof(double2);
-  k.h1 = p;
-  p += nv * sizeof(double2);
-  k.h2 = p;
-  p += nv * sizeof(double2);
-  k.npart = (double*)p;
-  p += KNB * sizeof(double);
-  k.n2 = (double*)p;
-  return k;
+
+template <typename S>
+__global__ void __launch_bounds__(KB) cgs_update_dots_kernel(const S* __restrict__ V, int nvec, size_t ldv,
+                                                             S* __restrict__ w, size_t N, const S* __restrict__ h1,
+                                                             S* __restrict__ partial, double* __restrict__ npart,
+                                                             S* __restrict__ h2, unsigned* __restrict__ count,
+                                                             S* __restrict__ hcol, size_t hstride,
+                                                             double* __restrict__ inv, GivensArgs gv) {
+  extern __shared__ __align__(16) unsigned char sraw[];
+  S* sacc = reinterpret_cast<S*>(sraw);
+  S* hs = sacc + nvec;
+  __shared__ S red[KB / 32][CG];
+  __shared__ double nred[KB / 32];
+  for (int i = threadIdx.x; i < nvec; i += KB) {
+    sacc[i] = Sc<S>::zero();
+    hs[i] = h1[i];
+  }
+  __syncthreads();
+  double nrm;
+  block_dots<S, true>(V, nvec, ldv, w, N, hs, sacc, red, &nrm);
+  for (int i = threadIdx.x; i < nvec; i += KB) partial[(size_t)i * gridDim.x + blockIdx.x] = sacc[i];
+  nrm = warp_sum(nrm);
+  if ((threadIdx.x & 31) == 0) nred[threadIdx.x >> 5] = nrm;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int q = 0; q < KB / 32; ++q) s += nred[q];
+    npart[blockIdx.x] = s;
+  }
+  if (!last_block(count)) return;
+  // ---- last block: h2, ||w''||, the Hessenberg column, breakdown, Givens ----
+  sum_partials(partial, nvec, h2);
+  __shared__ double wn2;
+  if (threadIdx.x < 32) {
+    double s = 0.0;
+    for (int b = threadIdx.x; b < (int)gridDim.x; b += 32) s += npart[b];
+    s = warp_sum(s);
+    if (threadIdx.x == 0) wn2 = s;
+  }
+  __syncthreads();
+  __shared__ double mx[KB / 32], h2n[KB / 32];
+  double m = 0.0, q2 = 0.0;
+  const int j = nvec - 1;
+  for (int i = threadIdx.x; i <= j; i += KB) {
+    const S b2 = h2[i];
+    const S v = add(h1[i], b2);
+    hcol[(size_t)i * hstride] = v;
+    m = fmax(m, sqrt(abs2(v)));
+    q2 += abs2(b2);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    q2 += __shfl_xor_sync(0xffffffffu, q2, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    mx[threadIdx.x >> 5] = m;
+    h2n[threadIdx.x >> 5] = q2;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double q = 0.0;
+    for (int k = 0; k < KB / 32; ++k) {
+      m = fmax(m, mx[k]);
+      q += h2n[k];
+    }
+    const double hn = sqrt(fmax(wn2 - q, 0.0));
+    hcol[(size_t)(j + 1) * hstride] = Sc<S>::from_real(hn);
+    // breakdown test of gmres.py:125 on max |H[:j+2, j]|
+    const bool brk = hn <= 1e-14 * fmax(fmax(m, hn), 1.0);
+    inv[0] = brk ? 0.0 : 1.0 / hn;
+    inv[1] = brk ? 1.0 : 0.0;
+    if (gv.H) givens_apply<S>((S*)gv.H, gv.ldh, j, (S*)gv.cs, (S*)gv.sn, (S*)gv.g, gv.beta, gv.est);
+  }
+}
+
+// w <- (w - V h2) * inv[0]   (inv[0] = 0 on breakdown: w - V h2 is left unscaled)
+template <typename S>
+__global__ void __launch_bounds__(KB) cgs_final_kernel(const S* __restrict__ V, int nvec, size_t ldv,
+                                                       S* __restrict__ w, size_t N, const S* __restrict__ h2,
+                                                       const double* __restrict__ inv) {
+  extern __shared__ __align__(16) unsigned char sraw[];
+  S* hs = reinterpret_cast<S*>(sraw);
+  for (int i = threadIdx.x; i < nvec; i += KB) hs[i] = h2[i];
+  __syncthreads();
+  const double f0 = inv[0];
+  const double f = f0 == 0.0 ? 1.0 : f0;
+  for (size_t n = blockIdx.x * (size_t)KB + threadIdx.x; n < N; n += (size_t)gridDim.x * KB) {
+    S x = w[n];
+    int i = 0;
+    for (; i + 4 <= nvec; i += 4) {
+      const S v0 = V[(size_t)i * ldv + n], v1 = V[(size_t)(i + 1) * ldv + n];
+      const S v2 = V[(size_t)(i + 2) * ldv + n], v3 = V[(size_t)(i + 3) * ldv + n];
+      x = fms_(hs[i], v0, x);
+      x = fms_(hs[i + 1], v1, x);
+      x = fms_(hs[i + 2], v2, x);
+      x = fms_(hs[i + 3], v3, x);
+    }
+    for (; i < nvec; ++i) x = fms_(hs[i], V[(size_t)i * ldv + n], x);
+    w[n] = scale(x, f);
+  }
+}
+
+template <typename S> static void set_smem(const void* fn, size_t bytes) {
+  HELM_CHECK(bytes <= 200 * 1024, "Krylov basis too large for the CGS2 kernels");
+  if (bytes > 48 * 1024) HELM_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
 }
 
 template <typename S>
-void krylov_dots(const S* V, int nvec, size_t ldv, const S* w, size_t N, S* out, void* scratch, cudaStream_t st) {
-  KScratch k = carve(scratch, nvec);
-  dots_kernel<S><<<KNB, KB, 0, st>>>(V, nvec, ldv, w, N, (S*)k.partial);
+static void cgs2_run(S* V, int j, size_t ldv, size_t N, S* hcol, size_t hstride, double* inv_out, void* scratch,
+                     GivensArgs gv, cudaStream_t st) {
+  const int nvec = j + 1;
+  CgsScratch k = carve(scratch, nvec);
+  S* w = V + (size_t)(j + 1) * ldv;
+  const size_t sm1 = (size_t)nvec * sizeof(S), sm2 = 2 * sm1;
+  set_smem<S>((const void*)cgs_dots_kernel<S>, sm1);
+  set_smem<S>((const void*)cgs_update_dots_kernel<S>, sm2);
+  set_smem<S>((const void*)cgs_final_kernel<S>, sm1);
+  cgs_dots_kernel<S><<<KNB, KB, sm1, st>>>(V, nvec, ldv, w, N, (S*)k.partial, (S*)k.h1, k.count);
   HELM_LAUNCH_CHECK();
-  reduce_rows_kernel<S><<<(nvec + 7) / 8, 256, 0, st>>>((S*)k.partial, nvec, KNB, out);
+  cgs_update_dots_kernel<S><<<KNB, KB, sm2, st>>>(V, nvec, ldv, w, N, (const S*)k.h1, (S*)k.partial, k.npart,
+                                                  (S*)k.h2, k.count + 1, hcol, hstride, inv_out, gv);
   HELM_LAUNCH_CHECK();
-}
-
-template <typename S>
-void krylov_update(S* w, const S* V, int nvec, size_t ldv, const S* h, double sign, size_t N, double* norm2_out,
-                   void* scratch, cudaStream_t st) {
-  KScratch k = carve(scratch, nvec);
-  const size_t smem = (size_t)nvec * sizeof(S);
-  static bool attr[2] = {false, false};
-  if (!attr[Sc<S>::cplx]) {
-    HELM_CUDA(cudaFuncSetAttribute(update_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    attr[Sc<S>::cplx] = true;
-  }
-  HELM_CHECK(smem <= 200 * 1024, "Krylov basis too large for the update kernel");
-  update_kernel<S><<<KNB, KB, smem, st>>>(w, V, nvec, ldv, h, sign, N, /*from_zero=*/0,
-                                          norm2_out ? k.npart : nullptr);
+  cgs_final_kernel<S><<<KNB, KB, sm1, st>>>(V, nvec, ldv, w, N, (const S*)k.h2, inv_out);
   HELM_LAUNCH_CHECK();
-  if (norm2_out) {
-    sum_partials_kernel<<<1, 32, 0, st>>>(k.npart, KNB, norm2_out);
-    HELM_LAUNCH_CHECK();
-  }
 }
 
 // x = sum_i h_i V_i (fresh output)
 template <typename S>
 void krylov_combine(S* x, const S* V, int nvec, size_t ldv, const S* h, size_t N, cudaStream_t st) {
   const size_t smem = (size_t)nvec * sizeof(S);
+  set_smem<S>((const void*)update_kernel<S>, smem);
   update_kernel<S><<<KNB, KB, smem, st>>>(x, V, nvec, ldv, h, 1.0, N, 1, nullptr);
   HELM_LAUNCH_CHECK();
 }
 
 template <typename S> void krylov_norm2(const S* x, size_t N, double* out, void* scratch, cudaStream_t st) {
-  KScratch k = carve(scratch, 1);
+  CgsScratch k = carve(scratch, 1);
   norm2_kernel<S><<<KNB, KB, 0, st>>>(x, N, k.npart);
   HELM_LAUNCH_CHECK();
   sum_partials_kernel<<<1, 32, 0, st>>>(k.npart, KNB, out);
@@ -296,26 +455,24 @@ template <typename S> void krylov_norm2(const S* x, size_t N, double* out, void*
 }
 
 // Arnoldi step j: V[j+1] holds w on entry; hcol points at H[0][j] with stride hstride.
-// inv_out[0] = 1/||w|| (0 on breakdown), inv_out[1] = breakdown flag.
+// inv_out[0] = 1/||w|| (0 on breakdown), inv_out[1] = breakdown flag.  With H != null the
+// Givens update of column j runs in the same launch (est_out[0] = |g[j+1]| / beta).
 template <typename S>
 void krylov_cgs2_impl(S* V, int j, size_t ldv, size_t N, S* hcol, size_t hstride, double* inv_out, void* scratch,
-                      cudaStream_t st) {
-  KScratch k = carve(scratch, j + 1);
-  S* w = V + (size_t)(j + 1) * ldv;
-  krylov_dots<S>(V, j + 1, ldv, w, N, (S*)k.h1, scratch, st);
-  krylov_update<S>(w, V, j + 1, ldv, (const S*)k.h1, -1.0, N, nullptr, scratch, st);
-  krylov_dots<S>(V, j + 1, ldv, w, N, (S*)k.h2, scratch, st);
-  krylov_update<S>(w, V, j + 1, ldv, (const S*)k.h2, -1.0, N, k.n2, scratch, st);
-  cgs2_finalize_kernel<S><<<1, 256, 0, st>>>((const S*)k.h1, (const S*)k.h2, k.n2, j, hcol, hstride, inv_out);
-  HELM_LAUNCH_CHECK();
-  scale_kernel<S><<<KNB, KB, 0, st>>>(w, w, inv_out, 0, N);
-  HELM_LAUNCH_CHECK();
+                      cudaStream_t st, S* H, int ldh, S* cs, S* sn, S* g, double beta, double* est_out) {
+  GivensArgs gv{H, ldh, cs, sn, g, beta, est_out};
+  cgs2_run<S>(V, j, ldv, N, hcol, hstride, inv_out, scratch, gv, st);
 }
 
 template <typename S>
 void krylov_cgs2(S* V, int j, size_t ldv, size_t N, S* hcol, void* scratch, cudaStream_t st) {
-  KScratch k = carve(scratch, j + 1);
-  krylov_cgs2_impl<S>(V, j, ldv, N, hcol, 1, k.n2 + 2, scratch, st);
+  CgsScratch k = carve(scratch, j + 1);
+  cgs2_run<S>(V, j, ldv, N, hcol, 1, k.scal + 2, scratch, GivensArgs{}, st);
+}
+
+template <typename S>
+__global__ void givens_kernel(S* H, int ldh, int j, S* cs, S* sn, S* g, double beta, double* est) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) givens_apply<S>(H, ldh, j, cs, sn, g, beta, est);
 }
 
 template <typename S>
@@ -341,12 +498,10 @@ template <typename S> void krylov_scale(S* x, const S* src, const double* s, int
 }
 
 #define HELM_INST(S)                                                                                          \
-  template void krylov_dots<S>(const S*, int, size_t, const S*, size_t, S*, void*, cudaStream_t);             \
-  template void krylov_update<S>(S*, const S*, int, size_t, const S*, double, size_t, double*, void*,         \
-                                 cudaStream_t);                                                               \
   template void krylov_combine<S>(S*, const S*, int, size_t, const S*, size_t, cudaStream_t);                 \
   template void krylov_norm2<S>(const S*, size_t, double*, void*, cudaStream_t);                              \
-  template void krylov_cgs2_impl<S>(S*, int, size_t, size_t, S*, size_t, double*, void*, cudaStream_t);       \
+  template void krylov_cgs2_impl<S>(S*, int, size_t, size_t, S*, size_t, double*, void*, cudaStream_t, S*, int, \
+                                    S*, S*, S*, double, double*);                                              \
   template void krylov_cgs2<S>(S*, int, size_t, size_t, S*, void*, cudaStream_t);                             \
   template void krylov_givens<S>(S*, int, int, S*, S*, S*, double, double*, cudaStream_t);                    \
   template void krylov_backsolve<S>(const S*, int, int, const S*, S*, cudaStream_t);                          \

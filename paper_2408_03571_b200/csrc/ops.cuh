@@ -34,17 +34,13 @@ template <typename S>
 void op_apply_M(const helm_plan* P, helm_workspace* ws, const S* x, S* y, int batch, cudaStream_t st);
 
 // Krylov kernels (krylov.cu)
-template <typename S>
-void krylov_dots(const S* V, int nvec, size_t ldv, const S* w, size_t N, S* out, void* scratch, cudaStream_t st);
-template <typename S>
-void krylov_update(S* w, const S* V, int nvec, size_t ldv, const S* h, double sign, size_t N, double* norm2_out,
-                   void* scratch, cudaStream_t st);
 template <typename S> void krylov_norm2(const S* x, size_t N, double* out, void* scratch, cudaStream_t st);
 template <typename S>
 void krylov_combine(S* x, const S* V, int nvec, size_t ldv, const S* h, size_t N, cudaStream_t st);
 template <typename S>
 void krylov_cgs2_impl(S* V, int j, size_t ldv, size_t N, S* hcol, size_t hstride, double* inv_out, void* scratch,
-                      cudaStream_t st);
+                      cudaStream_t st, S* H = nullptr, int ldh = 0, S* cs = nullptr, S* sn = nullptr,
+                      S* g = nullptr, double beta = 1.0, double* est_out = nullptr);
 template <typename S>
 void krylov_cgs2(S* V, int j, size_t ldv, size_t N, S* hcol, void* scratch, cudaStream_t st);
 template <typename S>
@@ -53,5 +49,10 @@ template <typename S> void krylov_backsolve(const S* H, int ldh, int j, const S*
 template <typename S> void krylov_scale(S* x, const S* src, const double* s, int invert, size_t N, cudaStream_t st);
 
 size_t krylov_scratch_bytes(int max_vec);
+
+// Krylov basis storage (basis.cu): returns the base of a contiguous device range with
+// at least `need` bytes backed; the base moves only when `need` exceeds the reservation.
+void* basis_ensure(helm_workspace* ws, size_t need, size_t reserve_hint, size_t chunk_min, cudaStream_t st);
+void basis_free(helm_workspace* ws);
 
 }  // namespace helm
