@@ -9,12 +9,15 @@
 // CGS2 equals MGS + re-orthogonalisation; numerically both keep the basis
 // orthogonal to working precision, which is what fixes the iteration count.
 // H, the rotations and g stay on the device; the host reads one estimate.
+#include <algorithm>
+
 #include "ops.cuh"
 
 namespace helm {
 
 constexpr int KB = 256;        // threads per block
-constexpr int KNB = 4 * 148;   // reduction blocks (4 per SM)
+constexpr int KNB = 4 * 148;   // blocks of the streaming Krylov kernels (4 per SM)
+constexpr int PB = 8 * 148;    // capacity of the per-block partial-sum arrays
 
 // w <- w + sign * sum_i h_i V_i ; optionally norm2 partial of the result per block
 template <typename S>
@@ -145,18 +148,18 @@ template <typename S> __device__ __forceinline__ S reduce8(const S (&v)[CG], int
 }
 
 // scratch layout (fixed offsets first: the counters must stay put and start at zero)
-//   [count 2 x u32 | pad][scal 8 doubles][npart KNB doubles][h1 nv S][h2 nv S][partial nv x KNB S]
+//   [count 2 x u32 | pad][scal 8 doubles][npart PB doubles][h1 nv S][h2 nv S][partial nv x PB S]
 struct CgsScratch {
   unsigned* count; // [2]
   double* scal;    // [8]
-  double* npart;   // [KNB]
+  double* npart;   // [PB]
   void* h1;        // [nvec] S
   void* h2;        // [nvec] S
-  void* partial;   // [nvec][KNB] S
+  void* partial;   // [nvec][<= PB] S
 };
 size_t krylov_scratch_bytes(int max_vec) {
   const size_t nv = (size_t)((max_vec + CG - 1) / CG) * CG;
-  return 64 + 8 * sizeof(double) + KNB * sizeof(double) + 2 * nv * sizeof(double2) + nv * KNB * sizeof(double2);
+  return 64 + 8 * sizeof(double) + PB * sizeof(double) + 2 * nv * sizeof(double2) + nv * PB * sizeof(double2);
 }
 static CgsScratch carve(void* scratch, int max_vec) {
   const size_t nv = (size_t)((max_vec + CG - 1) / CG) * CG;
@@ -167,7 +170,7 @@ static CgsScratch carve(void* scratch, int max_vec) {
   k.scal = (double*)p;
   p += 8 * sizeof(double);
   k.npart = (double*)p;
-  p += KNB * sizeof(double);
+  p += PB * sizeof(double);
   k.h1 = p;
   p += nv * sizeof(double2);
   k.h2 = p;
@@ -176,52 +179,42 @@ static CgsScratch carve(void* scratch, int max_vec) {
   return k;
 }
 
-// Block-level accumulation of sum_n conj(V_i[n]) x[n] for i in [0, nvec): per chunk of
-// KB elements (one per thread) and group of CG vectors, each warp reduces its 8 sums
-// (reduce8) and warp totals are added to sacc in warp order.
-template <typename S, bool UPDATE>
-__device__ __forceinline__ void block_dots(const S* __restrict__ V, int nvec, size_t ldv, S* __restrict__ w, size_t N,
-                                           const S* hs, S* sacc, S (*red)[CG], double* nrm_out) {
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  double nrm = 0.0;
-  for (size_t base = (size_t)blockIdx.x * KB; base < N; base += (size_t)gridDim.x * KB) {
-    const size_t n = base + threadIdx.x;
-    const bool ok = n < N;
-    S x = ok ? w[n] : Sc<S>::zero();
-    if (UPDATE) {  // x <- x - V h1 (read V from HBM), store, then the dots re-read V (L2)
-      if (ok) {
-        int i = 0;
-        for (; i + 4 <= nvec; i += 4) {
-          const S v0 = V[(size_t)i * ldv + n], v1 = V[(size_t)(i + 1) * ldv + n];
-          const S v2 = V[(size_t)(i + 2) * ldv + n], v3 = V[(size_t)(i + 3) * ldv + n];
-          x = fms_(hs[i], v0, x);
-          x = fms_(hs[i + 1], v1, x);
-          x = fms_(hs[i + 2], v2, x);
-          x = fms_(hs[i + 3], v3, x);
-        }
-        for (; i < nvec; ++i) x = fms_(hs[i], V[(size_t)i * ldv + n], x);
-        w[n] = x;
-        nrm += abs2(x);
-      }
-    }
-    for (int i0 = 0; i0 < nvec; i0 += CG) {
-      S acc[CG];
+// Per-warp accumulation of sum_n conj(V_i[n]) x[n]: a warp owns chunks of 32*E
+// elements; per group of CG vectors each lane forms CG partial sums, reduce8 leaves the
+// warp totals on lanes 0, 4, .., 28, which add them to the warp's own accumulator row
+// wacc[i] (shared memory, no block barrier inside the sweep).  Rows are summed in warp
+// order at the end: the result does not depend on scheduling.
+template <typename S, int E>
+__device__ __forceinline__ void warp_dots_acc(const S (&v)[E][CG], const S (&x)[E], int i0, int nvec, int lane,
+                                              S* wacc) {
+  S acc[CG];
 #pragma unroll
-      for (int g = 0; g < CG; ++g)
-        acc[g] = (ok && i0 + g < nvec) ? cmul(V[(size_t)(i0 + g) * ldv + n], x) : Sc<S>::zero();
-      const S s = reduce8(acc, lane);
-      if ((lane & 3) == 0) red[wid][lane >> 2] = s;
-      __syncthreads();
-      if (threadIdx.x < CG && i0 + threadIdx.x < nvec) {
-        S t = sacc[i0 + threadIdx.x];
+  for (int g = 0; g < CG; ++g) {
+    acc[g] = Sc<S>::zero();
 #pragma unroll
-        for (int q = 0; q < KB / 32; ++q) t = add(t, red[q][threadIdx.x]);
-        sacc[i0 + threadIdx.x] = t;
-      }
-      __syncthreads();
-    }
+    for (int e = 0; e < E; ++e) acc[g] = add(acc[g], cmul(v[e][g], x[e]));
   }
-  if (UPDATE) *nrm_out = nrm;
+  const S s = reduce8(acc, lane);
+  const int i = i0 + (lane >> 2);
+  if ((lane & 3) == 0 && i < nvec) wacc[i] = add(wacc[i], s);
+}
+
+template <typename S> __device__ __forceinline__ void cp_async_s(S* smem, const S* g, bool ok) {
+  if constexpr (sizeof(S) == 16)
+    cp_async16(smem, g, ok);
+  else
+    cp_async8(smem, g, ok);
+}
+
+// sum the warps' accumulator rows (fixed order) into partial[i][block]
+template <typename S>
+__device__ __forceinline__ void flush_warp_rows(const S* wacc, int nvec, int nwarps, S* __restrict__ partial) {
+  __syncthreads();
+  for (int i = threadIdx.x; i < nvec; i += blockDim.x) {
+    S t = Sc<S>::zero();
+    for (int q = 0; q < nwarps; ++q) t = add(t, wacc[(size_t)q * nvec + i]);
+    partial[(size_t)i * gridDim.x + blockIdx.x] = t;
+  }
 }
 
 // last block to arrive? (threadfence + counter; the counter is reset for the next use)
@@ -242,7 +235,7 @@ template <typename S>
 __device__ __forceinline__ void sum_partials(const S* __restrict__ partial, int nvec, S* out) {
   // one warp per vector, fixed order
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  for (int i = wid; i < nvec; i += KB / 32) {
+  for (int i = wid; i < nvec; i += blockDim.x / 32) {
     S s = Sc<S>::zero();
     for (int b = lane; b < (int)gridDim.x; b += 32) s = add(s, partial[(size_t)i * gridDim.x + b]);
     s = warp_sum(s);
@@ -250,17 +243,41 @@ __device__ __forceinline__ void sum_partials(const S* __restrict__ partial, int 
   }
 }
 
+constexpr int DE = 2;  // elements per lane per chunk in the dots sweep
+
+// K1: h = V^H w.  Block = KB threads; dynamic smem = (KB/32) * nvec accumulator rows.
 template <typename S>
 __global__ void __launch_bounds__(KB) cgs_dots_kernel(const S* __restrict__ V, int nvec, size_t ldv,
                                                       const S* __restrict__ w, size_t N, S* __restrict__ partial,
                                                       S* __restrict__ h, unsigned* __restrict__ count) {
   extern __shared__ __align__(16) unsigned char sraw[];
-  S* sacc = reinterpret_cast<S*>(sraw);
-  __shared__ S red[KB / 32][CG];
-  for (int i = threadIdx.x; i < nvec; i += KB) sacc[i] = Sc<S>::zero();
+  S* wacc_all = reinterpret_cast<S*>(sraw);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  constexpr int NW = KB / 32;
+  for (int i = threadIdx.x; i < NW * nvec; i += KB) wacc_all[i] = Sc<S>::zero();
   __syncthreads();
-  block_dots<S, false>(V, nvec, ldv, const_cast<S*>(w), N, nullptr, sacc, red, nullptr);
-  for (int i = threadIdx.x; i < nvec; i += KB) partial[(size_t)i * gridDim.x + blockIdx.x] = sacc[i];
+  S* wacc = wacc_all + (size_t)wid * nvec;
+  const size_t chunk = 32 * DE;
+  for (size_t base = ((size_t)blockIdx.x * NW + wid) * chunk; base < N; base += (size_t)gridDim.x * NW * chunk) {
+    S x[DE];
+#pragma unroll
+    for (int e = 0; e < DE; ++e) {
+      const size_t n = base + e * 32 + lane;
+      x[e] = n < N ? w[n] : Sc<S>::zero();
+    }
+    for (int i0 = 0; i0 < nvec; i0 += CG) {
+      S v[DE][CG];
+#pragma unroll
+      for (int e = 0; e < DE; ++e) {
+        const size_t n = base + e * 32 + lane;
+#pragma unroll
+        for (int g = 0; g < CG; ++g)
+          v[e][g] = (n < N && i0 + g < nvec) ? V[(size_t)(i0 + g) * ldv + n] : Sc<S>::zero();
+      }
+      warp_dots_acc<S, DE>(v, x, i0, nvec, lane, wacc);
+    }
+  }
+  flush_warp_rows(wacc_all, nvec, NW, partial);
   if (last_block(count)) sum_partials(partial, nvec, h);
 }
 
@@ -311,32 +328,94 @@ struct GivensArgs {
   double* est;
 };
 
-template <typename S>
-__global__ void __launch_bounds__(KB) cgs_update_dots_kernel(const S* __restrict__ V, int nvec, size_t ldv,
+constexpr int UW = 2;  // warps per block in the update+dots sweep
+
+// K2: w' = w - V h1 (stored), dots V^H w', ||w'||^2.  A warp owns 32-element chunks.
+// STAGED: the chunk's nvec basis rows are copied to the warp's shared-memory stage with
+// cp.async (all in flight at once), so the update and the dots read V from HBM once.
+// Otherwise the dots re-read V through L2.  Dynamic smem: UW * nvec accumulator rows,
+// the h1 copy, and (STAGED) UW * nvec * 32 staged elements.
+template <typename S, bool STAGED, int E>
+__global__ void __launch_bounds__(UW * 32) cgs_update_dots_kernel(const S* __restrict__ V, int nvec, size_t ldv,
                                                              S* __restrict__ w, size_t N, const S* __restrict__ h1,
                                                              S* __restrict__ partial, double* __restrict__ npart,
                                                              S* __restrict__ h2, unsigned* __restrict__ count,
                                                              S* __restrict__ hcol, size_t hstride,
                                                              double* __restrict__ inv, GivensArgs gv) {
   extern __shared__ __align__(16) unsigned char sraw[];
-  S* sacc = reinterpret_cast<S*>(sraw);
-  S* hs = sacc + nvec;
-  __shared__ S red[KB / 32][CG];
-  __shared__ double nred[KB / 32];
-  for (int i = threadIdx.x; i < nvec; i += KB) {
-    sacc[i] = Sc<S>::zero();
-    hs[i] = h1[i];
-  }
+  S* wacc_all = reinterpret_cast<S*>(sraw);
+  S* hs = wacc_all + (size_t)UW * nvec;
+  S* stage_all = hs + nvec;
+  __shared__ double nred[UW];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < UW * nvec; i += UW * 32) wacc_all[i] = Sc<S>::zero();
+  for (int i = threadIdx.x; i < nvec; i += UW * 32) hs[i] = h1[i];
   __syncthreads();
-  double nrm;
-  block_dots<S, true>(V, nvec, ldv, w, N, hs, sacc, red, &nrm);
-  for (int i = threadIdx.x; i < nvec; i += KB) partial[(size_t)i * gridDim.x + blockIdx.x] = sacc[i];
+  S* wacc = wacc_all + (size_t)wid * nvec;
+  S* stage = stage_all + (size_t)wid * nvec * 32 * E;  // [nvec][E][32]
+  double nrm = 0.0;
+  constexpr int CH = 32 * E;
+  for (size_t base = ((size_t)blockIdx.x * UW + wid) * CH; base < N; base += (size_t)gridDim.x * UW * CH) {
+    if (STAGED) {
+      for (int i = 0; i < nvec; ++i)
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const size_t n = base + e * 32 + lane;
+          cp_async_s(stage + (i * E + e) * 32 + lane, V + (size_t)i * ldv + (n < N ? n : 0), n < N);
+        }
+      cp_commit();
+    }
+    S x[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const size_t n = base + e * 32 + lane;
+      x[e] = n < N ? w[n] : Sc<S>::zero();
+    }
+    if (STAGED) {
+      cp_wait<0>();
+      __syncwarp();
+    }
+    auto vat = [&](int i, int e) {
+      const size_t n = base + e * 32 + lane;
+      return STAGED ? stage[(i * E + e) * 32 + lane] : (n < N ? V[(size_t)i * ldv + n] : Sc<S>::zero());
+    };
+    // x -= V h1 with two interleaved chains per element (latency), combined in a fixed order
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      S xa = x[e], xb = Sc<S>::zero();
+      int i = 0;
+      for (; i + 4 <= nvec; i += 4) {
+        const S v0 = vat(i, e), v1 = vat(i + 1, e), v2 = vat(i + 2, e), v3 = vat(i + 3, e);
+        xa = fms_(hs[i], v0, xa);
+        xb = fms_(hs[i + 1], v1, xb);
+        xa = fms_(hs[i + 2], v2, xa);
+        xb = fms_(hs[i + 3], v3, xb);
+      }
+      for (; i < nvec; ++i) xa = fms_(hs[i], vat(i, e), xa);
+      x[e] = add(xa, xb);
+      const size_t n = base + e * 32 + lane;
+      if (n < N) {
+        w[n] = x[e];
+        nrm += abs2(x[e]);
+      }
+    }
+    for (int i0 = 0; i0 < nvec; i0 += CG) {
+      S v[E][CG];
+#pragma unroll
+      for (int e = 0; e < E; ++e)
+#pragma unroll
+        for (int g = 0; g < CG; ++g) v[e][g] = i0 + g < nvec ? vat(i0 + g, e) : Sc<S>::zero();
+      warp_dots_acc<S, E>(v, x, i0, nvec, lane, wacc);
+    }
+    if (STAGED) __syncwarp();  // the stage is refilled by the next chunk
+  }
+  flush_warp_rows(wacc_all, nvec, UW, partial);
   nrm = warp_sum(nrm);
-  if ((threadIdx.x & 31) == 0) nred[threadIdx.x >> 5] = nrm;
+  if (lane == 0) nred[wid] = nrm;
   __syncthreads();
   if (threadIdx.x == 0) {
     double s = 0.0;
-    for (int q = 0; q < KB / 32; ++q) s += nred[q];
+    for (int q = 0; q < UW; ++q) s += nred[q];
     npart[blockIdx.x] = s;
   }
   if (!last_block(count)) return;
@@ -350,10 +429,10 @@ __global__ void __launch_bounds__(KB) cgs_update_dots_kernel(const S* __restrict
     if (threadIdx.x == 0) wn2 = s;
   }
   __syncthreads();
-  __shared__ double mx[KB / 32], h2n[KB / 32];
+  __shared__ double mx[UW], h2n[UW];
   double m = 0.0, q2 = 0.0;
   const int j = nvec - 1;
-  for (int i = threadIdx.x; i <= j; i += KB) {
+  for (int i = threadIdx.x; i <= j; i += UW * 32) {
     const S b2 = h2[i];
     const S v = add(h1[i], b2);
     hcol[(size_t)i * hstride] = v;
@@ -372,7 +451,7 @@ __global__ void __launch_bounds__(KB) cgs_update_dots_kernel(const S* __restrict
   __syncthreads();
   if (threadIdx.x == 0) {
     double q = 0.0;
-    for (int k = 0; k < KB / 32; ++k) {
+    for (int k = 0; k < UW; ++k) {
       m = fmax(m, mx[k]);
       q += h2n[k];
     }
@@ -398,24 +477,26 @@ __global__ void __launch_bounds__(KB) cgs_final_kernel(const S* __restrict__ V, 
   const double f0 = inv[0];
   const double f = f0 == 0.0 ? 1.0 : f0;
   for (size_t n = blockIdx.x * (size_t)KB + threadIdx.x; n < N; n += (size_t)gridDim.x * KB) {
-    S x = w[n];
+    S xa = w[n], xb = Sc<S>::zero();
     int i = 0;
     for (; i + 4 <= nvec; i += 4) {
       const S v0 = V[(size_t)i * ldv + n], v1 = V[(size_t)(i + 1) * ldv + n];
       const S v2 = V[(size_t)(i + 2) * ldv + n], v3 = V[(size_t)(i + 3) * ldv + n];
-      x = fms_(hs[i], v0, x);
-      x = fms_(hs[i + 1], v1, x);
-      x = fms_(hs[i + 2], v2, x);
-      x = fms_(hs[i + 3], v3, x);
+      xa = fms_(hs[i], v0, xa);
+      xb = fms_(hs[i + 1], v1, xb);
+      xa = fms_(hs[i + 2], v2, xa);
+      xb = fms_(hs[i + 3], v3, xb);
     }
-    for (; i < nvec; ++i) x = fms_(hs[i], V[(size_t)i * ldv + n], x);
-    w[n] = scale(x, f);
+    for (; i < nvec; ++i) xa = fms_(hs[i], V[(size_t)i * ldv + n], xa);
+    w[n] = scale(add(xa, xb), f);
   }
 }
 
-template <typename S> static void set_smem(const void* fn, size_t bytes) {
-  HELM_CHECK(bytes <= 200 * 1024, "Krylov basis too large for the CGS2 kernels");
-  if (bytes > 48 * 1024) HELM_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+constexpr size_t SMEM_MAX = 227 * 1024;
+
+static void set_smem(const void* fn, size_t bytes) {
+  HELM_CHECK(bytes <= SMEM_MAX, "Krylov basis too large for the CGS2 kernels");
+  if (bytes > 48 * 1024) HELM_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
 }
 
 template <typename S>
@@ -424,16 +505,36 @@ static void cgs2_run(S* V, int j, size_t ldv, size_t N, S* hcol, size_t hstride,
   const int nvec = j + 1;
   CgsScratch k = carve(scratch, nvec);
   S* w = V + (size_t)(j + 1) * ldv;
-  const size_t sm1 = (size_t)nvec * sizeof(S), sm2 = 2 * sm1;
-  set_smem<S>((const void*)cgs_dots_kernel<S>, sm1);
-  set_smem<S>((const void*)cgs_update_dots_kernel<S>, sm2);
-  set_smem<S>((const void*)cgs_final_kernel<S>, sm1);
+  const size_t es = sizeof(S);
+  // K1
+  const size_t sm1 = (size_t)(KB / 32) * nvec * es;
+  set_smem((const void*)cgs_dots_kernel<S>, sm1);
   cgs_dots_kernel<S><<<KNB, KB, sm1, st>>>(V, nvec, ldv, w, N, (S*)k.partial, (S*)k.h1, k.count);
   HELM_LAUNCH_CHECK();
-  cgs_update_dots_kernel<S><<<KNB, KB, sm2, st>>>(V, nvec, ldv, w, N, (const S*)k.h1, (S*)k.partial, k.npart,
-                                                  (S*)k.h2, k.count + 1, hcol, hstride, inv_out, gv);
+  // K2: staged while a block's stage fits in shared memory; E elements per lane keep
+  // ~32 staged rows per lane in flight for short bases
+  const int E = nvec >= 32 ? 1 : nvec >= 16 ? 2 : nvec >= 8 ? 4 : 8;
+  const size_t sm2 = (size_t)(UW + 1) * nvec * es;
+  const size_t sm2s = sm2 + (size_t)UW * nvec * 32 * E * es;
+  auto launch2 = [&](auto kern, int grid, size_t smem) {
+    set_smem((const void*)kern, smem);
+    kern<<<grid, UW * 32, smem, st>>>(V, nvec, ldv, w, N, (const S*)k.h1, (S*)k.partial, k.npart, (S*)k.h2,
+                                      k.count + 1, hcol, hstride, inv_out, gv);
+  };
+  if (sm2s <= SMEM_MAX) {
+    const int bps = (int)std::min<size_t>(8, std::max<size_t>(1, (SMEM_MAX + 1024) / (sm2s + 1024)));
+    if (E == 8) launch2(cgs_update_dots_kernel<S, true, 8>, 148 * bps, sm2s);
+    else if (E == 4) launch2(cgs_update_dots_kernel<S, true, 4>, 148 * bps, sm2s);
+    else if (E == 2) launch2(cgs_update_dots_kernel<S, true, 2>, 148 * bps, sm2s);
+    else launch2(cgs_update_dots_kernel<S, true, 1>, 148 * bps, sm2s);
+  } else {
+    launch2(cgs_update_dots_kernel<S, false, 1>, PB, sm2);
+  }
   HELM_LAUNCH_CHECK();
-  cgs_final_kernel<S><<<KNB, KB, sm1, st>>>(V, nvec, ldv, w, N, (const S*)k.h2, inv_out);
+  // K3
+  const size_t sm3 = (size_t)nvec * es;
+  set_smem((const void*)cgs_final_kernel<S>, sm3);
+  cgs_final_kernel<S><<<KNB, KB, sm3, st>>>(V, nvec, ldv, w, N, (const S*)k.h2, inv_out);
   HELM_LAUNCH_CHECK();
 }
 
@@ -441,7 +542,7 @@ static void cgs2_run(S* V, int j, size_t ldv, size_t N, S* hcol, size_t hstride,
 template <typename S>
 void krylov_combine(S* x, const S* V, int nvec, size_t ldv, const S* h, size_t N, cudaStream_t st) {
   const size_t smem = (size_t)nvec * sizeof(S);
-  set_smem<S>((const void*)update_kernel<S>, smem);
+  set_smem((const void*)update_kernel<S>, smem);
   update_kernel<S><<<KNB, KB, smem, st>>>(x, V, nvec, ldv, h, 1.0, N, 1, nullptr);
   HELM_LAUNCH_CHECK();
 }
