@@ -67,59 +67,84 @@ __device__ __forceinline__ void fwd_step(int pv, double2 l0, double2 l1, double2
   r1 = x2;
 }
 
-__device__ __forceinline__ double2 bwd_step(const double2* __restrict__ u, double2 v, double2 (&y)[4]) {
-  v = fms_(__ldg(u + 1), y[0], v);
-  v = fms_(__ldg(u + 2), y[1], v);
-  v = fms_(__ldg(u + 3), y[2], v);
-  v = fms_(__ldg(u + 4), y[3], v);
-  v = mul(v, __ldg(u));
-  y[3] = y[2];
-  y[2] = y[1];
-  y[1] = y[0];
-  y[0] = v;
-  return v;
-}
-
 // forward pass over rows [j0, j1) with state (r0, r1); writes eliminated rows to sm (if non-null)
 template <bool STORE>
 __device__ __forceinline__ void fwd_run(const SegRhs& rhs, const int* __restrict__ piv, const double2* __restrict__ L,
                                         int m0, int a, int j0, int j1, double2& r0, double2& r1, double2* sm,
                                         int sm_stride) {
+  // chunks of C rows, the next chunk's loads in flight while the current one is consumed
   constexpr int C = 4;
-  int j = j0;
-  for (; j + C <= j1; j += C) {
+  struct Chunk {
     int pv[C];
     double2 l0[C], l1[C], f[C];
+  };
+  auto load = [&](int j, Chunk& ch) {
 #pragma unroll
     for (int c = 0; c < C; ++c) {
-      const size_t e = (size_t)(j + c) * m0 + a;
-      pv[c] = __ldg(piv + e);
-      l0[c] = __ldg(L + 2 * e);
-      l1[c] = __ldg(L + 2 * e + 1);
-      f[c] = rhs(j + c + 2);
+      const bool ok = j + c < j1;
+      const size_t e = (size_t)(ok ? j + c : j0) * m0 + a;
+      ch.pv[c] = __ldg(piv + e);
+      ch.l0[c] = __ldg(L + 2 * e);
+      ch.l1[c] = __ldg(L + 2 * e + 1);
+      ch.f[c] = ok ? rhs(j + c + 2) : mk(0.0, 0.0);
     }
+  };
+  if (j0 >= j1) return;
+  Chunk cur, nxt;
+  load(j0, cur);
+  for (int j = j0; j < j1; j += C) {
+    if (j + C < j1) load(j + C, nxt);
 #pragma unroll
     for (int c = 0; c < C; ++c) {
-      double2 o;
-      fwd_step(pv[c], l0[c], l1[c], r0, r1, f[c], o);
-      if (STORE) sm[(j + c - j0) * sm_stride] = o;
+      if (j + c < j1) {
+        double2 o;
+        fwd_step(cur.pv[c], cur.l0[c], cur.l1[c], r0, r1, cur.f[c], o);
+        if (STORE) sm[(j + c - j0) * sm_stride] = o;
+      }
     }
-  }
-  for (; j < j1; ++j) {
-    const size_t e = (size_t)j * m0 + a;
-    double2 o;
-    fwd_step(__ldg(piv + e), __ldg(L + 2 * e), __ldg(L + 2 * e + 1), r0, r1, rhs(j + 2), o);
-    if (STORE) sm[(j - j0) * sm_stride] = o;
+    cur = nxt;
   }
 }
 
 template <typename Emit>
 __device__ __forceinline__ void bwd_run(const double2* __restrict__ U, int m0, int a, int j0, int j1,
                                         double2 (&y)[4], const double2* sm, int sm_stride, Emit&& emit) {
-#pragma unroll 4
-  for (int j = j1 - 1; j >= j0; --j) {
-    const double2 v = bwd_step(U + 5 * ((size_t)j * m0 + a), sm ? sm[(j - j0) * sm_stride] : mk(0.0, 0.0), y);
-    emit(j, v);
+  constexpr int C = 4;
+  struct Chunk {
+    double2 u[C][5];
+  };
+  auto load = [&](int j, Chunk& ch) {  // rows j, j-1, .., j-C+1
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+      const int r = j - c >= j0 ? j - c : j1 - 1;
+      const double2* u = U + 5 * ((size_t)r * m0 + a);
+#pragma unroll
+      for (int e = 0; e < 5; ++e) ch.u[c][e] = __ldg(u + e);
+    }
+  };
+  if (j0 >= j1) return;
+  Chunk cur, nxt;
+  load(j1 - 1, cur);
+  for (int j = j1 - 1; j >= j0; j -= C) {
+    if (j - C >= j0) load(j - C, nxt);
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+      const int r = j - c;
+      if (r >= j0) {
+        double2 v = sm ? sm[(r - j0) * sm_stride] : mk(0.0, 0.0);
+        v = fms_(cur.u[c][1], y[0], v);
+        v = fms_(cur.u[c][2], y[1], v);
+        v = fms_(cur.u[c][3], y[2], v);
+        v = fms_(cur.u[c][4], y[3], v);
+        v = mul(v, cur.u[c][0]);
+        y[3] = y[2];
+        y[2] = y[1];
+        y[1] = y[0];
+        y[0] = v;
+        emit(r, v);
+      }
+    }
+    cur = nxt;
   }
 }
 
@@ -184,14 +209,21 @@ __global__ void __launch_bounds__(SEG_THREADS) band_seg_kernel(
   // chain: s_{k+1} = Phi_k s_k + p_k (s_1 = p_0)
   if (k == 0 && va) {
     double2 s0 = fst[1][al][0], s1 = fst[1][al][1];
+    double2 pc[4], pn[4];  // Phi_kk in use, Phi_{kk+1} in flight
+#pragma unroll
+    for (int e = 0; e < 4; ++e) pc[e] = __ldg(phi + ((size_t)1 * 4 + e) * m0 + a);
     for (int kk = 1; kk < SEG; ++kk) {
-      const double2* P = phi + (size_t)kk * 4 * m0 + a;
-      const double2 n0 = add(fst[kk + 1][al][0], add(mul(__ldg(P), s0), mul(__ldg(P + m0), s1)));
-      const double2 n1 = add(fst[kk + 1][al][1], add(mul(__ldg(P + 2 * m0), s0), mul(__ldg(P + 3 * m0), s1)));
+      const int kn = kk + 1 < SEG ? kk + 1 : kk;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) pn[e] = __ldg(phi + ((size_t)kn * 4 + e) * m0 + a);
+      const double2 n0 = add(fst[kk + 1][al][0], add(mul(pc[0], s0), mul(pc[1], s1)));
+      const double2 n1 = add(fst[kk + 1][al][1], add(mul(pc[2], s0), mul(pc[3], s1)));
       fst[kk][al][0] = s0;  // entry state of segment kk
       fst[kk][al][1] = s1;
       s0 = n0;
       s1 = n1;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) pc[e] = pn[e];
     }
   }
   __syncthreads();
@@ -217,16 +249,23 @@ __global__ void __launch_bounds__(SEG_THREADS) band_seg_kernel(
     double2 t[4];
 #pragma unroll
     for (int i = 0; i < 4; ++i) t[i] = bst[SEG - 1][al][i];  // the top segment starts from zeros
+    double2 qc[16], qn[16];  // Psi_kk in use, Psi_{kk-1} in flight
+#pragma unroll
+    for (int e = 0; e < 16; ++e) qc[e] = __ldg(psi + ((size_t)(SEG - 2) * 16 + e) * m0 + a);
     for (int kk = SEG - 2; kk >= 0; --kk) {
       double2 n[4];
-      const double2* P = psi + (size_t)kk * 16 * m0 + a;
+      const int kn = kk > 0 ? kk - 1 : 0;
+#pragma unroll
+      for (int e = 0; e < 16; ++e) qn[e] = __ldg(psi + ((size_t)kn * 16 + e) * m0 + a);
 #pragma unroll
       for (int r = 0; r < 4; ++r) {
         double2 s = bst[kk][al][r];
 #pragma unroll
-        for (int c = 0; c < 4; ++c) s = fma_(__ldg(P + (r * 4 + c) * m0), t[c], s);
+        for (int c = 0; c < 4; ++c) s = fma_(qc[r * 4 + c], t[c], s);
         n[r] = s;
       }
+#pragma unroll
+      for (int e = 0; e < 16; ++e) qc[e] = qn[e];
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         bst[kk + 1][al][i] = t[i];  // entry state of segment kk  (stored one slot up)
