@@ -10,10 +10,11 @@
 // only d), so each 1-D transform is block diagonal with two blocks of DB = 20 (padded).
 // The four products then run on the FP64 tensor pipe as mma.sync.m8n8k4.f64 (DMMA):
 // complex data is a real matrix with interleaved (re, im) columns (LEFT products) or
-// rows (RIGHT products), V stays real.  One CTA (3 warps) owns one (box, right-hand
-// side); each warp keeps 20 accumulator tiles (8 x 8) in registers, reuses one operand
-// fragment across 10 tiles per k step, and the products update the shared tile in
-// place across a barrier.  Shared strides are chosen so every fragment load is two
+// rows (RIGHT products), V stays real.  One CTA (5 warps) owns one (box, right-hand
+// side); a warp owns a slice of the independent dimension (columns for LEFT, rows for
+// RIGHT) and all row / column tiles of the folded block, so each shared-memory fragment
+// feeds three DMMAs and the products update the shared tile in place with warp-level
+// synchronisation only.  Shared strides are chosen so every fragment load is two
 // wavefronts (the minimum for 32 x 8-byte accesses).
 #include "local.cuh"
 
@@ -22,7 +23,8 @@ namespace helm {
 constexpr int DB = 20;      // folded block (even / odd modes)
 constexpr int DT = 2 * DB;  // tile side
 constexpr int DVL = DT;     // V leading dimension (doubles): the plan's global tables, read through L1
-constexpr int DTH = 96;     // 3 warps
+constexpr int DWARPS = 5;   // warps per CTA: each owns 1/5 of the column (LEFT) / row (RIGHT) tiles
+constexpr int DTH = 32 * DWARPS;
 
 template <int NP> struct DmmaDims {
   static constexpr int XL = NP == 2 ? 88 : 40;  // X leading dimension (doubles), = 8 (mod 16)
@@ -36,78 +38,110 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
 }
 
 // LEFT product  X <- V' X  with V'(m, k) = TRANS ? V[k][m] : V[m][k], block diagonal:
-// rows of block b read and write only rows of block b, so the blocks run one after
-// the other (one set of accumulators live at a time), each in place across a barrier.
-// Warp w owns row tile (b, w) and all NT real-column tiles.  EPI(m, c, v) stores.
+// rows of block b read and write only rows of block b, so the blocks run one after the
+// other (one set of accumulators live at a time).  Columns are independent: warp w owns
+// TPW real-column tiles and all three 8-row tiles of the block, so every B fragment
+// (shared memory) feeds three DMMAs and every A fragment (V, through L1) TPW of them, and
+// the in-place update needs no block barrier (a warp only rewrites its own columns).
 template <int NP, bool TRANS, typename EPI>
 __device__ __forceinline__ void dmma_left(double* Xr, const double* __restrict__ V, EPI epi) {
-  constexpr int XL = DmmaDims<NP>::XL, NT = DmmaDims<NP>::NT;
+  constexpr int XL = DmmaDims<NP>::XL, NT = DmmaDims<NP>::NT, TPW = NT / DWARPS;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int g = lane >> 2, q = lane & 3;
+  const int c0 = w * TPW * 8;
 #pragma unroll
   for (int b = 0; b < 2; ++b) {
-    double acc[NT][2];
+    double acc[3][TPW][2];
 #pragma unroll
-    for (int t = 0; t < NT; ++t) acc[t][0] = acc[t][1] = 0.0;
-    const int m = b * DB + w * 8 + g;  // A row of this lane (may run into the next block: discarded)
+    for (int r = 0; r < 3; ++r)
+#pragma unroll
+      for (int t = 0; t < TPW; ++t) acc[r][t][0] = acc[r][t][1] = 0.0;
 #pragma unroll
     for (int ks = 0; ks < DB / 4; ++ks) {
       const int k = b * DB + ks * 4 + q;
-      const double a = (m < DT) ? __ldg(TRANS ? &V[k * DVL + m] : &V[m * DVL + k]) : 0.0;
+      double af[3], bf[TPW];
 #pragma unroll
-      for (int t = 0; t < NT; ++t) dmma(acc[t][0], acc[t][1], a, Xr[k * XL + t * 8 + g]);
+      for (int r = 0; r < 3; ++r) {
+        const int m = b * DB + r * 8 + g;  // rows past the block are discarded (past the tile: zero)
+        af[r] = (m < DT) ? __ldg(TRANS ? &V[k * DVL + m] : &V[m * DVL + k]) : 0.0;
+      }
+#pragma unroll
+      for (int t = 0; t < TPW; ++t) bf[t] = Xr[k * XL + c0 + t * 8 + g];
+#pragma unroll
+      for (int r = 0; r < 3; ++r)
+#pragma unroll
+        for (int t = 0; t < TPW; ++t) dmma(acc[r][t][0], acc[r][t][1], af[r], bf[t]);
     }
-    __syncthreads();
-    const int ml = w * 8 + g;
-    if (ml < DB) {
+    __syncwarp();
 #pragma unroll
-      for (int t = 0; t < NT; ++t) {
-        epi(b * DB + ml, t * 8 + 2 * q, acc[t][0]);
-        epi(b * DB + ml, t * 8 + 2 * q + 1, acc[t][1]);
+    for (int r = 0; r < 3; ++r) {
+      const int ml = r * 8 + g;
+      if (ml < DB) {
+#pragma unroll
+        for (int t = 0; t < TPW; ++t) {
+          epi(b * DB + ml, c0 + t * 8 + 2 * q, acc[r][t][0]);
+          epi(b * DB + ml, c0 + t * 8 + 2 * q + 1, acc[r][t][1]);
+        }
       }
     }
+    __syncwarp();
   }
 }
 
 // RIGHT product  X <- X V'  with V'(k, n) = TRANS ? V[n][k] : V[k][n], block diagonal in
 // the columns (blocks one after the other as above).  Real rows r = (m, part) read
-// X[m][k NP + part].  Warp w owns column tile (b, w) and all NT real-row tiles.
+// X[m][k NP + part] and are independent: warp w owns TPW real-row tiles and all three
+// 8-column tiles of the block (A from shared memory reused three times, B from V).
 template <int NP, bool TRANS, typename EPI>
 __device__ __forceinline__ void dmma_right(double* Xr, const double* __restrict__ V, EPI epi) {
-  constexpr int XL = DmmaDims<NP>::XL, NT = DmmaDims<NP>::NT;
+  constexpr int XL = DmmaDims<NP>::XL, NT = DmmaDims<NP>::NT, TPW = NT / DWARPS;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int g = lane >> 2, q = lane & 3;
+  const int r0 = w * TPW * 8;
 #pragma unroll
   for (int b = 0; b < 2; ++b) {
-    double acc[NT][2];
+    double acc[TPW][3][2];
 #pragma unroll
-    for (int t = 0; t < NT; ++t) acc[t][0] = acc[t][1] = 0.0;
-    const int n = b * DB + w * 8 + g;  // B column of this lane
+    for (int t = 0; t < TPW; ++t)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) acc[t][c][0] = acc[t][c][1] = 0.0;
 #pragma unroll
     for (int ks = 0; ks < DB / 4; ++ks) {
       const int k = b * DB + ks * 4 + q;
-      const double bv = (n < DT) ? __ldg(TRANS ? &V[n * DVL + k] : &V[k * DVL + n]) : 0.0;
+      double af[TPW], bf[3];
 #pragma unroll
-      for (int t = 0; t < NT; ++t) {
-        const int r = t * 8 + g;  // A row (real row) of this lane
-        dmma(acc[t][0], acc[t][1], Xr[(r / NP) * XL + k * NP + (r % NP)], bv);
+      for (int t = 0; t < TPW; ++t) {
+        const int r = r0 + t * 8 + g;  // A row (real row) of this lane
+        af[t] = Xr[(r / NP) * XL + k * NP + (r % NP)];
       }
-    }
-    __syncthreads();
 #pragma unroll
-    for (int t = 0; t < NT; ++t) {
-      const int r = t * 8 + g;
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int nl = w * 8 + 2 * q + e;
-        if (nl < DB) epi(r / NP, r % NP, b * DB + nl, acc[t][e]);
+      for (int c = 0; c < 3; ++c) {
+        const int n = b * DB + c * 8 + g;  // B column of this lane
+        bf[c] = (n < DT) ? __ldg(TRANS ? &V[n * DVL + k] : &V[k * DVL + n]) : 0.0;
       }
+#pragma unroll
+      for (int t = 0; t < TPW; ++t)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) dmma(acc[t][c][0], acc[t][c][1], af[t], bf[c]);
     }
+    __syncwarp();
+#pragma unroll
+    for (int t = 0; t < TPW; ++t) {
+      const int r = r0 + t * 8 + g;
+#pragma unroll
+      for (int c = 0; c < 3; ++c)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int nl = c * 8 + 2 * q + e;
+          if (nl < DB) epi(r / NP, r % NP, b * DB + nl, acc[t][c][e]);
+        }
+    }
+    __syncwarp();
   }
 }
 
 template <typename S>
-__global__ void __launch_bounds__(DTH, 5) local_fdm_dmma_kernel(const S* __restrict__ x, const S* __restrict__ base,
+__global__ void __launch_bounds__(DTH, 4) local_fdm_dmma_kernel(const S* __restrict__ x, const S* __restrict__ base,
                                                              S* __restrict__ y, S* __restrict__ ovl,
                                                              const int* __restrict__ boxes,
                                                              const double* __restrict__ classVf,
