@@ -57,9 +57,10 @@ template <typename S> void op_apply_A(const helm_plan* P, const S* x, S* y, int 
 template <typename S>
 static void op_coarse_correct(const helm_plan* P, helm_workspace* ws, const S* x, S* z, int batch, cudaStream_t st) {
   S* c = (S*)ws->c;
+  S* cy = (S*)ws->y0;  // a distinct output: no copy-back inside the coarse solve
   launch_restrict<S>(P->geo, x, c, batch, st);
-  launch_coarse_solve<S>(P, ws, c, c, batch, st);
-  launch_prolong<S>(P->geo, c, z, batch, st);
+  launch_coarse_solve<S>(P, ws, c, cy, batch, st);
+  launch_prolong<S>(P->geo, cy, z, batch, st);
 }
 
 // SchwarzPreconditioner.apply (schwarz.py:76-103): z = C x shared by every kind
@@ -71,18 +72,20 @@ void op_apply_M(const helm_plan* P, helm_workspace* ws, const S* x, S* y, int ba
     // z = R0^T A0^{-1} R0 x and d = x - A z (schwarz.py:86-88) with the prolongation
     // and the deflation stencil fused in one pass
     S* c = (S*)ws->c;
+    S* cy = (S*)ws->y0;  // a distinct output: no copy-back inside the coarse solve
     S* d = (S*)ws->d;
     launch_restrict<S>(P->geo, x, c, batch, st);
-    launch_coarse_solve<S>(P, ws, c, c, batch, st);
+    launch_coarse_solve<S>(P, ws, c, cy, batch, st);
     // z is not materialised: the local kernels add R0^T c at every node they write
     // (measured: 0.4 ms less per batch of 32 at config 5 than writing z and reading it back)
-    launch_prolong_deflate<S>(P->geo, c, x, nullptr, d, batch, st);
-    launch_local_sum<S>(P, d, c, y, (S*)ws->ovl, 1, batch, P->dev.band_node, st, /*coarse_base=*/true);
+    launch_prolong_deflate<S>(P->geo, cy, x, nullptr, d, batch, st);
+    launch_local_sum<S>(P, d, cy, y, (S*)ws->ovl, 1, batch, P->dev.band_node, st, /*coarse_base=*/true);
   } else {
     S* c = (S*)ws->c;
+    S* cy = (S*)ws->y0;
     launch_restrict<S>(P->geo, x, c, batch, st);
-    launch_coarse_solve<S>(P, ws, c, c, batch, st);
-    launch_local_sum<S>(P, x, c, y, (S*)ws->ovl, kind == HELM_SAS2 ? 1 : 0, batch, P->dev.band_node, st,
+    launch_coarse_solve<S>(P, ws, c, cy, batch, st);
+    launch_local_sum<S>(P, x, cy, y, (S*)ws->ovl, kind == HELM_SAS2 ? 1 : 0, batch, P->dev.band_node, st,
                         /*coarse_base=*/true);
   }
 }

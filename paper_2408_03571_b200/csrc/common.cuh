@@ -131,6 +131,26 @@ struct Geo {
   double2 tb;    // Sommerfeld 1-D end diagonal 1/h^2 - i k/h (discretization.py:136-148)
 };
 
+// One row of A (discretization.py:171-184) at node (iy, ix) applied to the centre value c
+// and its four neighbours (pass zero for neighbours outside the unknown set).
+template <typename S>
+__host__ __device__ __forceinline__ S stencil_point(const Geo& g, int ix, int iy, S c, S up, S dn, S lf, S rt) {
+  if constexpr (!Sc<S>::cplx) {
+    return (4.0 * g.inv_h2 - g.k2) * c - g.inv_h2 * (up + dn + lf + rt);
+  } else {
+    const int nu = g.nu;
+    const bool ey = (iy == 0) | (iy == nu - 1), ex = (ix == 0) | (ix == nu - 1);
+    const double wy = ey ? 0.5 : 1.0, wx = ex ? 0.5 : 1.0;
+    const double2 ty = ey ? g.tb : mk(2.0 * g.inv_h2, 0.0);
+    const double2 tx = ex ? g.tb : mk(2.0 * g.inv_h2, 0.0);
+    const double2 diag = mk(wx * ty.x + wy * tx.x - g.k2 * wy * wx, wx * ty.y + wy * tx.y);
+    S acc = mul(diag, c);
+    acc = sub(acc, scale(add(up, dn), wx * g.inv_h2));
+    acc = sub(acc, scale(add(lf, rt), wy * g.inv_h2));
+    return acc;
+  }
+}
+
 // Device-side constants of a plan (device pointers).
 struct PlanDev {
   // 1-D boxes
