@@ -13,10 +13,10 @@
 // Phi_k (2x2) and Psi_k (4x4) depend on the factors only; they are computed once per plan
 // (band_seg_setup_kernel).  Per solve, every (mode, segment) thread
 //   F1  runs its segment's forward recurrence from a zero state  -> p_k
-//   --  the CTA chains the segments:  s_{k+1} = Phi_k s_k + p_k  (one thread per mode)
+//   --  the segments are chained:  s_{k+1} = Phi_k s_k + p_k  (a warp-level affine scan per mode)
 //   F3  re-runs the segment from its true state, keeping the eliminated rows in shared memory
 //   B1  runs the backward recurrence over those rows from a zero state -> q_k
-//   --  chains downwards:  t_{k-1} = Psi_k t_k + q_k
+//   --  chained downwards:  t_{k-1} = Psi_k t_k + q_k  (suffix scan)
 //   B3  re-runs from the true state and writes x (+ add).
 // Exact in exact arithmetic (the same linear recurrence, associated differently); 1025-row
 // modes become 32-row segments, so the dependent chain is ~130 steps instead of ~2050.
@@ -51,6 +51,13 @@ struct SegRhs {
     return v;
   }
 };
+
+__device__ __forceinline__ double2 shfl_up_c(double2 v, int d) {
+  return mk(__shfl_up_sync(0xffffffffu, v.x, d), __shfl_up_sync(0xffffffffu, v.y, d));
+}
+__device__ __forceinline__ double2 shfl_dn_c(double2 v, int d) {
+  return mk(__shfl_down_sync(0xffffffffu, v.x, d), __shfl_down_sync(0xffffffffu, v.y, d));
+}
 
 __device__ __forceinline__ void fwd_step(int pv, double2 l0, double2 l1, double2& r0, double2& r1, double2 f,
                                          double2& out) {
@@ -106,12 +113,17 @@ __device__ __forceinline__ void fwd_run(const SegRhs& rhs, const int* __restrict
   }
 }
 
-template <typename Emit>
+// backward pass over rows [j0, j1) (descending) with state y; sm: eliminated rows (null:
+// zero); with out != null every solution row is stored (+ add[row] when add != null).  U and
+// the summands of the next chunk are in flight while the current chunk is consumed.
 __device__ __forceinline__ void bwd_run(const double2* __restrict__ U, int m0, int a, int j0, int j1,
-                                        double2 (&y)[4], const double2* sm, int sm_stride, Emit&& emit) {
+                                        double2 (&y)[4], const double2* sm, int sm_stride,
+                                        double2* __restrict__ out = nullptr,
+                                        const double2* __restrict__ addp = nullptr, bool store = false) {
   constexpr int C = 4;
   struct Chunk {
     double2 u[C][5];
+    double2 ad[C];
   };
   auto load = [&](int j, Chunk& ch) {  // rows j, j-1, .., j-C+1
 #pragma unroll
@@ -120,6 +132,7 @@ __device__ __forceinline__ void bwd_run(const double2* __restrict__ U, int m0, i
       const double2* u = U + 5 * ((size_t)r * m0 + a);
 #pragma unroll
       for (int e = 0; e < 5; ++e) ch.u[c][e] = __ldg(u + e);
+      ch.ad[c] = addp ? __ldg(addp + (size_t)r * m0) : mk(0.0, 0.0);
     }
   };
   if (j0 >= j1) return;
@@ -141,7 +154,7 @@ __device__ __forceinline__ void bwd_run(const double2* __restrict__ U, int m0, i
         y[2] = y[1];
         y[1] = y[0];
         y[0] = v;
-        emit(r, v);
+        if (out && store) out[(size_t)r * m0] = addp ? add(v, cur.ad[c]) : v;
       }
     }
     cur = nxt;
@@ -166,7 +179,7 @@ __global__ void band_seg_setup_kernel(const int* __restrict__ piv, const double2
   for (int c = 0; c < 4; ++c) {
     double2 y[4];
     for (int i = 0; i < 4; ++i) y[i] = mk(i == c ? 1.0 : 0.0, 0.0);
-    bwd_run(U, m0, a, j0, j1, y, nullptr, 0, [](int, double2) {});
+    bwd_run(U, m0, a, j0, j1, y, nullptr, 0);
     for (int r = 0; r < 4; ++r) psi[((size_t)k * 16 + r * 4 + c) * m0 + a] = y[r];
   }
 }
@@ -179,7 +192,7 @@ __global__ void __launch_bounds__(SEG_THREADS) band_seg_kernel(
   extern __shared__ __align__(16) unsigned char sraw[];
   double2* rows = reinterpret_cast<double2*>(sraw);  // [ls][SEG][SMB] eliminated rows
   __shared__ double2 fst[SEG + 1][SMB][2];           // forward states at segment starts
-  __shared__ double2 bst[SEG + 1][SMB][4];           // backward states at segment tops
+  __shared__ double2 bst[SEG + 2][SMB][4];           // backward states (exit of kk at kk+1 after the scan)
   const int al = threadIdx.x % SMB, k = threadIdx.x / SMB;
   const int a = blockIdx.x * SMB + al;
   const int b = blockIdx.y;
@@ -206,25 +219,38 @@ __global__ void __launch_bounds__(SEG_THREADS) band_seg_kernel(
   fst[k + 1][al][0] = r0;
   fst[k + 1][al][1] = r1;
   __syncthreads();
-  // chain: s_{k+1} = Phi_k s_k + p_k (s_1 = p_0)
-  if (k == 0 && va) {
-    double2 s0 = fst[1][al][0], s1 = fst[1][al][1];
-    double2 pc[4], pn[4];  // Phi_kk in use, Phi_{kk+1} in flight
+  // chain: s_{k+1} = Phi_k s_k + p_k (s_1 = p_0) as an inclusive affine scan over the
+  // segments: warp w takes mode w, lane kk segment kk; f_kk(s) = Phi_kk s + p_kk with
+  // f_0 = p_0 (Phi_0 = 0), composed in log2(SEG) shuffle steps
+  {
+    const int w = threadIdx.x >> 5, kk = threadIdx.x & 31;
+    const int aw = blockIdx.x * SMB + w;
+    double2 F[4], pv[2];
+    pv[0] = fst[kk + 1][w][0];
+    pv[1] = fst[kk + 1][w][1];
 #pragma unroll
-    for (int e = 0; e < 4; ++e) pc[e] = __ldg(phi + ((size_t)1 * 4 + e) * m0 + a);
-    for (int kk = 1; kk < SEG; ++kk) {
-      const int kn = kk + 1 < SEG ? kk + 1 : kk;
+    for (int e = 0; e < 4; ++e) F[e] = (kk > 0 && aw < m0) ? __ldg(phi + ((size_t)kk * 4 + e) * m0 + aw) : mk(0.0, 0.0);
 #pragma unroll
-      for (int e = 0; e < 4; ++e) pn[e] = __ldg(phi + ((size_t)kn * 4 + e) * m0 + a);
-      const double2 n0 = add(fst[kk + 1][al][0], add(mul(pc[0], s0), mul(pc[1], s1)));
-      const double2 n1 = add(fst[kk + 1][al][1], add(mul(pc[2], s0), mul(pc[3], s1)));
-      fst[kk][al][0] = s0;  // entry state of segment kk
-      fst[kk][al][1] = s1;
-      s0 = n0;
-      s1 = n1;
+    for (int d = 1; d < SEG; d <<= 1) {
+      double2 Fo[4], po[2];
 #pragma unroll
-      for (int e = 0; e < 4; ++e) pc[e] = pn[e];
+      for (int e = 0; e < 4; ++e) Fo[e] = shfl_up_c(F[e], d);
+      po[0] = shfl_up_c(pv[0], d);
+      po[1] = shfl_up_c(pv[1], d);
+      if (kk >= d) {  // (mine) o (theirs): F <- F Fo, p <- F po + p
+        const double2 n0 = add(pv[0], add(mul(F[0], po[0]), mul(F[1], po[1])));
+        const double2 n1 = add(pv[1], add(mul(F[2], po[0]), mul(F[3], po[1])));
+        const double2 G0 = add(mul(F[0], Fo[0]), mul(F[1], Fo[2])), G1 = add(mul(F[0], Fo[1]), mul(F[1], Fo[3]));
+        const double2 G2 = add(mul(F[2], Fo[0]), mul(F[3], Fo[2])), G3 = add(mul(F[2], Fo[1]), mul(F[3], Fo[3]));
+        F[0] = G0; F[1] = G1; F[2] = G2; F[3] = G3;
+        pv[0] = n0;
+        pv[1] = n1;
+      }
     }
+    __syncthreads();  // every lane has read its p before the entry states overwrite fst
+    // entry state of segment kk+1 = exit of kk
+    fst[kk + 1][w][0] = pv[0];
+    fst[kk + 1][w][1] = pv[1];
   }
   __syncthreads();
   // F3: true forward pass, eliminated rows kept in shared memory
@@ -240,48 +266,61 @@ __global__ void __launch_bounds__(SEG_THREADS) band_seg_kernel(
   double2 y[4];
 #pragma unroll
   for (int i = 0; i < 4; ++i) y[i] = mk(0.0, 0.0);
-  bwd_run(U, m0, ac, j0, j1, y, mysm, sstride, [](int, double2) {});
+  bwd_run(U, m0, ac, j0, j1, y, mysm, sstride);
 #pragma unroll
   for (int i = 0; i < 4; ++i) bst[k][al][i] = y[i];
   __syncthreads();
-  // chain downwards: the state entering segment k is the exit state of segment k+1
-  if (k == 0 && va) {
-    double2 t[4];
+  // chain downwards: exit_kk = Psi_kk entry_kk + q_kk with entry_kk = exit_{kk+1} and a
+  // zero entry at the top, as a suffix affine scan (lane kk composes with lane kk + d)
+  {
+    const int w = threadIdx.x >> 5, kk = threadIdx.x & 31;
+    const int aw = blockIdx.x * SMB + w;
+    double2 Q[16], qv[4];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) t[i] = bst[SEG - 1][al][i];  // the top segment starts from zeros
-    double2 qc[16], qn[16];  // Psi_kk in use, Psi_{kk-1} in flight
+    for (int i = 0; i < 4; ++i) qv[i] = bst[kk][w][i];
 #pragma unroll
-    for (int e = 0; e < 16; ++e) qc[e] = __ldg(psi + ((size_t)(SEG - 2) * 16 + e) * m0 + a);
-    for (int kk = SEG - 2; kk >= 0; --kk) {
-      double2 n[4];
-      const int kn = kk > 0 ? kk - 1 : 0;
+    for (int e = 0; e < 16; ++e)
+      Q[e] = (kk < SEG - 1 && aw < m0) ? __ldg(psi + ((size_t)kk * 16 + e) * m0 + aw) : mk(0.0, 0.0);
 #pragma unroll
-      for (int e = 0; e < 16; ++e) qn[e] = __ldg(psi + ((size_t)kn * 16 + e) * m0 + a);
+    for (int d = 1; d < SEG; d <<= 1) {
+      double2 Qo[16], qo[4];
 #pragma unroll
-      for (int r = 0; r < 4; ++r) {
-        double2 s = bst[kk][al][r];
+      for (int e = 0; e < 16; ++e) Qo[e] = shfl_dn_c(Q[e], d);
 #pragma unroll
-        for (int c = 0; c < 4; ++c) s = fma_(qc[r * 4 + c], t[c], s);
-        n[r] = s;
-      }
+      for (int i = 0; i < 4; ++i) qo[i] = shfl_dn_c(qv[i], d);
+      if (kk + d < SEG) {  // (mine) o (theirs): Q <- Q Qo, q <- Q qo + q
+        double2 nq[4], NQ[16];
 #pragma unroll
-      for (int e = 0; e < 16; ++e) qc[e] = qn[e];
+        for (int r = 0; r < 4; ++r) {
+          double2 t = qv[r];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        bst[kk + 1][al][i] = t[i];  // entry state of segment kk  (stored one slot up)
-        t[i] = n[i];
+          for (int c = 0; c < 4; ++c) t = fma_(Q[r * 4 + c], qo[c], t);
+          nq[r] = t;
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            double2 m = mk(0.0, 0.0);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) m = fma_(Q[r * 4 + i], Qo[i * 4 + c], m);
+            NQ[r * 4 + c] = m;
+          }
+        }
+#pragma unroll
+        for (int e = 0; e < 16; ++e) Q[e] = NQ[e];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) qv[i] = nq[i];
       }
     }
+    __syncthreads();
+    // entry state of segment kk = exit of kk+1: stored one slot up (bst[kk+1] = exit_kk)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) bst[kk + 1][w][i] = qv[i];
   }
   __syncthreads();
   // B3: true backward pass
 #pragma unroll
-  for (int i = 0; i < 4; ++i) y[i] = k == SEG - 1 ? mk(0.0, 0.0) : bst[k + 1][al][i];
-  double2* o = out + (size_t)b * N0 + ac;
-  const double2* ad = addv ? addv + (size_t)b * N0 + ac : nullptr;
-  bwd_run(U, m0, ac, j0, j1, y, mysm, sstride, [&](int j, double2 v) {
-    if (va) o[(size_t)j * m0] = ad ? ::helm::add(v, __ldg(ad + (size_t)j * m0)) : v;
-  });
+  for (int i = 0; i < 4; ++i) y[i] = k == SEG - 1 ? mk(0.0, 0.0) : bst[k + 2][al][i];
+  bwd_run(U, m0, ac, j0, j1, y, mysm, sstride, out + (size_t)b * N0 + ac,
+          addv ? addv + (size_t)b * N0 + ac : nullptr, va);
 }
 
 static int seg_len(int m0) { return (m0 + SEG - 1) / SEG; }
