@@ -24,6 +24,8 @@
 // Everything is O(m0^2 log m0) per right-hand side and HBM-bound (dense fast
 // diagonalisation would be O(m0^3) FP64).  refine_steps iterative-refinement
 // steps r = c - A0 y (25-point residual), y += solve(r) follow.
+#include <type_traits>
+
 #include "ops.cuh"
 
 namespace helm {
@@ -41,6 +43,7 @@ __global__ void __launch_bounds__(256) strip_reduce_kernel(const S* __restrict__
   if (y >= m0) return;
   const S* row = Yh + ((size_t)b * m0 + y) * m0;
   S acc[4] = {Sc<S>::zero(), Sc<S>::zero(), Sc<S>::zero(), Sc<S>::zero()};
+#pragma unroll 8
   for (int a = lane; a < m0; a += 32) {
     const S v = row[a];
     const double4 qa = *reinterpret_cast<const double4*>(q + (size_t)a * 4);
@@ -247,11 +250,144 @@ __global__ void __launch_bounds__(256) strip_reduce_right_kernel(const double2* 
   }
 }
 
+// Small batches (<= 4 right-hand sides, NC = 4 * batch strip columns): one warp per output
+// row, the fold / unfold and the 4x4 epilogue fused into the product (one launch per side).
+// left:  row r of the packed mode blocks, t = A_g[r] . fold(Z), out[r] = Hm[r] t  (Hm may be null)
+template <int NC>
+__global__ void __launch_bounds__(256) strip_left_fused_kernel(const double2* __restrict__ A,
+                                                               const double2* __restrict__ Z,
+                                                               double2* __restrict__ out,
+                                                               const double2* __restrict__ Hm, int m0) {
+  const int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (r >= m0) return;
+  const int he = (m0 + 1) / 2, ho = m0 / 2;
+  const bool odd = r >= he;
+  const int Mg = odd ? ho : he;
+  const double2* arow = A + (odd ? (size_t)he * he + (size_t)(r - he) * ho : (size_t)r * he);
+  double2 acc[NC];
+#pragma unroll
+  for (int c = 0; c < NC; ++c) acc[c] = mk(0.0, 0.0);
+#pragma unroll 4
+  for (int k = lane; k < Mg; k += 32) {
+    const double2 av = arow[k];
+    const double2* z0 = Z + (size_t)k * NC;
+    const double2* z1 = Z + (size_t)(m0 - 1 - k) * NC;
+    const bool centre = !odd && k == ho;  // odd m0: the centre row belongs to the even block alone
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      const double2 a = z0[c];
+      const double2 f = centre ? a : (odd ? sub(a, z1[c]) : add(a, z1[c]));
+      acc[c] = fma_(av, f, acc[c]);
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < NC; ++c) acc[c] = warp_sum(acc[c]);
+  if (lane < NC) {
+    const int g = lane >> 2, i = lane & 3;
+    double2 v;
+    if (Hm) {
+      const double2* h = Hm + (size_t)r * 16 + i * 4;
+      v = mk(0.0, 0.0);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        double2 tj = acc[0];
+#pragma unroll
+        for (int c = 0; c < NC; ++c)
+          if (c == g * 4 + j) tj = acc[c];
+        v = fma_(h[j], tj, v);
+      }
+    } else {
+      v = acc[0];
+#pragma unroll
+      for (int c = 1; c < NC; ++c)
+        if (lane == c) v = acc[c];
+    }
+    out[(size_t)r * NC + lane] = v;
+  }
+}
+
+// right: for y < he, E = A_e[y] . cin[0:he), O = A_o[y] . cin[he:m0) (y < ho);
+// out[y] = E + O (- minus[y]), out[m0-1-y] = E - O (- minus[m0-1-y]), out[centre] = E
+template <int NC>
+__global__ void __launch_bounds__(256) strip_right_fused_kernel(const double2* __restrict__ A,
+                                                                const double2* __restrict__ cin,
+                                                                double2* __restrict__ out,
+                                                                const double2* __restrict__ minus, int m0) {
+  const int y = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int he = (m0 + 1) / 2, ho = m0 / 2;
+  if (y >= he) return;
+  const double2* ae = A + (size_t)y * he;
+  double2 E[NC], O[NC];
+#pragma unroll
+  for (int c = 0; c < NC; ++c) E[c] = O[c] = mk(0.0, 0.0);
+#pragma unroll 4
+  for (int k = lane; k < he; k += 32) {
+    const double2 av = ae[k];
+#pragma unroll
+    for (int c = 0; c < NC; ++c) E[c] = fma_(av, cin[(size_t)k * NC + c], E[c]);
+  }
+  if (y < ho) {
+    const double2* ao = A + (size_t)he * he + (size_t)y * ho;
+#pragma unroll 4
+    for (int k = lane; k < ho; k += 32) {
+      const double2 av = ao[k];
+#pragma unroll
+      for (int c = 0; c < NC; ++c) O[c] = fma_(av, cin[(size_t)(he + k) * NC + c], O[c]);
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    E[c] = warp_sum(E[c]);
+    O[c] = warp_sum(O[c]);
+  }
+  if (lane < NC) {
+    double2 e = E[0], o = O[0];
+#pragma unroll
+    for (int c = 1; c < NC; ++c)
+      if (lane == c) {
+        e = E[c];
+        o = O[c];
+      }
+    const size_t pl = (size_t)y * NC + lane, ph = (size_t)(m0 - 1 - y) * NC + lane;
+    if (y < ho) {
+      double2 lo = add(e, o), hi = sub(e, o);
+      if (minus) {
+        lo = sub(lo, minus[pl]);
+        hi = sub(hi, minus[ph]);
+      }
+      out[pl] = lo;
+      out[ph] = hi;
+    } else {
+      out[pl] = minus ? sub(e, minus[pl]) : e;
+    }
+  }
+}
+
 // out = fold-GEMM of Zin with the packed blocks A; left: + 4x4 epilogue Hm (Zin in y order,
 // folded here into Zf); right: unfolded, minus subtracted (Zin in mode order).
 static void strip_gemm_fold(const double2* A, const double2* Zin, double2* out, bool left, const double2* Hm,
                             const double2* minus, int m0, int batch, double2* Zf, double2* part, cudaStream_t st) {
   const int ldn = 4 * batch, he = (m0 + 1) / 2, ho = m0 / 2;
+  if (batch <= 4) {
+    const int blocks_l = (m0 * 32 + 255) / 256, blocks_r = (he * 32 + 255) / 256;
+    auto go = [&](auto nc) {
+      constexpr int NC = decltype(nc)::value;
+      if (left)
+        strip_left_fused_kernel<NC><<<blocks_l, 256, 0, st>>>(A, Zin, out, Hm, m0);
+      else
+        strip_right_fused_kernel<NC><<<blocks_r, 256, 0, st>>>(A, Zin, out, minus, m0);
+    };
+    switch (batch) {
+      case 1: go(std::integral_constant<int, 4>{}); break;
+      case 2: go(std::integral_constant<int, 8>{}); break;
+      case 3: go(std::integral_constant<int, 12>{}); break;
+      default: go(std::integral_constant<int, 16>{}); break;
+    }
+    HELM_LAUNCH_CHECK();
+    return;
+  }
   const double2* B = Zin;
   if (left) {
     strip_fold_kernel<<<(he * ldn + 255) / 256, 256, 0, st>>>(Zin, Zf, m0, ldn);
