@@ -16,7 +16,7 @@ FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-lineinfo", "-O3", "-std=c++17", "-Xcompiler", "-fPIC",
     "-Xptxas", "-v", "--expt-relaxed-constexpr",
-]
+] + os.environ.get("HELM_NVCC_EXTRA", "").split()  # development experiments only
 
 
 def _stale(target: str, deps) -> bool:
