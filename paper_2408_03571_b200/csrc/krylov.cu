@@ -496,7 +496,8 @@ constexpr size_t SMEM_MAX = 227 * 1024;
 
 static void set_smem(const void* fn, size_t bytes) {
   HELM_CHECK(bytes <= SMEM_MAX, "Krylov basis too large for the CGS2 kernels");
-  if (bytes > 48 * 1024) HELM_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+  // opt in above 32 KB: the 48 KB default also has to hold the kernels' static shared variables
+  if (bytes > 32 * 1024) HELM_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
 }
 
 template <typename S>

@@ -41,6 +41,10 @@ CASES = {
     "cfg4a": (1025, 200.0, "MP2", 32, 2, 2, "point", False),
     "cfg4b": (1025, 200.0, "MP2", 32, 2, 2, "random", False),
 }
+# Config 4(b) (seed-0 random RHS) does not converge within 1000 iterations (the device solver
+# measures |r|/|b| = 3.4e-3 at 1000), and the reference needs hours per thousand iterations
+# at n = 1025: its golden is a fixed-length run, compared iterate by iterate.
+CAP = {"cfg4b": 100}
 
 GMRES_RTOL = 1e-6
 GMRES_CAP = 1000
@@ -95,7 +99,9 @@ def run_case(name: str):
             Mk = H.SchwarzPreconditioner(kind, prob.A, dec, cs, local_factorizations=M.local_factorizations)
             out["M_" + kind.lower()] = Mk(x)
     b = prob.f if rhs_kind == "point" else random_rhs(N)
-    rep = H.gmres(prob.A, M, b, H.GmresConfig(rtol=GMRES_RTOL, max_iter=GMRES_CAP, side="right"))
+    cap = CAP.get(name, GMRES_CAP)
+    rep = H.gmres(prob.A, M, b, H.GmresConfig(rtol=GMRES_RTOL, max_iter=cap, side="right"))
+    out["gmres_cap"] = cap
     out["gmres_rhs"] = rhs_kind
     out["gmres_iterations"] = rep.iterations
     out["gmres_converged"] = rep.converged

@@ -205,3 +205,27 @@ def test_segmented_band_solve_matches_lane_recurrence(n, k, p):
         y1 = M.coarse_solve(C[i])  # batch 1: segmented recurrence
         assert rel(y1, Yb[i]) <= 1e-13
         assert np.linalg.norm(a0 @ y1 - C[i]) / np.linalg.norm(C[i]) <= 1e-12
+
+
+def test_cgs2_every_basis_size_launches():
+    """The CGS2 kernels size their shared memory by the basis length: every length up to a
+    long run (including the 48 KB opt-in boundary at 384 vectors) must launch, and the new
+    vector must come out orthonormal to the basis."""
+    import paper_2408_03571_b200 as hb
+
+    grid = hb.Grid(65, "sommerfeld")
+    prob = hb.assemble(grid, 10.0, "MP2")
+    M = hb.SchwarzPreconditioner("SHS2", prob.A, hb.extend(hb.partition(grid, 8), 2), hb.build_hocs(grid, 2))
+    lib, pl = M.plan.lib, M.plan
+    N = M.N
+    g = torch.Generator(device="cuda").manual_seed(0)
+    for j in (0, 7, 31, 216, 217, 383, 384, 600):
+        Q, _ = torch.linalg.qr(torch.randn(N, j + 1, dtype=torch.complex128, device="cuda", generator=g))
+        V = torch.cat([Q.T.contiguous(), torch.randn(1, N, dtype=torch.complex128, device="cuda", generator=g)])
+        h = torch.empty(j + 2, dtype=torch.complex128, device="cuda")
+        st = torch.cuda.current_stream().cuda_stream
+        assert lib.helm_cgs2(pl.handle, pl.ws, V.data_ptr(), j, h.data_ptr(), st) == 0, lib.helm_last_error()
+        torch.cuda.synchronize()
+        w = V[j + 1]
+        assert abs(torch.linalg.vector_norm(w).item() - 1.0) < 1e-12
+        assert torch.abs(V[: j + 1].conj() @ w).max().item() < 1e-12
