@@ -79,14 +79,14 @@ void op_apply_M(const helm_plan* P, helm_workspace* ws, const S* x, S* y, int ba
     // z is not materialised: the local kernels add R0^T c at every node they write
     // (measured: 0.4 ms less per batch of 32 at config 5 than writing z and reading it back)
     launch_prolong_deflate<S>(P->geo, cy, x, nullptr, d, batch, st);
-    launch_local_sum<S>(P, d, cy, y, (S*)ws->ovl, 1, batch, P->dev.band_node, st, /*coarse_base=*/true);
+    launch_local_sum<S>(P, d, cy, y, (S*)ws->ovl, 1, batch, P->dev.band_node, st, /*coarse_base=*/true, ws);
   } else {
     S* c = (S*)ws->c;
     S* cy = (S*)ws->y0;
     launch_restrict<S>(P->geo, x, c, batch, st);
     launch_coarse_solve<S>(P, ws, c, cy, batch, st);
     launch_local_sum<S>(P, x, cy, y, (S*)ws->ovl, kind == HELM_SAS2 ? 1 : 0, batch, P->dev.band_node, st,
-                        /*coarse_base=*/true);
+                        /*coarse_base=*/true, ws);
   }
 }
 
@@ -534,6 +534,9 @@ int helm_workspace_create(const helm_plan* P, int32_t max_batch, helm_workspace*
     HELM_CUDA(cudaMalloc(&w->red, w->red_bytes));
     HELM_CUDA(cudaMemset(w->red, 0, w->red_bytes));  // the CGS2 completion counters start at zero
     HELM_CUDA(cudaMallocHost(&w->pinned, 64 * sizeof(double)));
+    HELM_CUDA(cudaStreamCreateWithFlags(&w->side, cudaStreamNonBlocking));
+    HELM_CUDA(cudaEventCreateWithFlags(&w->fork, cudaEventDisableTiming));
+    HELM_CUDA(cudaEventCreateWithFlags(&w->join, cudaEventDisableTiming));
     *out = w;
   });
 }
@@ -547,6 +550,9 @@ int helm_workspace_destroy(helm_workspace* w) {
     for (void* q : ptrs)
       if (q) cudaFree(q);
     if (w->pinned) cudaFreeHost(w->pinned);
+    if (w->side) cudaStreamDestroy(w->side);
+    if (w->fork) cudaEventDestroy(w->fork);
+    if (w->join) cudaEventDestroy(w->join);
     delete w;
   });
 }
@@ -625,7 +631,7 @@ int helm_local_sum(const helm_plan* P, helm_workspace* ws, const void* x, const 
     dispatch(P, [&](auto t) {
       using S = decltype(t);
       launch_local_sum<S>(P, (const S*)x, (const S*)base, (S*)y, (S*)ws->ovl, weighted ? 1 : 0, batch,
-                          P->dev.band_node, (cudaStream_t)stream);
+                          P->dev.band_node, (cudaStream_t)stream, /*coarse_base=*/false, ws);
     });
   });
 }

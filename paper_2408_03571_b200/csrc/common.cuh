@@ -258,4 +258,6 @@ struct helm_workspace {
   size_t red_bytes;
   void* pinned;   // small pinned host buffer for scalar read-back
   void* basis;    // GMRES Krylov basis (basis.cu: reserved address range, physical chunks on demand)
+  cudaStream_t side;       // second stream: the boundary-box solves run beside the tensor-core boxes
+  cudaEvent_t fork, join;  // ordering of the side stream against the caller's stream
 };

@@ -156,7 +156,7 @@ size_t local_smem_bytes(int ld, size_t elem) { return (size_t)(4 * ld * ld + 2 *
 
 template <typename S>
 void launch_local_sum(const helm_plan* P, const S* x, const S* base, S* y, S* ovl, int weighted, int batch,
-                      const int* band_node, cudaStream_t st, bool coarse_base) {
+                      const int* band_node, cudaStream_t st, bool coarse_base, helm_workspace* ws) {
   const PlanDev& d = P->dev;
   HELM_CHECK(d.p > 0, "plan was created without subdomains");
   LocalArgs a;
@@ -180,7 +180,7 @@ void launch_local_sum(const helm_plan* P, const S* x, const S* base, S* y, S* ov
   a.node_band = d.node_band;
   const int ld = d.max_len;
   dim3 grd(d.p * d.p, batch);
-  if (!launch_local_fast<S>(P, x, base, y, ovl, a, batch, st)) {
+  if (!launch_local_fast<S>(P, x, base, y, ovl, a, batch, st, ws)) {
     const size_t smem = local_smem_bytes(ld, sizeof(S));
     static bool attr_set[2] = {false, false};
     if (!attr_set[Sc<S>::cplx]) {
@@ -202,8 +202,8 @@ void launch_local_sum(const helm_plan* P, const S* x, const S* base, S* y, S* ov
 }
 
 template void launch_local_sum<double>(const helm_plan*, const double*, const double*, double*, double*, int, int,
-                                       const int*, cudaStream_t, bool);
+                                       const int*, cudaStream_t, bool, helm_workspace*);
 template void launch_local_sum<double2>(const helm_plan*, const double2*, const double2*, double2*, double2*, int,
-                                        int, const int*, cudaStream_t, bool);
+                                        int, const int*, cudaStream_t, bool, helm_workspace*);
 
 }  // namespace helm

@@ -104,7 +104,7 @@ __host__ __device__ __forceinline__ size_t base_stride(const LocalArgs& a) {
 // Returns false (nothing launched) when the plan's boxes are larger.
 template <typename S>
 bool launch_local_fast(const helm_plan* P, const S* x, const S* base, S* y, S* ovl, const LocalArgs& a, int batch,
-                       cudaStream_t st);
+                       cudaStream_t st, helm_workspace* ws);
 
 // Folded boxes (both classes real and symmetric) on the FP64 tensor pipe (local_dmma.cu).
 template <typename S>

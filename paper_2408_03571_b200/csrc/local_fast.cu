@@ -212,18 +212,31 @@ static void fast_launch(const helm_plan* P, const S* x, const S* base, S* y, S* 
 
 template <typename S>
 bool launch_local_fast(const helm_plan* P, const S* x, const S* base, S* y, S* ovl, const LocalArgs& a, int batch,
-                       cudaStream_t st) {
+                       cudaStream_t st, helm_workspace* ws) {
   const PlanDev& d = P->dev;
   if (d.max_len > LT) return false;
+  // The box groups write disjoint nodes / overlap slots, so with a workspace the DFMA boxes
+  // run on its side stream beside the tensor-core boxes (at batch 1 they are < 1 wave and
+  // would otherwise leave most SMs idle for their whole duration).
+  const bool fork = ws && ws->side && (d.n_rr + d.n_mix) > 0;
+  cudaStream_t sf = fork ? ws->side : st;
+  if (fork) {
+    HELM_CUDA(cudaEventRecord(ws->fork, st));
+    HELM_CUDA(cudaStreamWaitEvent(ws->side, ws->fork, 0));
+  }
+  fast_launch<S, false>(P, x, base, y, ovl, a, d.box_mix, d.n_mix, batch, sf);
+  fast_launch<S, true>(P, x, base, y, ovl, a, d.box_rr, d.n_rr, batch, sf);
   launch_local_dmma<S>(P, x, base, y, ovl, a, batch, st);  // folded real classes: FP64 tensor pipe
-  fast_launch<S, true>(P, x, base, y, ovl, a, d.box_rr, d.n_rr, batch, st);
-  fast_launch<S, false>(P, x, base, y, ovl, a, d.box_mix, d.n_mix, batch, st);
+  if (fork) {
+    HELM_CUDA(cudaEventRecord(ws->join, ws->side));
+    HELM_CUDA(cudaStreamWaitEvent(st, ws->join, 0));
+  }
   return true;
 }
 
 template bool launch_local_fast<double>(const helm_plan*, const double*, const double*, double*, double*,
-                                        const LocalArgs&, int, cudaStream_t);
+                                        const LocalArgs&, int, cudaStream_t, helm_workspace*);
 template bool launch_local_fast<double2>(const helm_plan*, const double2*, const double2*, double2*, double2*,
-                                         const LocalArgs&, int, cudaStream_t);
+                                         const LocalArgs&, int, cudaStream_t, helm_workspace*);
 
 }  // namespace helm

@@ -11,7 +11,8 @@ template <typename S>
 void launch_prolong_deflate(const Geo& g, const S* c, const S* x, S* z, S* d, int batch, cudaStream_t st);
 template <typename S>
 void launch_local_sum(const helm_plan* P, const S* x, const S* base, S* y, S* ovl, int weighted, int batch,
-                      const int* band_node, cudaStream_t st, bool coarse_base = false);
+                      const int* band_node, cudaStream_t st, bool coarse_base = false,
+                      helm_workspace* ws = nullptr);
 template <typename S>
 void launch_coarse_solve(const helm_plan* P, helm_workspace* ws, const S* c, S* y, int batch, cudaStream_t st);
 
