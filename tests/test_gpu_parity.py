@@ -94,16 +94,26 @@ def test_gmres_matches_reference(name):
 
 @pytest.mark.parametrize("name", RUN_CASES)
 def test_gmres_large_configs(name):
-    """BASELINE configs 3 and 4: iteration counts, residual histories, sampled solutions."""
+    """BASELINE configs 3 and 4: iteration counts, residual histories, sampled solutions.
+    Config 4(b) (random RHS) does not converge within 1000 iterations; its golden is the
+    reference's first 100 iterations, compared estimate by estimate and on the iterate."""
     import paper_2408_03571_b200 as hb
 
     g, prob, Ms = build(name)
     b = prob.f if str(g["gmres_rhs"]) == "point" else random_rhs(prob.A.N)
-    rep = hb.gmres(prob.A, Ms["SHS2"], b, hb.GmresConfig(rtol=1e-6, max_iter=1000))
+    cap = int(g["gmres_cap"]) if "gmres_cap" in g else 1000
+    rep = hb.gmres(prob.A, Ms["SHS2"], b, hb.GmresConfig(rtol=1e-6, max_iter=cap))
     raw, refined = reference_count(name, g)
     stride = int(g["gmres_x_sample_stride"])
     xe = rel(rep.x[::stride], g["gmres_x_sample"])
     print(name, rep.iterations, raw, refined, f"x(sample) {xe:.1e}", f"{rep.wall_seconds:.2f}s")
+    if not bool(g["gmres_converged"]):  # fixed-length run: the same iterates
+        assert not rep.converged and rep.iterations == raw
+        h, hr = rep.residual_history, g["gmres_history"]
+        assert np.all(np.abs(h - hr) <= 1e-9 * hr), np.max(np.abs(h - hr) / hr)
+        assert abs(rep.final_residual - float(g["gmres_final_residual"])) <= 1e-9 * float(g["gmres_final_residual"])
+        assert xe <= X_TOL
+        return
     assert rep.converged and count_matches(rep.iterations, raw, refined), (rep.iterations, raw, refined)
     assert rep.final_residual <= 1e-6
     assert xe <= (REF_SPREAD if name in UNREPRODUCIBLE else X_TOL)
