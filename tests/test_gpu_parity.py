@@ -239,3 +239,38 @@ def test_cgs2_every_basis_size_launches():
         w = V[j + 1]
         assert abs(torch.linalg.vector_norm(w).item() - 1.0) < 1e-12
         assert torch.abs(V[: j + 1].conj() @ w).max().item() < 1e-12
+
+
+@pytest.mark.parametrize("problem,n,k,p", [("MP2", 65, 10.0, 8), ("MP1", 65, 12.0, 4)])
+@pytest.mark.parametrize("kind", ["AS2", "SAS2", "SHS2"])
+def test_weights_before_solve_matches_oracle(problem, n, k, p, kind):
+    """schwarz.py:69-70 (weights applied before the local solves) for every kind."""
+    import helmdd_oracle as O  # checker only
+    import paper_2408_03571_b200 as hb
+
+    grid = hb.Grid(n, "dirichlet" if problem == "MP1" else "sommerfeld")
+    prob = hb.assemble(grid, k, problem)
+    dec = hb.extend(hb.partition(grid, p), 2)
+    M = hb.SchwarzPreconditioner(kind, prob.A, dec, hb.build_hocs(grid, 2), weights_before_solve=True)
+    oprob, odec, ocs, _ = O.build_shs2(n, k, problem, p, 2)
+    oM = O.OSchwarz(kind, oprob.A, odec, ocs, weights_before_solve=True)
+    x = operator_input(prob.A.N, problem == "MP2")
+    assert rel(M(x), oM(x)) <= OP_TOL
+
+
+@pytest.mark.parametrize("problem,n,k,p", [("MP2", 65, 10.0, 8), ("MP1", 65, 20.0, 4)])
+def test_left_preconditioned_gmres_matches_oracle(problem, n, k, p):
+    """Left preconditioning (gmres.py:79-85,154: stops on the preconditioned estimate):
+    same count, history and solution as the oracle."""
+    import helmdd_oracle as O  # checker only
+    import paper_2408_03571_b200 as hb
+
+    grid = hb.Grid(n, "dirichlet" if problem == "MP1" else "sommerfeld")
+    prob = hb.assemble(grid, k, problem)
+    M = hb.SchwarzPreconditioner("SHS2", prob.A, hb.extend(hb.partition(grid, p), 2), hb.build_hocs(grid, 2))
+    oprob, _, _, oM = O.build_shs2(n, k, problem, p, 2)
+    rep = hb.gmres(prob.A, M, prob.f, hb.GmresConfig(rtol=1e-7, max_iter=200, side="left"))
+    orep = O.gmres(oprob.A, oM, oprob.f, 1e-7, 200, side="left")
+    assert rep.converged == orep.converged and rep.iterations == orep.iterations
+    assert np.all(np.abs(rep.residual_history - orep.residual_history) <= 1e-6 * orep.residual_history + 1e-14)
+    assert rel(rep.x, orep.x) <= X_TOL
