@@ -5,6 +5,8 @@
 #include <atomic>
 #include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "ops.cuh"
@@ -190,18 +192,35 @@ static void gmres_impl(const helm_plan* P, helm_workspace* ws, const S* b, S* x,
     return std::sqrt(hp[0]) / bnorm;
   };
 
+  static const bool trace = std::getenv("HELM_GMRES_TRACE") != nullptr;
+  cudaEvent_t tev[3] = {nullptr, nullptr, nullptr};
+  if (trace)
+    for (auto& e : tev) HELM_CUDA(cudaEventCreate(&e));
+  auto tprev = std::chrono::steady_clock::now();
   bool done = false;
   for (int j = 0; j < mi && !done; ++j) {
     ensure_basis(j + 2);
     S* vj = Vp + (size_t)j * N;
+    if (trace) HELM_CUDA(cudaEventRecord(tev[0], st));
     applyOp(vj, vj + N);
     // CGS2 (3 sweeps) with the Givens update of column j fused into its reducing block
+    if (trace) HELM_CUDA(cudaEventRecord(tev[1], st));
     krylov_cgs2_impl<S>(Vp, j, N, N, H.p + j, (size_t)mi, scal.p + 2, scratch, st, H.p, mi, cs.p, sn.p, g.p, beta,
                         scal.p + 4);
+    if (trace) HELM_CUDA(cudaEventRecord(tev[2], st));
     HELM_CUDA(cudaMemcpyAsync(hp, scal.p + 2, 3 * sizeof(double), cudaMemcpyDeviceToHost, st));
     HELM_CUDA(cudaStreamSynchronize(st));
     const bool brk = hp[1] != 0.0;
     const double est = hp[2];
+    if (trace) {  // HELM_GMRES_TRACE=1: per-iteration device times of the operator and of CGS2
+      float t_op = 0.f, t_cgs = 0.f;
+      cudaEventElapsedTime(&t_op, tev[0], tev[1]);
+      cudaEventElapsedTime(&t_cgs, tev[1], tev[2]);
+      const auto tn = std::chrono::steady_clock::now();
+      std::fprintf(stderr, "gmres it %d wall %.3f ms op %.3f cgs2 %.3f\n", j,
+                   std::chrono::duration<double, std::milli>(tn - tprev).count(), t_op, t_cgs);
+      tprev = tn;
+    }
     if (history) history[j + 1] = est;
     if (est <= rtol || brk) {
       form_solution(j);
@@ -224,6 +243,8 @@ static void gmres_impl(const helm_plan* P, helm_workspace* ws, const S* b, S* x,
     rep->final_residual = true_residual();
   }
   HELM_CUDA(cudaStreamSynchronize(st));
+  if (trace)
+    for (auto& e : tev) cudaEventDestroy(e);
   rep->wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
 }
 
