@@ -268,7 +268,7 @@ __global__ void __launch_bounds__(256) strip_left_fused_kernel(const double2* __
   double2 acc[NC];
 #pragma unroll
   for (int c = 0; c < NC; ++c) acc[c] = mk(0.0, 0.0);
-#pragma unroll 4
+#pragma unroll 8
   for (int k = lane; k < Mg; k += 32) {
     const double2 av = arow[k];
     const double2* z0 = Z + (size_t)k * NC;
@@ -322,7 +322,7 @@ __global__ void __launch_bounds__(256) strip_right_fused_kernel(const double2* _
   double2 E[NC], O[NC];
 #pragma unroll
   for (int c = 0; c < NC; ++c) E[c] = O[c] = mk(0.0, 0.0);
-#pragma unroll 4
+#pragma unroll 8
   for (int k = lane; k < he; k += 32) {
     const double2 av = ae[k];
 #pragma unroll
@@ -330,7 +330,7 @@ __global__ void __launch_bounds__(256) strip_right_fused_kernel(const double2* _
   }
   if (y < ho) {
     const double2* ao = A + (size_t)he * he + (size_t)y * ho;
-#pragma unroll 4
+#pragma unroll 8
     for (int k = lane; k < ho; k += 32) {
       const double2 av = ao[k];
 #pragma unroll
