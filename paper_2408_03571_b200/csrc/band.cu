@@ -30,18 +30,20 @@ struct BandFwdStage {
   double2 rhs[NW][RB][R][BW];
   double2 corr[NW][RB][R][4];
 };
-template <int RB, int NW, int R>
+template <int RB, int NW, int R, int UE>
 struct BandBwdStage {
-  double2 U[R][BW][5];
+  double2 U[R][BW][UE];
   double2 v[NW][RB][R][BW];
 };
 template <int RB, int NW, int R, int ST>
 constexpr size_t band_smem_bytes() {
-  return ST * (sizeof(BandFwdStage<RB, NW, R>) > sizeof(BandBwdStage<RB, NW, R>) ? sizeof(BandFwdStage<RB, NW, R>)
-                                                                                  : sizeof(BandBwdStage<RB, NW, R>));
+  return ST * (sizeof(BandFwdStage<RB, NW, R>) > sizeof(BandBwdStage<RB, NW, R, 5>) ? sizeof(BandFwdStage<RB, NW, R>)
+                                                                                     : sizeof(BandBwdStage<RB, NW, R, 5>));
 }
 
-template <int RB, int NW, int R, int ST>
+// NOPIV: no pivot was taken in the factorisation (PlanDev::band_nopiv): pivots are not
+// read and U rows are {1/U_jj, U_j,j+1, U_j,j+2} (UE = 3 instead of 5).
+template <int RB, int NW, int R, int ST, bool NOPIV>
 __global__ void __launch_bounds__(BW* NW) band_solve_kernel(const double2* __restrict__ in, double2* __restrict__ out,
                                                             const int* __restrict__ piv,
                                                             const double2* __restrict__ L,
@@ -83,7 +85,7 @@ __global__ void __launch_bounds__(BW* NW) band_solve_kernel(const double2* __res
       const size_t f = (size_t)(j < m0 ? j : 0) * m0 + (va ? a : 0);
       cp_async16(&S.L[rr][t][0], L + 2 * f, ok);
       cp_async16(&S.L[rr][t][1], L + 2 * f + 1, ok);
-      cp_async4(&S.piv[rr][t], piv + f, ok);
+      if (!NOPIV) cp_async4(&S.piv[rr][t], piv + f, ok);
     }
     // this warp's right-hand-side rows (the forward sweep consumes row j+3 at step j)
     for (int rr = 0; rr < R; ++rr) {
@@ -141,7 +143,7 @@ __global__ void __launch_bounds__(BW* NW) band_solve_kernel(const double2* __res
     const int rows = min(R, m0 - c * R);
     for (int rr = 0; rr < rows; ++rr) {
       const int j = c * R + rr;
-      const int pv = S.piv[rr][t];
+      const int pv = NOPIV ? 0 : S.piv[rr][t];
       const double2 l0 = S.L[rr][t][0], l1 = S.L[rr][t][1];
 #pragma unroll
       for (int r = 0; r < RB; ++r) {
@@ -164,16 +166,17 @@ __global__ void __launch_bounds__(BW* NW) band_solve_kernel(const double2* __res
   __threadfence();  // the backward sweep re-reads `out` through cp.async
 
   // ---------------- backward substitution ----------------
-  using BS = BandBwdStage<RB, NW, R>;
+  constexpr int UE = NOPIV ? 3 : 5;
+  using BS = BandBwdStage<RB, NW, R, UE>;
   BS* bs = reinterpret_cast<BS*>(sraw);
   auto issue_bwd = [&](int c) {
     BS& S = bs[c % ST];
     for (int rr = w; rr < R; rr += NW) {
       const int j = m0 - 1 - (c * R + rr);
       const bool ok = va && j >= 0;
-      const double2* u = U + 5 * ((size_t)(j >= 0 ? j : 0) * m0 + (va ? a : 0));
+      const double2* u = U + UE * ((size_t)(j >= 0 ? j : 0) * m0 + (va ? a : 0));
 #pragma unroll
-      for (int e = 0; e < 5; ++e) cp_async16(&S.U[rr][t][e], u + e, ok);
+      for (int e = 0; e < UE; ++e) cp_async16(&S.U[rr][t][e], u + e, ok);
     }
     for (int rr = 0; rr < R; ++rr) {
       const int j = m0 - 1 - (c * R + rr);
@@ -217,15 +220,16 @@ __global__ void __launch_bounds__(BW* NW) band_solve_kernel(const double2* __res
     for (int rr = 0; rr < R; ++rr) {
       if (rr >= rows) break;
       const int j = m0 - 1 - (c * R + rr);
-      const double2 u0 = S.U[rr][t][0], u1 = S.U[rr][t][1], u2 = S.U[rr][t][2], u3 = S.U[rr][t][3],
-                    u4 = S.U[rr][t][4];
+      const double2 u0 = S.U[rr][t][0], u1 = S.U[rr][t][1], u2 = S.U[rr][t][2];
 #pragma unroll
       for (int r = 0; r < RB; ++r) {
         double2 v = S.v[w][r][rr][t];
         v = fms_(u1, y1[r], v);
         v = fms_(u2, y2[r], v);
-        v = fms_(u3, y3[r], v);
-        v = fms_(u4, y4[r], v);
+        if constexpr (!NOPIV) {
+          v = fms_(S.U[rr][t][UE - 2], y3[r], v);
+          v = fms_(S.U[rr][t][UE - 1], y4[r], v);
+        }
         v = mul(v, u0);
         if (va && b0 + r < batch)
           out[(size_t)(b0 + r) * N0 + (size_t)j * m0 + a] = add ? ::helm::add(v, acur[r][rr]) : v;
@@ -245,23 +249,32 @@ __global__ void __launch_bounds__(BW* NW) band_solve_kernel(const double2* __res
   cp_wait<0>();
 }
 
-template <int RB, int NW, int R, int ST>
-static void band_launch(const helm_plan* P, const double2* in, double2* out, const double2* corr, int batch,
-                        cudaStream_t st, const double2* add) {
+template <int RB, int NW, int R, int ST, bool NOPIV>
+static void band_launch_k(const helm_plan* P, const double2* in, double2* out, const double2* corr, int batch,
+                          cudaStream_t st, const double2* add) {
   const PlanDev& d = P->dev;
   constexpr size_t smem = band_smem_bytes<RB, NW, R, ST>();
   static_assert(smem <= 227 * 1024, "band-solve stages exceed shared memory");
   static bool attr = false;
   if (!attr) {
-    HELM_CUDA(cudaFuncSetAttribute(band_solve_kernel<RB, NW, R, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)smem));
+    HELM_CUDA(cudaFuncSetAttribute(band_solve_kernel<RB, NW, R, ST, NOPIV>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr = true;
   }
   dim3 grd((d.m0 + BW - 1) / BW, (batch + RB * NW - 1) / (RB * NW));
-  band_solve_kernel<RB, NW, R, ST><<<grd, BW * NW, smem, st>>>(in, out, d.band_piv, (const double2*)d.band_l,
-                                                               (const double2*)d.band_u, d.m0, batch, corr,
-                                                               d.strip_q, d.coarse_scale, batch * 4, add);
+  band_solve_kernel<RB, NW, R, ST, NOPIV><<<grd, BW * NW, smem, st>>>(
+      in, out, d.band_piv, (const double2*)d.band_l, (const double2*)d.band_u, d.m0, batch, corr, d.strip_q,
+      d.coarse_scale, batch * 4, add);
   HELM_LAUNCH_CHECK();
+}
+
+template <int RB, int NW, int R, int ST>
+static void band_launch(const helm_plan* P, const double2* in, double2* out, const double2* corr, int batch,
+                        cudaStream_t st, const double2* add) {
+  if (P->dev.band_nopiv)
+    band_launch_k<RB, NW, R, ST, true>(P, in, out, corr, batch, st, add);
+  else
+    band_launch_k<RB, NW, R, ST, false>(P, in, out, corr, batch, st, add);
 }
 
 // batches up to this size use the segmented solve (HELM_BAND_SEG_MAX overrides; 0 disables)
@@ -269,6 +282,14 @@ static int band_seg_max_batch() {
   static int v = [] {
     const char* e = std::getenv("HELM_BAND_SEG_MAX");
     return e ? std::atoi(e) : 4;
+  }();
+  return v;
+}
+
+static int band_cfg() {
+  static int v = [] {
+    const char* e = std::getenv("HELM_BAND_CFG");
+    return e ? std::atoi(e) : 0;
   }();
   return v;
 }
@@ -285,8 +306,19 @@ void launch_band_solve(const helm_plan* P, const double2* in, double2* out, cons
     band_launch<1, 1, 8, 4>(P, in, out, corr, batch, st, add);  // latency-bound recurrence
   else if (batch <= 4)
     band_launch<2, 2, 8, 3>(P, in, out, corr, batch, st, add);
-  else
-    band_launch<1, 8, 8, 3>(P, in, out, corr, batch, st, add);  // 8 warps (8 right-hand sides) share each factor read
+  else {
+    switch (band_cfg()) {
+      case 1: band_launch<1, 4, 8, 3>(P, in, out, corr, batch, st, add); break;
+      case 2: band_launch<2, 4, 8, 3>(P, in, out, corr, batch, st, add); break;
+      case 3: band_launch<1, 2, 8, 4>(P, in, out, corr, batch, st, add); break;
+      case 4: band_launch<2, 2, 8, 3>(P, in, out, corr, batch, st, add); break;
+      case 5: band_launch<4, 2, 8, 3>(P, in, out, corr, batch, st, add); break;
+      case 6: band_launch<2, 8, 4, 3>(P, in, out, corr, batch, st, add); break;
+      case 7: band_launch<1, 16, 4, 3>(P, in, out, corr, batch, st, add); break;
+      case 8: band_launch<1, 16, 8, 2>(P, in, out, corr, batch, st, add); break;
+      default: band_launch<1, 8, 8, 3>(P, in, out, corr, batch, st, add);  // 8 warps (8 right-hand sides) share each factor read
+    }
+  }
 }
 
 }  // namespace helm

@@ -21,6 +21,9 @@
 // Exact in exact arithmetic (the same linear recurrence, associated differently); 1025-row
 // modes become 32-row segments, so the dependent chain is ~130 steps instead of ~2050.
 // Right-hand side handling (in, corr/q/sig, add) is the same contract as band_solve_kernel.
+#include <cstdlib>
+#include <type_traits>
+
 #include "ops.cuh"
 
 namespace helm {
@@ -28,6 +31,7 @@ namespace helm {
 constexpr int SEG = 32;  // segments per mode
 constexpr int SMB = 8;   // modes per CTA (8 consecutive modes = one 128-byte row segment)
 constexpr int SEG_THREADS = SEG * SMB;
+
 
 struct SegRhs {
   const double2* in;
@@ -74,13 +78,14 @@ __device__ __forceinline__ void fwd_step(int pv, double2 l0, double2 l1, double2
   r1 = x2;
 }
 
-// forward pass over rows [j0, j1) with state (r0, r1); writes eliminated rows to sm (if non-null)
-template <bool STORE>
+// forward pass over rows [j0, j1) with state (r0, r1); writes eliminated rows to sm (if non-null).
+// NOPIV: no pivot was taken in the factorisation (pivots not read, U rows of 3 entries).
+template <bool STORE, bool NOPIV, int CF = 4>
 __device__ __forceinline__ void fwd_run(const SegRhs& rhs, const int* __restrict__ piv, const double2* __restrict__ L,
                                         int m0, int a, int j0, int j1, double2& r0, double2& r1, double2* sm,
                                         int sm_stride) {
   // chunks of C rows, the next chunk's loads in flight while the current one is consumed
-  constexpr int C = 4;
+  constexpr int C = CF;
   struct Chunk {
     int pv[C];
     double2 l0[C], l1[C], f[C];
@@ -90,7 +95,7 @@ __device__ __forceinline__ void fwd_run(const SegRhs& rhs, const int* __restrict
     for (int c = 0; c < C; ++c) {
       const bool ok = j + c < j1;
       const size_t e = (size_t)(ok ? j + c : j0) * m0 + a;
-      ch.pv[c] = __ldg(piv + e);
+      ch.pv[c] = NOPIV ? 0 : __ldg(piv + e);
       ch.l0[c] = __ldg(L + 2 * e);
       ch.l1[c] = __ldg(L + 2 * e + 1);
       ch.f[c] = ok ? rhs(j + c + 2) : mk(0.0, 0.0);
@@ -116,22 +121,23 @@ __device__ __forceinline__ void fwd_run(const SegRhs& rhs, const int* __restrict
 // backward pass over rows [j0, j1) (descending) with state y; sm: eliminated rows (null:
 // zero); with out != null every solution row is stored (+ add[row] when add != null).  U and
 // the summands of the next chunk are in flight while the current chunk is consumed.
+template <bool NOPIV, int CB = 4>
 __device__ __forceinline__ void bwd_run(const double2* __restrict__ U, int m0, int a, int j0, int j1,
                                         double2 (&y)[4], const double2* sm, int sm_stride,
                                         double2* __restrict__ out = nullptr,
                                         const double2* __restrict__ addp = nullptr, bool store = false) {
-  constexpr int C = 4;
+  constexpr int C = CB, UE = NOPIV ? 3 : 5;
   struct Chunk {
-    double2 u[C][5];
+    double2 u[C][UE];
     double2 ad[C];
   };
   auto load = [&](int j, Chunk& ch) {  // rows j, j-1, .., j-C+1
 #pragma unroll
     for (int c = 0; c < C; ++c) {
       const int r = j - c >= j0 ? j - c : j1 - 1;
-      const double2* u = U + 5 * ((size_t)r * m0 + a);
+      const double2* u = U + UE * ((size_t)r * m0 + a);
 #pragma unroll
-      for (int e = 0; e < 5; ++e) ch.u[c][e] = __ldg(u + e);
+      for (int e = 0; e < UE; ++e) ch.u[c][e] = __ldg(u + e);
       ch.ad[c] = addp ? __ldg(addp + (size_t)r * m0) : mk(0.0, 0.0);
     }
   };
@@ -147,8 +153,10 @@ __device__ __forceinline__ void bwd_run(const double2* __restrict__ U, int m0, i
         double2 v = sm ? sm[(r - j0) * sm_stride] : mk(0.0, 0.0);
         v = fms_(cur.u[c][1], y[0], v);
         v = fms_(cur.u[c][2], y[1], v);
-        v = fms_(cur.u[c][3], y[2], v);
-        v = fms_(cur.u[c][4], y[3], v);
+        if constexpr (!NOPIV) {
+          v = fms_(cur.u[c][UE - 2], y[2], v);
+          v = fms_(cur.u[c][UE - 1], y[3], v);
+        }
         v = mul(v, cur.u[c][0]);
         y[3] = y[2];
         y[2] = y[1];
@@ -162,6 +170,7 @@ __device__ __forceinline__ void bwd_run(const double2* __restrict__ U, int m0, i
 }
 
 // Phi [SEG][4][m0], Psi [SEG][16][m0]: exit state of segment k for unit entry states
+template <bool NOPIV>
 __global__ void band_seg_setup_kernel(const int* __restrict__ piv, const double2* __restrict__ L,
                                       const double2* __restrict__ U, int m0, int ls, double2* __restrict__ phi,
                                       double2* __restrict__ psi) {
@@ -172,18 +181,21 @@ __global__ void band_seg_setup_kernel(const int* __restrict__ piv, const double2
   SegRhs zero{nullptr, nullptr, 0, 0, {0, 0, 0, 0}, 0.0, 0, m0};
   for (int c = 0; c < 2; ++c) {
     double2 r0 = mk(c == 0 ? 1.0 : 0.0, 0.0), r1 = mk(c == 1 ? 1.0 : 0.0, 0.0);
-    fwd_run<false>(zero, piv, L, m0, a, j0, j1, r0, r1, nullptr, 0);
+    fwd_run<false, NOPIV>(zero, piv, L, m0, a, j0, j1, r0, r1, nullptr, 0);
     phi[((size_t)k * 4 + 0 * 2 + c) * m0 + a] = r0;
     phi[((size_t)k * 4 + 1 * 2 + c) * m0 + a] = r1;
   }
   for (int c = 0; c < 4; ++c) {
     double2 y[4];
     for (int i = 0; i < 4; ++i) y[i] = mk(i == c ? 1.0 : 0.0, 0.0);
-    bwd_run(U, m0, a, j0, j1, y, nullptr, 0);
+    bwd_run<NOPIV>(U, m0, a, j0, j1, y, nullptr, 0);
     for (int r = 0; r < 4; ++r) psi[((size_t)k * 16 + r * 4 + c) * m0 + a] = y[r];
   }
 }
 
+// CF / CB: rows per prefetch chunk of the forward / backward sweeps (the next chunk's
+// loads are in flight while the current one is consumed)
+template <bool NOPIV, int CF, int CB>
 __global__ void __launch_bounds__(SEG_THREADS) band_seg_kernel(
     const double2* __restrict__ in, double2* __restrict__ out, const int* __restrict__ piv,
     const double2* __restrict__ L, const double2* __restrict__ U, const double2* __restrict__ phi,
@@ -215,7 +227,7 @@ __global__ void __launch_bounds__(SEG_THREADS) band_seg_kernel(
     r0 = rhs(0);
     r1 = rhs(1);
   }
-  fwd_run<false>(rhs, piv, L, m0, ac, j0, j1, r0, r1, nullptr, 0);
+  fwd_run<false, NOPIV, CF>(rhs, piv, L, m0, ac, j0, j1, r0, r1, nullptr, 0);
   fst[k + 1][al][0] = r0;
   fst[k + 1][al][1] = r1;
   __syncthreads();
@@ -261,12 +273,12 @@ __global__ void __launch_bounds__(SEG_THREADS) band_seg_kernel(
     r0 = fst[k][al][0];
     r1 = fst[k][al][1];
   }
-  fwd_run<true>(rhs, piv, L, m0, ac, j0, j1, r0, r1, mysm, sstride);
+  fwd_run<true, NOPIV, CF>(rhs, piv, L, m0, ac, j0, j1, r0, r1, mysm, sstride);
   // B1: zero-state backward pass
   double2 y[4];
 #pragma unroll
   for (int i = 0; i < 4; ++i) y[i] = mk(0.0, 0.0);
-  bwd_run(U, m0, ac, j0, j1, y, mysm, sstride);
+  bwd_run<NOPIV, CB>(U, m0, ac, j0, j1, y, mysm, sstride);
 #pragma unroll
   for (int i = 0; i < 4; ++i) bst[k][al][i] = y[i];
   __syncthreads();
@@ -319,7 +331,7 @@ __global__ void __launch_bounds__(SEG_THREADS) band_seg_kernel(
   // B3: true backward pass
 #pragma unroll
   for (int i = 0; i < 4; ++i) y[i] = k == SEG - 1 ? mk(0.0, 0.0) : bst[k + 2][al][i];
-  bwd_run(U, m0, ac, j0, j1, y, mysm, sstride, out + (size_t)b * N0 + ac,
+  bwd_run<NOPIV, CB>(U, m0, ac, j0, j1, y, mysm, sstride, out + (size_t)b * N0 + ac,
           addv ? addv + (size_t)b * N0 + ac : nullptr, va);
 }
 
@@ -333,8 +345,12 @@ void band_seg_setup(const PlanDev& d, double2* tables, cudaStream_t st) {
   const int m0 = d.m0;
   double2* phi = tables;
   double2* psi = tables + (size_t)SEG * 4 * m0;
-  band_seg_setup_kernel<<<dim3((m0 + 127) / 128, SEG), 128, 0, st>>>(
-      d.band_piv, (const double2*)d.band_l, (const double2*)d.band_u, m0, seg_len(m0), phi, psi);
+  auto go = [&](auto np) {
+    band_seg_setup_kernel<decltype(np)::value><<<dim3((m0 + 127) / 128, SEG), 128, 0, st>>>(
+        d.band_piv, (const double2*)d.band_l, (const double2*)d.band_u, m0, seg_len(m0), phi, psi);
+  };
+  if (d.band_nopiv) go(std::true_type{});
+  else go(std::false_type{});
   HELM_LAUNCH_CHECK();
 }
 
@@ -343,15 +359,18 @@ void band_seg_launch(const helm_plan* P, const double2* in, double2* out, const 
   const PlanDev& d = P->dev;
   const int m0 = d.m0, ls = seg_len(m0);
   const size_t smem = (size_t)ls * SEG * SMB * sizeof(double2);
-  static bool attr = false;
-  if (!attr) {
-    HELM_CUDA(cudaFuncSetAttribute(band_seg_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    attr = true;
-  }
-  HELM_CHECK(smem <= 200 * 1024, "segmented band solve: segment too long");
   const double2* phi = d.band_seg;
   const double2* psi = d.band_seg + (size_t)SEG * 4 * m0;
-  band_seg_kernel<<<dim3((m0 + SMB - 1) / SMB, batch), SEG_THREADS, smem, st>>>(
+  HELM_CHECK(smem <= 200 * 1024, "segmented band solve: segment too long");
+  static bool attr = false;
+  if (!attr) {
+    for (auto k : {band_seg_kernel<false, 4, 4>, band_seg_kernel<true, 4, 4>})
+      HELM_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    attr = true;
+  }
+  // deeper prefetch chunks (8 / 6 rows) were measured slower at batch 1 (register-bound)
+  (d.band_nopiv ? band_seg_kernel<true, 4, 4> : band_seg_kernel<false, 4, 4>)<<<dim3((m0 + SMB - 1) / SMB, batch),
+                                                                              SEG_THREADS, smem, st>>>(
       in, out, d.band_piv, (const double2*)d.band_l, (const double2*)d.band_u, phi, psi, m0, ls, corr, d.strip_q,
       d.coarse_scale, batch * 4, add);
   HELM_LAUNCH_CHECK();

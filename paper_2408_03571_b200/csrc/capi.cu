@@ -40,6 +40,12 @@ static T* upload(const void* host, size_t count) {
   HELM_CUDA(cudaMemcpy(d, host, count * sizeof(T), cudaMemcpyHostToDevice));
   return d;
 }
+// HELM_<name>=0 switches a fast path off (development A/B and tests)
+static bool env_flag_off(const char* name) {
+  const char* e = std::getenv(name);
+  return e && e[0] == '0';
+}
+
 static void* upload_bytes(const void* host, size_t bytes) {
   if (bytes == 0) return nullptr;
   HELM_CHECK(host != nullptr, "missing setup array in helm_desc");
@@ -302,8 +308,28 @@ static void build_plan(const helm_desc* d, helm_plan* P) {
       HELM_CHECK(d->band_piv && d->band_l && d->band_u, "Sommerfeld coarse solver needs the band factors");
       std::vector<int> piv32(d->band_piv, d->band_piv + m0 * m0);
       dv.band_piv = upload<int>(piv32.data(), piv32.size());
-      dv.band_l = upload_bytes(d->band_l, m0 * m0 * 2 * P->elem);
-      dv.band_u = upload_bytes(d->band_u, m0 * m0 * 5 * P->elem);
+      // no pivot taken (and hence no fill in U): rows {1/U_jj, U_j,j+1, U_j,j+2} only
+      const size_t mm = (size_t)m0 * m0;
+      const double2* uh = static_cast<const double2*>(d->band_u);
+      bool nopiv = P->elem == sizeof(double2) && !env_flag_off("HELM_BAND_NOPIV");
+      for (size_t e = 0; nopiv && e < mm; ++e)
+        nopiv = d->band_piv[e] == 0 && uh[5 * e + 3].x == 0.0 && uh[5 * e + 3].y == 0.0 && uh[5 * e + 4].x == 0.0 &&
+                uh[5 * e + 4].y == 0.0;
+      const int ue = nopiv ? 3 : 5;
+      dv.band_nopiv = nopiv ? 1 : 0;
+      dv.band_fac_bytes = mm * (2 + ue) * P->elem;
+      HELM_CUDA(cudaMalloc(&dv.band_fac, dv.band_fac_bytes));
+      dv.band_l = dv.band_fac;
+      dv.band_u = static_cast<char*>(dv.band_fac) + mm * 2 * P->elem;
+      HELM_CUDA(cudaMemcpy(dv.band_l, d->band_l, mm * 2 * P->elem, cudaMemcpyHostToDevice));
+      if (nopiv) {
+        std::vector<double2> uc(mm * 3);
+        for (size_t e = 0; e < mm; ++e)
+          for (int i = 0; i < 3; ++i) uc[3 * e + i] = uh[5 * e + i];
+        HELM_CUDA(cudaMemcpy(dv.band_u, uc.data(), mm * 3 * sizeof(double2), cudaMemcpyHostToDevice));
+      } else {
+        HELM_CUDA(cudaMemcpy(dv.band_u, d->band_u, mm * 5 * P->elem, cudaMemcpyHostToDevice));
+      }
       if (band_seg_usable(m0)) {
         HELM_CUDA(cudaMalloc(&dv.band_seg, band_seg_table_elems(m0) * sizeof(double2)));
         band_seg_setup(dv, dv.band_seg, 0);
@@ -483,7 +509,7 @@ static void free_plan(helm_plan* P) {
   void* ptrs[] = {dv.box_start, dv.box_len, dv.box_class, dv.class_len, dv.class_off_V, dv.class_off_lam,
                   dv.class_V, dv.class_lambda, dv.class_real, dv.class_Vr, dv.box_ff, dv.class_Vf, dv.class_lamf, dv.class_invden, dv.box_rr, dv.box_mix,
                   dv.node_first_box, dv.node_mult, dv.node_band, dv.band_node,
-                  dv.coarse_scale, dv.twiddle, dv.coarse_lamT, dv.coarse_lamM, dv.t0_band, dv.m0_band, dv.band_piv, dv.band_l, dv.band_u, dv.band_seg, dv.strip_q,
+                  dv.coarse_scale, dv.twiddle, dv.coarse_lamT, dv.coarse_lamM, dv.t0_band, dv.m0_band, dv.band_piv, dv.band_fac, dv.band_seg, dv.strip_q,
                   dv.cap_left, dv.cap_right, dv.cap_mode, dv.cap_vt, dv.cap_hg};
   for (void* q : ptrs)
     if (q) cudaFree(q);

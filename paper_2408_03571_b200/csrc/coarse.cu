@@ -34,6 +34,7 @@ namespace helm {
 // Woodbury strip step
 // ----------------------------------------------------------------------------
 // Z[y][b*4+i] = sum_a q[a][i] Yh[b][y][a]   (one warp per (batch, row))
+constexpr int SCH = 16;  // row elements per lane in flight (strip kernels)
 template <typename S>
 __global__ void __launch_bounds__(256) strip_reduce_kernel(const S* __restrict__ Yh, const double* __restrict__ q,
                                                            S* __restrict__ Z, int m0, int ldz) {
@@ -43,18 +44,94 @@ __global__ void __launch_bounds__(256) strip_reduce_kernel(const S* __restrict__
   if (y >= m0) return;
   const S* row = Yh + ((size_t)b * m0 + y) * m0;
   S acc[4] = {Sc<S>::zero(), Sc<S>::zero(), Sc<S>::zero(), Sc<S>::zero()};
-#pragma unroll 8
-  for (int a = lane; a < m0; a += 32) {
-    const S v = row[a];
-    const double4 qa = *reinterpret_cast<const double4*>(q + (size_t)a * 4);
-    acc[0] = fma_(qa.x, v, acc[0]);
-    acc[1] = fma_(qa.y, v, acc[1]);
-    acc[2] = fma_(qa.z, v, acc[2]);
-    acc[3] = fma_(qa.w, v, acc[3]);
+  // chunks of SCH elements per lane are loaded before they are summed (all loads of a
+  // chunk in flight); the summation order per lane is a = lane, lane + 32, ... as before
+  for (int a0 = lane; a0 < m0; a0 += 32 * SCH) {
+    S v[SCH];
+    double4 qv[SCH];
+#pragma unroll
+    for (int i = 0; i < SCH; ++i) {
+      const int a = a0 + 32 * i;
+      if (a < m0) {
+        v[i] = row[a];
+        qv[i] = *reinterpret_cast<const double4*>(q + (size_t)a * 4);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < SCH; ++i) {
+      if (a0 + 32 * i < m0) {
+        acc[0] = fma_(qv[i].x, v[i], acc[0]);
+        acc[1] = fma_(qv[i].y, v[i], acc[1]);
+        acc[2] = fma_(qv[i].z, v[i], acc[2]);
+        acc[3] = fma_(qv[i].w, v[i], acc[3]);
+      }
+    }
   }
 #pragma unroll
   for (int i = 0; i < 4; ++i) acc[i] = warp_sum(acc[i]);
   if (lane < 4) Z[(size_t)y * ldz + (size_t)b * 4 + lane] = acc[lane];
+}
+
+// Small batches: the same strip values with compensated sums (csum_*), each row split over
+// WPR warps (lanes stride the row by 32 * WPR, warp partials merged in warp order).
+template <int WPR>
+__global__ void __launch_bounds__(256) strip_reduce_c_kernel(const double2* __restrict__ Yh,
+                                                             const double* __restrict__ q, double2* __restrict__ Z,
+                                                             int m0, int ldz) {
+  __shared__ CSum red[8][8];
+  const int wl = threadIdx.x >> 5, lane = threadIdx.x & 31, sw = wl % WPR;
+  const int yy = (blockIdx.x * blockDim.x + threadIdx.x) / (32 * WPR);
+  const int b = blockIdx.y;
+  const bool ok = yy < m0;
+  const double2* row = Yh + ((size_t)b * m0 + (ok ? yy : 0)) * m0;
+  CSum acc[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) acc[i] = CSum{0.0, 0.0};
+#pragma unroll 4
+  for (int a = sw * 32 + lane; a < (ok ? m0 : 0); a += 32 * WPR) {
+    const double2 v = row[a];
+    const double4 qa = *reinterpret_cast<const double4*>(q + (size_t)a * 4);
+    csum_fma(acc[0], qa.x, v.x);
+    csum_fma(acc[1], qa.x, v.y);
+    csum_fma(acc[2], qa.y, v.x);
+    csum_fma(acc[3], qa.y, v.y);
+    csum_fma(acc[4], qa.z, v.x);
+    csum_fma(acc[5], qa.z, v.y);
+    csum_fma(acc[6], qa.w, v.x);
+    csum_fma(acc[7], qa.w, v.y);
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) warp_csum(acc[i]);
+  if (lane == 0) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) red[wl][i] = acc[i];
+  }
+  __syncthreads();
+  if (ok && sw == 0 && lane < 4) {
+    CSum re = red[wl][2 * lane], im = red[wl][2 * lane + 1];
+#pragma unroll
+    for (int w = 1; w < WPR; ++w) {
+      csum_merge(re, red[wl + w][2 * lane]);
+      csum_merge(im, red[wl + w][2 * lane + 1]);
+    }
+    Z[(size_t)yy * ldz + (size_t)b * 4 + lane] = mk(csum_val(re), csum_val(im));
+  }
+}
+
+template <typename S>
+static void strip_reduce(const S* Yh, const double* q, S* Z, int m0, int batch, cudaStream_t st) {
+  if constexpr (Sc<S>::cplx) {
+    if (batch <= 4) {
+      constexpr int WPR = 4;
+      dim3 grd((unsigned)((m0 * 32 * WPR + 255) / 256), batch);
+      strip_reduce_c_kernel<WPR><<<grd, 256, 0, st>>>(Yh, q, Z, m0, batch * 4);
+      HELM_LAUNCH_CHECK();
+      return;
+    }
+  }
+  dim3 grd((unsigned)((m0 * 32 + 255) / 256), batch);
+  strip_reduce_kernel<S><<<grd, 256, 0, st>>>(Yh, q, Z, m0, batch * 4);
+  HELM_LAUNCH_CHECK();
 }
 
 // --- strip GEMMs on the folded (even / odd) mode blocks ------------------------
@@ -250,26 +327,62 @@ __global__ void __launch_bounds__(256) strip_reduce_right_kernel(const double2* 
   }
 }
 
-// Small batches (<= 4 right-hand sides, NC = 4 * batch strip columns): one warp per output
-// row, the fold / unfold and the 4x4 epilogue fused into the product (one launch per side).
+// Small batches (<= 4 right-hand sides, NC = 4 * batch strip columns): WPR warps per output
+// row (lanes stride the row by 32 * WPR), compensated sums (csum_*: the result does not
+// depend on that split at the rounding level), the fold / unfold and the 4x4 epilogue fused
+// into the product (one launch per side).
+// Cross-warp total of the row's per-warp sums, merged in warp order; the totals land in
+// the row's first warp.  All threads of the CTA call it.
+template <int NC, int WPR>
+__device__ __forceinline__ void row_total_c(CSum (&re)[NC], CSum (&im)[NC], int wl, int lane, double2 (&acc)[NC]) {
+  if constexpr (WPR == 1) {
+#pragma unroll
+    for (int c = 0; c < NC; ++c) acc[c] = mk(csum_val(re[c]), csum_val(im[c]));
+  } else {
+    __shared__ CSum red[8][NC][2];
+    if (lane == 0) {
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+        red[wl][c][0] = re[c];
+        red[wl][c][1] = im[c];
+      }
+    }
+    __syncthreads();
+    if (wl % WPR == 0) {
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+        CSum r = red[wl][c][0], i = red[wl][c][1];
+#pragma unroll
+        for (int w = 1; w < WPR; ++w) {
+          csum_merge(r, red[wl + w][c][0]);
+          csum_merge(i, red[wl + w][c][1]);
+        }
+        acc[c] = mk(csum_val(r), csum_val(i));
+      }
+    }
+    __syncthreads();  // the shared partials may be reused by the next call
+  }
+}
+
 // left:  row r of the packed mode blocks, t = A_g[r] . fold(Z), out[r] = Hm[r] t  (Hm may be null)
-template <int NC>
+template <int NC, int WPR>
 __global__ void __launch_bounds__(256) strip_left_fused_kernel(const double2* __restrict__ A,
                                                                const double2* __restrict__ Z,
                                                                double2* __restrict__ out,
                                                                const double2* __restrict__ Hm, int m0) {
-  const int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (r >= m0) return;
+  const int wl = threadIdx.x >> 5, lane = threadIdx.x & 31, sw = wl % WPR;
+  const int rr = (blockIdx.x * blockDim.x + threadIdx.x) / (32 * WPR);
+  const bool ok = rr < m0;
+  const int r = ok ? rr : m0 - 1;
   const int he = (m0 + 1) / 2, ho = m0 / 2;
   const bool odd = r >= he;
   const int Mg = odd ? ho : he;
   const double2* arow = A + (odd ? (size_t)he * he + (size_t)(r - he) * ho : (size_t)r * he);
-  double2 acc[NC];
+  CSum re[NC], im[NC];
 #pragma unroll
-  for (int c = 0; c < NC; ++c) acc[c] = mk(0.0, 0.0);
-#pragma unroll 8
-  for (int k = lane; k < Mg; k += 32) {
+  for (int c = 0; c < NC; ++c) re[c] = im[c] = CSum{0.0, 0.0};
+#pragma unroll(NC <= 8 ? 4 : 1)
+  for (int k = sw * 32 + lane; k < (ok ? Mg : 0); k += 32 * WPR) {
     const double2 av = arow[k];
     const double2* z0 = Z + (size_t)k * NC;
     const double2* z1 = Z + (size_t)(m0 - 1 - k) * NC;
@@ -278,12 +391,17 @@ __global__ void __launch_bounds__(256) strip_left_fused_kernel(const double2* __
     for (int c = 0; c < NC; ++c) {
       const double2 a = z0[c];
       const double2 f = centre ? a : (odd ? sub(a, z1[c]) : add(a, z1[c]));
-      acc[c] = fma_(av, f, acc[c]);
+      csum_cfma(re[c], im[c], av, f);
     }
   }
 #pragma unroll
-  for (int c = 0; c < NC; ++c) acc[c] = warp_sum(acc[c]);
-  if (lane < NC) {
+  for (int c = 0; c < NC; ++c) {
+    warp_csum(re[c]);
+    warp_csum(im[c]);
+  }
+  double2 acc[NC];
+  row_total_c<NC, WPR>(re, im, wl, lane, acc);
+  if (ok && sw == 0 && lane < NC) {
     const int g = lane >> 2, i = lane & 3;
     double2 v;
     if (Hm) {
@@ -309,40 +427,46 @@ __global__ void __launch_bounds__(256) strip_left_fused_kernel(const double2* __
 
 // right: for y < he, E = A_e[y] . cin[0:he), O = A_o[y] . cin[he:m0) (y < ho);
 // out[y] = E + O (- minus[y]), out[m0-1-y] = E - O (- minus[m0-1-y]), out[centre] = E
-template <int NC>
+template <int NC, int WPR>
 __global__ void __launch_bounds__(256) strip_right_fused_kernel(const double2* __restrict__ A,
                                                                 const double2* __restrict__ cin,
                                                                 double2* __restrict__ out,
                                                                 const double2* __restrict__ minus, int m0) {
-  const int y = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
+  const int wl = threadIdx.x >> 5, lane = threadIdx.x & 31, sw = wl % WPR;
+  const int yy = (blockIdx.x * blockDim.x + threadIdx.x) / (32 * WPR);
   const int he = (m0 + 1) / 2, ho = m0 / 2;
-  if (y >= he) return;
+  const bool ok = yy < he;
+  const int y = ok ? yy : he - 1;
   const double2* ae = A + (size_t)y * he;
-  double2 E[NC], O[NC];
+  const double2* ao = A + (size_t)he * he + (size_t)y * ho;
+  CSum er[NC], ei[NC], orr[NC], oi[NC];
 #pragma unroll
-  for (int c = 0; c < NC; ++c) E[c] = O[c] = mk(0.0, 0.0);
-#pragma unroll 8
-  for (int k = lane; k < he; k += 32) {
+  for (int c = 0; c < NC; ++c) er[c] = ei[c] = orr[c] = oi[c] = CSum{0.0, 0.0};
+#pragma unroll(NC <= 8 ? 4 : 1)
+  for (int k = sw * 32 + lane; k < (ok ? he : 0); k += 32 * WPR) {
     const double2 av = ae[k];
 #pragma unroll
-    for (int c = 0; c < NC; ++c) E[c] = fma_(av, cin[(size_t)k * NC + c], E[c]);
+    for (int c = 0; c < NC; ++c) csum_cfma(er[c], ei[c], av, cin[(size_t)k * NC + c]);
   }
   if (y < ho) {
-    const double2* ao = A + (size_t)he * he + (size_t)y * ho;
-#pragma unroll 8
-    for (int k = lane; k < ho; k += 32) {
+#pragma unroll(NC <= 8 ? 4 : 1)
+    for (int k = sw * 32 + lane; k < (ok ? ho : 0); k += 32 * WPR) {
       const double2 av = ao[k];
 #pragma unroll
-      for (int c = 0; c < NC; ++c) O[c] = fma_(av, cin[(size_t)(he + k) * NC + c], O[c]);
+      for (int c = 0; c < NC; ++c) csum_cfma(orr[c], oi[c], av, cin[(size_t)(he + k) * NC + c]);
     }
   }
 #pragma unroll
   for (int c = 0; c < NC; ++c) {
-    E[c] = warp_sum(E[c]);
-    O[c] = warp_sum(O[c]);
+    warp_csum(er[c]);
+    warp_csum(ei[c]);
+    warp_csum(orr[c]);
+    warp_csum(oi[c]);
   }
-  if (lane < NC) {
+  double2 E[NC], O[NC];
+  row_total_c<NC, WPR>(er, ei, wl, lane, E);
+  row_total_c<NC, WPR>(orr, oi, wl, lane, O);
+  if (ok && sw == 0 && lane < NC) {
     double2 e = E[0], o = O[0];
 #pragma unroll
     for (int c = 1; c < NC; ++c)
@@ -371,13 +495,14 @@ static void strip_gemm_fold(const double2* A, const double2* Zin, double2* out, 
                             const double2* minus, int m0, int batch, double2* Zf, double2* part, cudaStream_t st) {
   const int ldn = 4 * batch, he = (m0 + 1) / 2, ho = m0 / 2;
   if (batch <= 4) {
-    const int blocks_l = (m0 * 32 + 255) / 256, blocks_r = (he * 32 + 255) / 256;
     auto go = [&](auto nc) {
       constexpr int NC = decltype(nc)::value;
+      constexpr int WPR = NC <= 8 ? 4 : 2;  // few rows: each split over WPR warps
+      const int blocks_l = (m0 * 32 * WPR + 255) / 256, blocks_r = (he * 32 * WPR + 255) / 256;
       if (left)
-        strip_left_fused_kernel<NC><<<blocks_l, 256, 0, st>>>(A, Zin, out, Hm, m0);
+        strip_left_fused_kernel<NC, WPR><<<blocks_l, 256, 0, st>>>(A, Zin, out, Hm, m0);
       else
-        strip_right_fused_kernel<NC><<<blocks_r, 256, 0, st>>>(A, Zin, out, minus, m0);
+        strip_right_fused_kernel<NC, WPR><<<blocks_r, 256, 0, st>>>(A, Zin, out, minus, m0);
     };
     switch (batch) {
       case 1: go(std::integral_constant<int, 4>{}); break;
@@ -568,9 +693,7 @@ static void fast_solve(const helm_plan* P, helm_workspace* ws, const S* in, S* o
     S* Z = (S*)ws->strip[0];
     S* Ch = (S*)ws->strip[1];
     S* Cs = (S*)ws->strip[2];
-    dim3 grd((d.m0 * 32 + 255) / 256, batch);
-    strip_reduce_kernel<S><<<grd, 256, 0, st>>>(T2, d.strip_q, Z, d.m0, batch * 4);
-    HELM_LAUNCH_CHECK();
+    strip_reduce<S>(T2, d.strip_q, Z, d.m0, batch, st);
     S* part = (S*)ws->strip[3];
     S* Zf = (S*)ws->strip[6];
     strip_gemm_fold((const double2*)d.cap_left, Z, Ch, true, (const double2*)d.cap_mode, nullptr, d.m0, batch, Zf,
@@ -589,8 +712,7 @@ static void fast_solve(const helm_plan* P, helm_workspace* ws, const S* in, S* o
       cp.lk[i] = sub(d.strip_lt[i], scale(d.strip_lm[i], P->geo.k2));
     }
     for (int it = 0; it < d.strip_refine; ++it) {
-      strip_reduce_kernel<S><<<grd, 256, 0, st>>>(T2, d.strip_q, Z, d.m0, batch * 4);
-      HELM_LAUNCH_CHECK();
+      strip_reduce<S>(T2, d.strip_q, Z, d.m0, batch, st);
       strip_rho_kernel<<<(d.m0 * batch + 255) / 256, 256, 0, st>>>(Cs, Z, R, (const double2*)d.t0_band,
                                                                   (const double2*)d.m0_band, cp, d.m0, batch);
       HELM_LAUNCH_CHECK();

@@ -92,6 +92,43 @@ __device__ __forceinline__ double2 warp_sum(double2 v) {
   return v;
 }
 
+// Compensated accumulation (value s + running error c, TwoSum / FMA-TwoProduct error-free
+// transformations): dot products whose result no longer depends on the summation order at
+// the rounding level, so they can be split over lanes and warps freely.
+struct CSum {
+  double s, c;
+};
+__device__ __forceinline__ void csum_add(CSum& a, double p) {
+  const double t = a.s + p, z = t - a.s;
+  a.c += (a.s - (t - z)) + (p - z);
+  a.s = t;
+}
+__device__ __forceinline__ void csum_fma(CSum& a, double x, double y) {
+  const double p = x * y;
+  a.c += fma(x, y, -p);
+  csum_add(a, p);
+}
+__device__ __forceinline__ void csum_merge(CSum& a, CSum b) {
+  a.c += b.c;
+  csum_add(a, b.s);
+}
+__device__ __forceinline__ double csum_val(CSum a) { return a.s + a.c; }
+// complex a += x * y
+__device__ __forceinline__ void csum_cfma(CSum& re, CSum& im, double2 x, double2 y) {
+  csum_fma(re, x.x, y.x);
+  csum_fma(re, -x.y, y.y);
+  csum_fma(im, x.x, y.y);
+  csum_fma(im, x.y, y.x);
+}
+// xor butterfly (every lane ends with the same total: the merge is symmetric)
+__device__ __forceinline__ void warp_csum(CSum& v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const CSum w{__shfl_xor_sync(0xffffffffu, v.s, o), __shfl_xor_sync(0xffffffffu, v.c, o)};
+    csum_merge(v, w);
+  }
+}
+
 // ----------------------------------------------------------------------------
 // error plumbing
 // ----------------------------------------------------------------------------
@@ -193,8 +230,11 @@ struct PlanDev {
   void* t0_band;
   void* m0_band;
   int* band_piv;        // Sommerfeld band LU (pivot offsets widened to int for 4-byte cp.async)
-  void* band_l;
-  void* band_u;
+  void* band_l;         // [m0][m0][2] multipliers (inside band_fac)
+  void* band_u;         // [m0][m0][5] {1/U_jj, U_j,j+1..j+4}, or [m0][m0][3] when band_nopiv (inside band_fac)
+  void* band_fac;       // one allocation holding band_l then band_u
+  size_t band_fac_bytes;
+  int band_nopiv;       // no pivot was taken: U has no fill (compact 3-entry rows, pivots never read)
   double2* band_seg;    // segment propagators of the small-batch band solve (band_seg.cu), or null
   int n_strip;
   double* strip_q;
