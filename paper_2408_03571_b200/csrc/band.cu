@@ -52,6 +52,7 @@ __global__ void __launch_bounds__(BW* NW) band_solve_kernel(const double2* __res
                                                             const double* __restrict__ q,
                                                             const double* __restrict__ sig, int ldc,
                                                             const double2* __restrict__ add) {
+  pdl_wait();  // PDL: the predecessor's writes are visible (no-op without PDL)
   extern __shared__ __align__(16) unsigned char sraw[];
   const int t = threadIdx.x & (BW - 1), w = threadIdx.x / BW;
   const int a0 = blockIdx.x * BW;
@@ -262,8 +263,7 @@ static void band_launch_k(const helm_plan* P, const double2* in, double2* out, c
     attr = true;
   }
   dim3 grd((d.m0 + BW - 1) / BW, (batch + RB * NW - 1) / (RB * NW));
-  band_solve_kernel<RB, NW, R, ST, NOPIV><<<grd, BW * NW, smem, st>>>(
-      in, out, d.band_piv, (const double2*)d.band_l, (const double2*)d.band_u, d.m0, batch, corr, d.strip_q,
+  launch_pdl(band_solve_kernel<RB, NW, R, ST, NOPIV>, grd, BW * NW, smem, st, in, out, d.band_piv, (const double2*)d.band_l, (const double2*)d.band_u, d.m0, batch, corr, d.strip_q,
       d.coarse_scale, batch * 4, add);
   HELM_LAUNCH_CHECK();
 }

@@ -174,6 +174,7 @@ template <bool NOPIV>
 __global__ void band_seg_setup_kernel(const int* __restrict__ piv, const double2* __restrict__ L,
                                       const double2* __restrict__ U, int m0, int ls, double2* __restrict__ phi,
                                       double2* __restrict__ psi) {
+  pdl_wait();  // PDL: the predecessor's writes are visible (no-op without PDL)
   const int a = blockIdx.x * blockDim.x + threadIdx.x;
   const int k = blockIdx.y;
   if (a >= m0) return;
@@ -201,6 +202,7 @@ __global__ void __launch_bounds__(SEG_THREADS) band_seg_kernel(
     const double2* __restrict__ L, const double2* __restrict__ U, const double2* __restrict__ phi,
     const double2* __restrict__ psi, int m0, int ls, const double2* __restrict__ corr, const double* __restrict__ q,
     const double* __restrict__ sig, int ldc, const double2* __restrict__ addv) {
+  pdl_wait();  // PDL: the predecessor's writes are visible (no-op without PDL)
   extern __shared__ __align__(16) unsigned char sraw[];
   double2* rows = reinterpret_cast<double2*>(sraw);  // [ls][SEG][SMB] eliminated rows
   __shared__ double2 fst[SEG + 1][SMB][2];           // forward states at segment starts
@@ -346,8 +348,7 @@ void band_seg_setup(const PlanDev& d, double2* tables, cudaStream_t st) {
   double2* phi = tables;
   double2* psi = tables + (size_t)SEG * 4 * m0;
   auto go = [&](auto np) {
-    band_seg_setup_kernel<decltype(np)::value><<<dim3((m0 + 127) / 128, SEG), 128, 0, st>>>(
-        d.band_piv, (const double2*)d.band_l, (const double2*)d.band_u, m0, seg_len(m0), phi, psi);
+    launch_pdl(band_seg_setup_kernel<decltype(np)::value>, dim3((m0 + 127) / 128, SEG), 128, 0, st, d.band_piv, (const double2*)d.band_l, (const double2*)d.band_u, m0, seg_len(m0), phi, psi);
   };
   if (d.band_nopiv) go(std::true_type{});
   else go(std::false_type{});
@@ -368,11 +369,12 @@ void band_seg_launch(const helm_plan* P, const double2* in, double2* out, const 
       HELM_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     attr = true;
   }
-  // deeper prefetch chunks (8 / 6 rows) were measured slower at batch 1 (register-bound)
-  (d.band_nopiv ? band_seg_kernel<true, 4, 4> : band_seg_kernel<false, 4, 4>)<<<dim3((m0 + SMB - 1) / SMB, batch),
-                                                                              SEG_THREADS, smem, st>>>(
-      in, out, d.band_piv, (const double2*)d.band_l, (const double2*)d.band_u, phi, psi, m0, ls, corr, d.strip_q,
-      d.coarse_scale, batch * 4, add);
+  // measured at batch 1, n = 2049: deeper register prefetch chunks (8 / 6 rows) slower
+  // (register-bound), L2 prefetches 1-2 chunks further ahead no faster
+  auto kern = d.band_nopiv ? band_seg_kernel<true, 4, 4> : band_seg_kernel<false, 4, 4>;
+  launch_pdl(kern, dim3((m0 + SMB - 1) / SMB, batch), SEG_THREADS, smem, st, in, out, d.band_piv,
+             (const double2*)d.band_l, (const double2*)d.band_u, phi, psi, m0, ls, corr, d.strip_q, d.coarse_scale,
+             batch * 4, add);
   HELM_LAUNCH_CHECK();
 }
 

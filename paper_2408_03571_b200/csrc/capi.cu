@@ -40,6 +40,14 @@ static T* upload(const void* host, size_t count) {
   HELM_CUDA(cudaMemcpy(d, host, count * sizeof(T), cudaMemcpyHostToDevice));
   return d;
 }
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("HELM_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 // HELM_<name>=0 switches a fast path off (development A/B and tests)
 static bool env_flag_off(const char* name) {
   const char* e = std::getenv(name);
@@ -199,12 +207,21 @@ static void gmres_impl(const helm_plan* P, helm_workspace* ws, const S* b, S* x,
   };
 
   static const bool trace = std::getenv("HELM_GMRES_TRACE") != nullptr;
+  // Look-ahead: iteration j+1 is enqueued before the host reads iteration j's three scalars
+  // (two pinned slots by parity, an event per slot), so the device never idles on the
+  // host's convergence test.  Iteration j+1 writes only V[j+2], column j+1 of H and the
+  // Givens entries j+1, j+2, none of which x_j = M V_j y_j (gmres.py:98-105) reads, so a
+  // converged x_j is the same as without look-ahead; the speculative iteration is skipped
+  // when the estimate extrapolated from the last two is within 10x of the tolerance (a
+  // wasted iteration costs a whole M^-1 + CGS2).  HELM_GMRES_LOOKAHEAD=0 turns it off.
+  const bool look = !trace && !env_flag_off("HELM_GMRES_LOOKAHEAD");
+  double* slot = hp + 16;  // [2][4]
+  cudaEvent_t sev[2];
+  for (auto& e : sev) HELM_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   cudaEvent_t tev[3] = {nullptr, nullptr, nullptr};
   if (trace)
     for (auto& e : tev) HELM_CUDA(cudaEventCreate(&e));
-  auto tprev = std::chrono::steady_clock::now();
-  bool done = false;
-  for (int j = 0; j < mi && !done; ++j) {
+  auto enqueue = [&](int j) {
     ensure_basis(j + 2);
     S* vj = Vp + (size_t)j * N;
     if (trace) HELM_CUDA(cudaEventRecord(tev[0], st));
@@ -214,10 +231,35 @@ static void gmres_impl(const helm_plan* P, helm_workspace* ws, const S* b, S* x,
     krylov_cgs2_impl<S>(Vp, j, N, N, H.p + j, (size_t)mi, scal.p + 2, scratch, st, H.p, mi, cs.p, sn.p, g.p, beta,
                         scal.p + 4);
     if (trace) HELM_CUDA(cudaEventRecord(tev[2], st));
-    HELM_CUDA(cudaMemcpyAsync(hp, scal.p + 2, 3 * sizeof(double), cudaMemcpyDeviceToHost, st));
-    HELM_CUDA(cudaStreamSynchronize(st));
-    const bool brk = hp[1] != 0.0;
-    const double est = hp[2];
+    HELM_CUDA(cudaMemcpyAsync(slot + 4 * (j & 1), scal.p + 2, 3 * sizeof(double), cudaMemcpyDeviceToHost, st));
+    HELM_CUDA(cudaEventRecord(sev[j & 1], st));
+  };
+  auto tprev = std::chrono::steady_clock::now();
+  bool done = false;
+  double est1 = 1.0, est2 = 1.0;  // estimates of the last two iterations
+  int queued = 0;                 // iterations enqueued so far
+  if (mi > 0) {
+    enqueue(0);
+    queued = 1;
+  }
+  for (int j = 0; j < mi && !done; ++j) {
+    if (queued == j) {  // not enqueued ahead
+      enqueue(j);
+      queued = j + 1;
+    }
+    if (look && j + 1 < mi && queued == j + 1) {
+      const double pred = est1 * (est1 / std::max(est2, 1e-300));  // extrapolated estimate of iteration j
+      if (pred > 10.0 * rtol) {
+        enqueue(j + 1);
+        queued = j + 2;
+      }
+    }
+    HELM_CUDA(cudaEventSynchronize(sev[j & 1]));
+    const double* hj = slot + 4 * (j & 1);
+    const bool brk = hj[1] != 0.0;
+    const double est = hj[2];
+    est2 = est1;
+    est1 = est;
     if (trace) {  // HELM_GMRES_TRACE=1: per-iteration device times of the operator and of CGS2
       float t_op = 0.f, t_cgs = 0.f;
       cudaEventElapsedTime(&t_op, tev[0], tev[1]);
@@ -241,6 +283,7 @@ static void gmres_impl(const helm_plan* P, helm_workspace* ws, const S* b, S* x,
       }
     }
   }
+  for (auto& e : sev) cudaEventDestroy(e);
   if (!done) {
     form_solution(mi - 1);
     rep->iterations = mi;

@@ -24,6 +24,7 @@
 // Everything is O(m0^2 log m0) per right-hand side and HBM-bound (dense fast
 // diagonalisation would be O(m0^3) FP64).  refine_steps iterative-refinement
 // steps r = c - A0 y (25-point residual), y += solve(r) follow.
+#include <cstdlib>
 #include <type_traits>
 
 #include "ops.cuh"
@@ -38,6 +39,7 @@ constexpr int SCH = 16;  // row elements per lane in flight (strip kernels)
 template <typename S>
 __global__ void __launch_bounds__(256) strip_reduce_kernel(const S* __restrict__ Yh, const double* __restrict__ q,
                                                            S* __restrict__ Z, int m0, int ldz) {
+  pdl_wait();  // PDL: the predecessor's writes are visible (no-op without PDL)
   const int y = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   const int b = blockIdx.y;
@@ -72,33 +74,33 @@ __global__ void __launch_bounds__(256) strip_reduce_kernel(const S* __restrict__
   if (lane < 4) Z[(size_t)y * ldz + (size_t)b * 4 + lane] = acc[lane];
 }
 
-// Small batches: the same strip values with compensated sums (csum_*), each row split over
+// Small batches: the same strip values with compensated sums (CSum), each row split over
 // WPR warps (lanes stride the row by 32 * WPR, warp partials merged in warp order).
-template <int WPR>
+template <int WPR, bool COMP>
 __global__ void __launch_bounds__(256) strip_reduce_c_kernel(const double2* __restrict__ Yh,
                                                              const double* __restrict__ q, double2* __restrict__ Z,
                                                              int m0, int ldz) {
-  __shared__ CSum red[8][8];
+  pdl_wait();  // PDL: the predecessor's writes are visible (no-op without PDL)
+  using CS = CSum<COMP>;
+  __shared__ CS red[8][8];
   const int wl = threadIdx.x >> 5, lane = threadIdx.x & 31, sw = wl % WPR;
   const int yy = (blockIdx.x * blockDim.x + threadIdx.x) / (32 * WPR);
   const int b = blockIdx.y;
   const bool ok = yy < m0;
   const double2* row = Yh + ((size_t)b * m0 + (ok ? yy : 0)) * m0;
-  CSum acc[8];
-#pragma unroll
-  for (int i = 0; i < 8; ++i) acc[i] = CSum{0.0, 0.0};
+  CS acc[8];
 #pragma unroll 4
   for (int a = sw * 32 + lane; a < (ok ? m0 : 0); a += 32 * WPR) {
     const double2 v = row[a];
     const double4 qa = *reinterpret_cast<const double4*>(q + (size_t)a * 4);
-    csum_fma(acc[0], qa.x, v.x);
-    csum_fma(acc[1], qa.x, v.y);
-    csum_fma(acc[2], qa.y, v.x);
-    csum_fma(acc[3], qa.y, v.y);
-    csum_fma(acc[4], qa.z, v.x);
-    csum_fma(acc[5], qa.z, v.y);
-    csum_fma(acc[6], qa.w, v.x);
-    csum_fma(acc[7], qa.w, v.y);
+    acc[0].fma(qa.x, v.x);
+    acc[1].fma(qa.x, v.y);
+    acc[2].fma(qa.y, v.x);
+    acc[3].fma(qa.y, v.y);
+    acc[4].fma(qa.z, v.x);
+    acc[5].fma(qa.z, v.y);
+    acc[6].fma(qa.w, v.x);
+    acc[7].fma(qa.w, v.y);
   }
 #pragma unroll
   for (int i = 0; i < 8; ++i) warp_csum(acc[i]);
@@ -108,14 +110,27 @@ __global__ void __launch_bounds__(256) strip_reduce_c_kernel(const double2* __re
   }
   __syncthreads();
   if (ok && sw == 0 && lane < 4) {
-    CSum re = red[wl][2 * lane], im = red[wl][2 * lane + 1];
+    CS re = red[wl][2 * lane], im = red[wl][2 * lane + 1];
 #pragma unroll
     for (int w = 1; w < WPR; ++w) {
-      csum_merge(re, red[wl + w][2 * lane]);
-      csum_merge(im, red[wl + w][2 * lane + 1]);
+      re.merge(red[wl + w][2 * lane]);
+      im.merge(red[wl + w][2 * lane + 1]);
     }
-    Z[(size_t)yy * ldz + (size_t)b * 4 + lane] = mk(csum_val(re), csum_val(im));
+    Z[(size_t)yy * ldz + (size_t)b * 4 + lane] = mk(re.val(), im.val());
   }
+}
+
+// which small-batch strip sums are compensated: bit 0 the strip reduction, bit 1 the
+// fold GEMVs (HELM_STRIP_COMP, default 0).  Measured at batch 1, n = 2049: plain 0.330 ms
+// per coarse solve, fully compensated 0.378 ms; the cfg4a GMRES count is 364 with either
+// (and on both band paths), so the plain sums are the default and the compensated ones the
+// check that a count does not hinge on the split's rounding.
+static int strip_comp() {
+  static const int v = [] {
+    const char* e = std::getenv("HELM_STRIP_COMP");
+    return e ? std::atoi(e) : 0;
+  }();
+  return v;
 }
 
 template <typename S>
@@ -124,13 +139,16 @@ static void strip_reduce(const S* Yh, const double* q, S* Z, int m0, int batch, 
     if (batch <= 4) {
       constexpr int WPR = 4;
       dim3 grd((unsigned)((m0 * 32 * WPR + 255) / 256), batch);
-      strip_reduce_c_kernel<WPR><<<grd, 256, 0, st>>>(Yh, q, Z, m0, batch * 4);
+      if (strip_comp() & 1)
+        launch_pdl(strip_reduce_c_kernel<WPR, true>, grd, 256, 0, st, Yh, q, Z, m0, batch * 4);
+      else
+        launch_pdl(strip_reduce_c_kernel<WPR, false>, grd, 256, 0, st, Yh, q, Z, m0, batch * 4);
       HELM_LAUNCH_CHECK();
       return;
     }
   }
   dim3 grd((unsigned)((m0 * 32 + 255) / 256), batch);
-  strip_reduce_kernel<S><<<grd, 256, 0, st>>>(Yh, q, Z, m0, batch * 4);
+  launch_pdl(strip_reduce_kernel<S>, grd, 256, 0, st, Yh, q, Z, m0, batch * 4);
   HELM_LAUNCH_CHECK();
 }
 
@@ -144,6 +162,7 @@ static void strip_reduce(const S* Yh, const double* q, S* Z, int m0, int batch, 
 // Columns are the batch's 4 strip columns per right-hand side (ldn = 4 * batch).
 __global__ void __launch_bounds__(256) strip_fold_kernel(const double2* __restrict__ Z, double2* __restrict__ Zf,
                                                          int m0, int ldn) {
+  pdl_wait();  // PDL: the predecessor's writes are visible (no-op without PDL)
   const int he = (m0 + 1) / 2, ho = m0 / 2;
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= he * ldn) return;
@@ -170,6 +189,7 @@ struct FoldGemmSmem {
 __global__ void __launch_bounds__(256) strip_gemm_fold_kernel(const double2* __restrict__ A,
                                                               const double2* __restrict__ B,
                                                               double2* __restrict__ part, int m0, int ldn) {
+  pdl_wait();  // PDL: the predecessor's writes are visible (no-op without PDL)
   extern __shared__ __align__(16) unsigned char sraw[];
   FoldGemmSmem& sm = *reinterpret_cast<FoldGemmSmem*>(sraw);
   const int he = (m0 + 1) / 2, ho = m0 / 2;
@@ -245,6 +265,7 @@ template <int NC>
 __global__ void __launch_bounds__(256) strip_gemm_fold_rows_kernel(const double2* __restrict__ A,
                                                                    const double2* __restrict__ B,
                                                                    double2* __restrict__ part, int m0) {
+  pdl_wait();  // PDL: the predecessor's writes are visible (no-op without PDL)
   const int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (r >= m0) return;
@@ -276,6 +297,7 @@ __global__ void __launch_bounds__(256) strip_reduce_left_kernel(const double2* _
                                                                 double2* __restrict__ out,
                                                                 const double2* __restrict__ Hm, int m0,
                                                                 int ngroups, int nks) {
+  pdl_wait();  // PDL: the predecessor's writes are visible (no-op without PDL)
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= m0 * ngroups) return;
   const int r = e / ngroups, g = e % ngroups;
@@ -303,6 +325,7 @@ __global__ void __launch_bounds__(256) strip_reduce_right_kernel(const double2* 
                                                                  double2* __restrict__ out,
                                                                  const double2* __restrict__ minus, int m0,
                                                                  int ldn, int nks) {
+  pdl_wait();  // PDL: the predecessor's writes are visible (no-op without PDL)
   const int he = (m0 + 1) / 2, ho = m0 / 2;
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= he * ldn) return;
@@ -328,18 +351,19 @@ __global__ void __launch_bounds__(256) strip_reduce_right_kernel(const double2* 
 }
 
 // Small batches (<= 4 right-hand sides, NC = 4 * batch strip columns): WPR warps per output
-// row (lanes stride the row by 32 * WPR), compensated sums (csum_*: the result does not
+// row (lanes stride the row by 32 * WPR), compensated sums (CSum: the result does not
 // depend on that split at the rounding level), the fold / unfold and the 4x4 epilogue fused
 // into the product (one launch per side).
 // Cross-warp total of the row's per-warp sums, merged in warp order; the totals land in
 // the row's first warp.  All threads of the CTA call it.
-template <int NC, int WPR>
-__device__ __forceinline__ void row_total_c(CSum (&re)[NC], CSum (&im)[NC], int wl, int lane, double2 (&acc)[NC]) {
+template <int NC, int WPR, bool C>
+__device__ __forceinline__ void row_total_c(CSum<C> (&re)[NC], CSum<C> (&im)[NC], int wl, int lane,
+                                            double2 (&acc)[NC]) {
   if constexpr (WPR == 1) {
 #pragma unroll
-    for (int c = 0; c < NC; ++c) acc[c] = mk(csum_val(re[c]), csum_val(im[c]));
+    for (int c = 0; c < NC; ++c) acc[c] = mk(re[c].val(), im[c].val());
   } else {
-    __shared__ CSum red[8][NC][2];
+    __shared__ CSum<C> red[8][NC][2];
     if (lane == 0) {
 #pragma unroll
       for (int c = 0; c < NC; ++c) {
@@ -351,13 +375,13 @@ __device__ __forceinline__ void row_total_c(CSum (&re)[NC], CSum (&im)[NC], int 
     if (wl % WPR == 0) {
 #pragma unroll
       for (int c = 0; c < NC; ++c) {
-        CSum r = red[wl][c][0], i = red[wl][c][1];
+        CSum<C> r = red[wl][c][0], i = red[wl][c][1];
 #pragma unroll
         for (int w = 1; w < WPR; ++w) {
-          csum_merge(r, red[wl + w][c][0]);
-          csum_merge(i, red[wl + w][c][1]);
+          r.merge(red[wl + w][c][0]);
+          i.merge(red[wl + w][c][1]);
         }
-        acc[c] = mk(csum_val(r), csum_val(i));
+        acc[c] = mk(r.val(), i.val());
       }
     }
     __syncthreads();  // the shared partials may be reused by the next call
@@ -365,11 +389,12 @@ __device__ __forceinline__ void row_total_c(CSum (&re)[NC], CSum (&im)[NC], int 
 }
 
 // left:  row r of the packed mode blocks, t = A_g[r] . fold(Z), out[r] = Hm[r] t  (Hm may be null)
-template <int NC, int WPR>
+template <int NC, int WPR, bool COMP>
 __global__ void __launch_bounds__(256) strip_left_fused_kernel(const double2* __restrict__ A,
                                                                const double2* __restrict__ Z,
                                                                double2* __restrict__ out,
                                                                const double2* __restrict__ Hm, int m0) {
+  pdl_wait();  // PDL: the predecessor's writes are visible (no-op without PDL)
   const int wl = threadIdx.x >> 5, lane = threadIdx.x & 31, sw = wl % WPR;
   const int rr = (blockIdx.x * blockDim.x + threadIdx.x) / (32 * WPR);
   const bool ok = rr < m0;
@@ -378,9 +403,7 @@ __global__ void __launch_bounds__(256) strip_left_fused_kernel(const double2* __
   const bool odd = r >= he;
   const int Mg = odd ? ho : he;
   const double2* arow = A + (odd ? (size_t)he * he + (size_t)(r - he) * ho : (size_t)r * he);
-  CSum re[NC], im[NC];
-#pragma unroll
-  for (int c = 0; c < NC; ++c) re[c] = im[c] = CSum{0.0, 0.0};
+  CSum<COMP> re[NC], im[NC];
 #pragma unroll(NC <= 8 ? 4 : 1)
   for (int k = sw * 32 + lane; k < (ok ? Mg : 0); k += 32 * WPR) {
     const double2 av = arow[k];
@@ -427,11 +450,12 @@ __global__ void __launch_bounds__(256) strip_left_fused_kernel(const double2* __
 
 // right: for y < he, E = A_e[y] . cin[0:he), O = A_o[y] . cin[he:m0) (y < ho);
 // out[y] = E + O (- minus[y]), out[m0-1-y] = E - O (- minus[m0-1-y]), out[centre] = E
-template <int NC, int WPR>
+template <int NC, int WPR, bool COMP>
 __global__ void __launch_bounds__(256) strip_right_fused_kernel(const double2* __restrict__ A,
                                                                 const double2* __restrict__ cin,
                                                                 double2* __restrict__ out,
                                                                 const double2* __restrict__ minus, int m0) {
+  pdl_wait();  // PDL: the predecessor's writes are visible (no-op without PDL)
   const int wl = threadIdx.x >> 5, lane = threadIdx.x & 31, sw = wl % WPR;
   const int yy = (blockIdx.x * blockDim.x + threadIdx.x) / (32 * WPR);
   const int he = (m0 + 1) / 2, ho = m0 / 2;
@@ -439,9 +463,7 @@ __global__ void __launch_bounds__(256) strip_right_fused_kernel(const double2* _
   const int y = ok ? yy : he - 1;
   const double2* ae = A + (size_t)y * he;
   const double2* ao = A + (size_t)he * he + (size_t)y * ho;
-  CSum er[NC], ei[NC], orr[NC], oi[NC];
-#pragma unroll
-  for (int c = 0; c < NC; ++c) er[c] = ei[c] = orr[c] = oi[c] = CSum{0.0, 0.0};
+  CSum<COMP> er[NC], ei[NC], orr[NC], oi[NC];
 #pragma unroll(NC <= 8 ? 4 : 1)
   for (int k = sw * 32 + lane; k < (ok ? he : 0); k += 32 * WPR) {
     const double2 av = ae[k];
@@ -499,10 +521,15 @@ static void strip_gemm_fold(const double2* A, const double2* Zin, double2* out, 
       constexpr int NC = decltype(nc)::value;
       constexpr int WPR = NC <= 8 ? 4 : 2;  // few rows: each split over WPR warps
       const int blocks_l = (m0 * 32 * WPR + 255) / 256, blocks_r = (he * 32 * WPR + 255) / 256;
-      if (left)
-        strip_left_fused_kernel<NC, WPR><<<blocks_l, 256, 0, st>>>(A, Zin, out, Hm, m0);
+      const bool comp = strip_comp() & 2;
+      if (left && comp)
+        launch_pdl(strip_left_fused_kernel<NC, WPR, true>, blocks_l, 256, 0, st, A, Zin, out, Hm, m0);
+      else if (left)
+        launch_pdl(strip_left_fused_kernel<NC, WPR, false>, blocks_l, 256, 0, st, A, Zin, out, Hm, m0);
+      else if (comp)
+        launch_pdl(strip_right_fused_kernel<NC, WPR, true>, blocks_r, 256, 0, st, A, Zin, out, minus, m0);
       else
-        strip_right_fused_kernel<NC, WPR><<<blocks_r, 256, 0, st>>>(A, Zin, out, minus, m0);
+        launch_pdl(strip_right_fused_kernel<NC, WPR, false>, blocks_r, 256, 0, st, A, Zin, out, minus, m0);
     };
     switch (batch) {
       case 1: go(std::integral_constant<int, 4>{}); break;
@@ -515,17 +542,17 @@ static void strip_gemm_fold(const double2* A, const double2* Zin, double2* out, 
   }
   const double2* B = Zin;
   if (left) {
-    strip_fold_kernel<<<(he * ldn + 255) / 256, 256, 0, st>>>(Zin, Zf, m0, ldn);
+    launch_pdl(strip_fold_kernel, (he * ldn + 255) / 256, 256, 0, st, Zin, Zf, m0, ldn);
     HELM_LAUNCH_CHECK();
     B = Zf;
   }
   int nks = 1;
   const int rows_blocks = (m0 * 32 + 255) / 256;
   switch (batch) {
-    case 1: strip_gemm_fold_rows_kernel<4><<<rows_blocks, 256, 0, st>>>(A, B, part, m0); break;
-    case 2: strip_gemm_fold_rows_kernel<8><<<rows_blocks, 256, 0, st>>>(A, B, part, m0); break;
-    case 3: strip_gemm_fold_rows_kernel<12><<<rows_blocks, 256, 0, st>>>(A, B, part, m0); break;
-    case 4: strip_gemm_fold_rows_kernel<16><<<rows_blocks, 256, 0, st>>>(A, B, part, m0); break;
+    case 1: launch_pdl(strip_gemm_fold_rows_kernel<4>, rows_blocks, 256, 0, st, A, B, part, m0); break;
+    case 2: launch_pdl(strip_gemm_fold_rows_kernel<8>, rows_blocks, 256, 0, st, A, B, part, m0); break;
+    case 3: launch_pdl(strip_gemm_fold_rows_kernel<12>, rows_blocks, 256, 0, st, A, B, part, m0); break;
+    case 4: launch_pdl(strip_gemm_fold_rows_kernel<16>, rows_blocks, 256, 0, st, A, B, part, m0); break;
     default: {
       static bool attr = false;
       if (!attr) {
@@ -535,15 +562,15 @@ static void strip_gemm_fold(const double2* A, const double2* Zin, double2* out, 
       }
       const int tiles = (he + FG_M - 1) / FG_M + (ho + FG_M - 1) / FG_M;
       dim3 grd((ldn + FG_N - 1) / FG_N, tiles, FG_KS);
-      strip_gemm_fold_kernel<<<grd, 256, sizeof(FoldGemmSmem), st>>>(A, B, part, m0, ldn);
+      launch_pdl(strip_gemm_fold_kernel, grd, 256, sizeof(FoldGemmSmem), st, A, B, part, m0, ldn);
       nks = FG_KS;
     }
   }
   HELM_LAUNCH_CHECK();
   if (left)
-    strip_reduce_left_kernel<<<(m0 * batch + 255) / 256, 256, 0, st>>>(part, out, Hm, m0, batch, nks);
+    launch_pdl(strip_reduce_left_kernel, (m0 * batch + 255) / 256, 256, 0, st, part, out, Hm, m0, batch, nks);
   else
-    strip_reduce_right_kernel<<<(he * ldn + 255) / 256, 256, 0, st>>>(part, out, minus, m0, ldn, nks);
+    launch_pdl(strip_reduce_right_kernel, (he * ldn + 255) / 256, 256, 0, st, part, out, minus, m0, ldn, nks);
   HELM_LAUNCH_CHECK();
 }
 
@@ -559,6 +586,7 @@ __global__ void __launch_bounds__(256) strip_rho_kernel(const double2* __restric
                                                         double2* __restrict__ rho, const double2* __restrict__ t0b,
                                                         const double2* __restrict__ m0b, StripCoupling cp, int m0,
                                                         int batch) {
+  pdl_wait();  // PDL: the predecessor's writes are visible (no-op without PDL)
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= m0 * batch) return;
   const int y = e / batch, b = e % batch;
@@ -593,6 +621,7 @@ __global__ void __launch_bounds__(256) strip_rho_kernel(const double2* __restric
 }
 
 __global__ void strip_axpy_kernel(double2* __restrict__ c, const double2* __restrict__ w, size_t n) {
+  pdl_wait();  // PDL: the predecessor's writes are visible (no-op without PDL)
   const size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e < n) c[e] = add(c[e], w[e]);
 }
@@ -606,6 +635,7 @@ template <typename S>
 __global__ void __launch_bounds__(256) a0_residual_kernel(const S* __restrict__ c, const S* __restrict__ y,
                                                           S* __restrict__ r, const S* __restrict__ t0b,
                                                           const S* __restrict__ m0b, double k2, int m0) {
+  pdl_wait();  // PDL: the predecessor's writes are visible (no-op without PDL)
   extern __shared__ __align__(16) unsigned char sraw[];
   S (*ys)[RSX + 4] = reinterpret_cast<S (*)[RSX + 4]>(sraw);
   S (*xm)[RSX] = reinterpret_cast<S (*)[RSX]>(ys + (RSY + 4));
@@ -713,7 +743,7 @@ static void fast_solve(const helm_plan* P, helm_workspace* ws, const S* in, S* o
     }
     for (int it = 0; it < d.strip_refine; ++it) {
       strip_reduce<S>(T2, d.strip_q, Z, d.m0, batch, st);
-      strip_rho_kernel<<<(d.m0 * batch + 255) / 256, 256, 0, st>>>(Cs, Z, R, (const double2*)d.t0_band,
+      launch_pdl(strip_rho_kernel, (d.m0 * batch + 255) / 256, 256, 0, st, Cs, Z, R, (const double2*)d.t0_band,
                                                                   (const double2*)d.m0_band, cp, d.m0, batch);
       HELM_LAUNCH_CHECK();
       strip_gemm_fold((const double2*)d.cap_vt, R, Ch, true, (const double2*)d.cap_hg, nullptr, d.m0, batch, Zf,
@@ -722,7 +752,7 @@ static void fast_solve(const helm_plan* P, helm_workspace* ws, const S* in, S* o
       launch_band_solve(P, nullptr, T3, W, batch, st, T2);  // T3 = T2 + B^{-1}(-ext(W))
       if (it + 1 < d.strip_refine) {
         const size_t ns = (size_t)d.m0 * batch * 4;
-        strip_axpy_kernel<<<(unsigned)((ns + 255) / 256), 256, 0, st>>>(Cs, W, ns);
+        launch_pdl(strip_axpy_kernel, (unsigned)((ns + 255) / 256), 256, 0, st, Cs, W, ns);
         HELM_LAUNCH_CHECK();
       }
       std::swap(T2, T3);
@@ -748,7 +778,7 @@ void launch_coarse_solve(const helm_plan* P, helm_workspace* ws, const S* c, S* 
       attr = true;
     }
     dim3 blk(32, 8), grd((m0 + RSX - 1) / RSX, (m0 + RSY - 1) / RSY, batch);
-    a0_residual_kernel<S><<<grd, blk, smem, st>>>(c, yy, r, (const S*)P->dev.t0_band, (const S*)P->dev.m0_band,
+    launch_pdl(a0_residual_kernel<S>, grd, blk, smem, st, c, yy, r, (const S*)P->dev.t0_band, (const S*)P->dev.m0_band,
                                                   P->geo.k2, m0);
     HELM_LAUNCH_CHECK();
     fast_solve<S>(P, ws, r, yy, batch, st, /*accumulate=*/true);  // yy += A0~^{-1} r

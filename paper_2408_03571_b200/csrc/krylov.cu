@@ -24,6 +24,7 @@ template <typename S>
 __global__ void __launch_bounds__(KB) update_kernel(S* __restrict__ w, const S* __restrict__ V, int nvec,
                                                     size_t ldv, const S* __restrict__ h, double sign, size_t N,
                                                     int from_zero, double* __restrict__ npart) {
+  pdl_wait();  // PDL: the predecessor's writes are visible (no-op without PDL)
   extern __shared__ __align__(16) unsigned char sraw[];
   S* hs = reinterpret_cast<S*>(sraw);
   __shared__ double nred[KB / 32];
@@ -60,6 +61,7 @@ __global__ void __launch_bounds__(KB) update_kernel(S* __restrict__ w, const S* 
 
 template <typename S>
 __global__ void __launch_bounds__(KB) norm2_kernel(const S* __restrict__ x, size_t N, double* __restrict__ npart) {
+  pdl_wait();  // PDL: the predecessor's writes are visible (no-op without PDL)
   __shared__ double nred[KB / 32];
   double nrm = 0.0;
   for (size_t n = blockIdx.x * (size_t)blockDim.x + threadIdx.x; n < N; n += (size_t)gridDim.x * blockDim.x)
@@ -75,6 +77,7 @@ __global__ void __launch_bounds__(KB) norm2_kernel(const S* __restrict__ x, size
 }
 
 __global__ void sum_partials_kernel(const double* __restrict__ npart, int nb, double* __restrict__ out) {
+  pdl_wait();  // PDL: the predecessor's writes are visible (no-op without PDL)
   double s = 0.0;
   for (int b = threadIdx.x; b < nb; b += 32) s += npart[b];
   s = warp_sum(s);
@@ -84,6 +87,7 @@ __global__ void sum_partials_kernel(const double* __restrict__ npart, int nb, do
 template <typename S>
 __global__ void scale_kernel(S* __restrict__ x, const S* __restrict__ src, const double* __restrict__ s, int invert,
                              size_t N) {
+  pdl_wait();  // PDL: the predecessor's writes are visible (no-op without PDL)
   const double f = invert ? 1.0 / s[0] : s[0];
   if (!invert && f == 0.0) return;  // breakdown: leave the vector alone
   for (size_t n = blockIdx.x * (size_t)blockDim.x + threadIdx.x; n < N; n += (size_t)gridDim.x * blockDim.x)
@@ -93,6 +97,7 @@ __global__ void scale_kernel(S* __restrict__ x, const S* __restrict__ src, const
 // --- y = R^{-1} g with R = H[:j+1, :j+1] upper triangular (gmres.py:98-103) -----
 template <typename S>
 __global__ void backsolve_kernel(const S* __restrict__ H, int ldh, int j, const S* __restrict__ g, S* __restrict__ y) {
+  pdl_wait();  // PDL: the predecessor's writes are visible (no-op without PDL)
   extern __shared__ __align__(16) unsigned char sraw[];
   S* rhs = reinterpret_cast<S*>(sraw);
   __shared__ S yi_s;
@@ -250,6 +255,7 @@ template <typename S>
 __global__ void __launch_bounds__(KB) cgs_dots_kernel(const S* __restrict__ V, int nvec, size_t ldv,
                                                       const S* __restrict__ w, size_t N, S* __restrict__ partial,
                                                       S* __restrict__ h, unsigned* __restrict__ count) {
+  pdl_wait();  // PDL: the predecessor's writes are visible (no-op without PDL)
   extern __shared__ __align__(16) unsigned char sraw[];
   S* wacc_all = reinterpret_cast<S*>(sraw);
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -342,6 +348,7 @@ __global__ void __launch_bounds__(UW * 32) cgs_update_dots_kernel(const S* __res
                                                              S* __restrict__ h2, unsigned* __restrict__ count,
                                                              S* __restrict__ hcol, size_t hstride,
                                                              double* __restrict__ inv, GivensArgs gv) {
+  pdl_wait();  // PDL: the predecessor's writes are visible (no-op without PDL)
   extern __shared__ __align__(16) unsigned char sraw[];
   S* wacc_all = reinterpret_cast<S*>(sraw);
   S* hs = wacc_all + (size_t)UW * nvec;
@@ -470,6 +477,7 @@ template <typename S>
 __global__ void __launch_bounds__(KB) cgs_final_kernel(const S* __restrict__ V, int nvec, size_t ldv,
                                                        S* __restrict__ w, size_t N, const S* __restrict__ h2,
                                                        const double* __restrict__ inv) {
+  pdl_wait();  // PDL: the predecessor's writes are visible (no-op without PDL)
   extern __shared__ __align__(16) unsigned char sraw[];
   S* hs = reinterpret_cast<S*>(sraw);
   for (int i = threadIdx.x; i < nvec; i += KB) hs[i] = h2[i];
@@ -510,7 +518,7 @@ static void cgs2_run(S* V, int j, size_t ldv, size_t N, S* hcol, size_t hstride,
   // K1
   const size_t sm1 = (size_t)(KB / 32) * nvec * es;
   set_smem((const void*)cgs_dots_kernel<S>, sm1);
-  cgs_dots_kernel<S><<<KNB, KB, sm1, st>>>(V, nvec, ldv, w, N, (S*)k.partial, (S*)k.h1, k.count);
+  launch_pdl(cgs_dots_kernel<S>, KNB, KB, sm1, st, V, nvec, ldv, w, N, (S*)k.partial, (S*)k.h1, k.count);
   HELM_LAUNCH_CHECK();
   // K2: staged while a block's stage fits in shared memory; E elements per lane keep
   // ~32 staged rows per lane in flight for short bases
@@ -519,7 +527,7 @@ static void cgs2_run(S* V, int j, size_t ldv, size_t N, S* hcol, size_t hstride,
   const size_t sm2s = sm2 + (size_t)UW * nvec * 32 * E * es;
   auto launch2 = [&](auto kern, int grid, size_t smem) {
     set_smem((const void*)kern, smem);
-    kern<<<grid, UW * 32, smem, st>>>(V, nvec, ldv, w, N, (const S*)k.h1, (S*)k.partial, k.npart, (S*)k.h2,
+    launch_pdl(kern, grid, UW * 32, smem, st, V, nvec, ldv, w, N, (const S*)k.h1, (S*)k.partial, k.npart, (S*)k.h2,
                                       k.count + 1, hcol, hstride, inv_out, gv);
   };
   if (sm2s <= SMEM_MAX) {
@@ -535,7 +543,7 @@ static void cgs2_run(S* V, int j, size_t ldv, size_t N, S* hcol, size_t hstride,
   // K3
   const size_t sm3 = (size_t)nvec * es;
   set_smem((const void*)cgs_final_kernel<S>, sm3);
-  cgs_final_kernel<S><<<KNB, KB, sm3, st>>>(V, nvec, ldv, w, N, (const S*)k.h2, inv_out);
+  launch_pdl(cgs_final_kernel<S>, KNB, KB, sm3, st, V, nvec, ldv, w, N, (const S*)k.h2, inv_out);
   HELM_LAUNCH_CHECK();
 }
 
@@ -544,15 +552,15 @@ template <typename S>
 void krylov_combine(S* x, const S* V, int nvec, size_t ldv, const S* h, size_t N, cudaStream_t st) {
   const size_t smem = (size_t)nvec * sizeof(S);
   set_smem((const void*)update_kernel<S>, smem);
-  update_kernel<S><<<KNB, KB, smem, st>>>(x, V, nvec, ldv, h, 1.0, N, 1, nullptr);
+  launch_pdl(update_kernel<S>, KNB, KB, smem, st, x, V, nvec, ldv, h, 1.0, N, 1, nullptr);
   HELM_LAUNCH_CHECK();
 }
 
 template <typename S> void krylov_norm2(const S* x, size_t N, double* out, void* scratch, cudaStream_t st) {
   CgsScratch k = carve(scratch, 1);
-  norm2_kernel<S><<<KNB, KB, 0, st>>>(x, N, k.npart);
+  launch_pdl(norm2_kernel<S>, KNB, KB, 0, st, x, N, k.npart);
   HELM_LAUNCH_CHECK();
-  sum_partials_kernel<<<1, 32, 0, st>>>(k.npart, KNB, out);
+  launch_pdl(sum_partials_kernel, 1, 32, 0, st, k.npart, KNB, out);
   HELM_LAUNCH_CHECK();
 }
 
@@ -574,12 +582,13 @@ void krylov_cgs2(S* V, int j, size_t ldv, size_t N, S* hcol, void* scratch, cuda
 
 template <typename S>
 __global__ void givens_kernel(S* H, int ldh, int j, S* cs, S* sn, S* g, double beta, double* est) {
+  pdl_wait();  // PDL: the predecessor's writes are visible (no-op without PDL)
   if (threadIdx.x == 0 && blockIdx.x == 0) givens_apply<S>(H, ldh, j, cs, sn, g, beta, est);
 }
 
 template <typename S>
 void krylov_givens(S* H, int ldh, int j, S* cs, S* sn, S* g, double beta, double* est, cudaStream_t st) {
-  givens_kernel<S><<<1, 32, 0, st>>>(H, ldh, j, cs, sn, g, beta, est);
+  launch_pdl(givens_kernel<S>, 1, 32, 0, st, H, ldh, j, cs, sn, g, beta, est);
   HELM_LAUNCH_CHECK();
 }
 
@@ -590,12 +599,12 @@ template <typename S> void krylov_backsolve(const S* H, int ldh, int j, const S*
     HELM_CUDA(cudaFuncSetAttribute(backsolve_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     attr[Sc<S>::cplx] = true;
   }
-  backsolve_kernel<S><<<1, 256, smem, st>>>(H, ldh, j, g, y);
+  launch_pdl(backsolve_kernel<S>, 1, 256, smem, st, H, ldh, j, g, y);
   HELM_LAUNCH_CHECK();
 }
 
 template <typename S> void krylov_scale(S* x, const S* src, const double* s, int invert, size_t N, cudaStream_t st) {
-  scale_kernel<S><<<KNB, KB, 0, st>>>(x, src, s, invert, N);
+  launch_pdl(scale_kernel<S>, KNB, KB, 0, st, x, src, s, invert, N);
   HELM_LAUNCH_CHECK();
 }
 

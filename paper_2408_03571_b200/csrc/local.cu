@@ -40,6 +40,7 @@ __global__ void __launch_bounds__(256) local_fdm_kernel(const S* __restrict__ x,
                                                         const S* __restrict__ classV,
                                                         const S* __restrict__ classLam, LocalArgs a,
                                                         int ld) {
+  pdl_wait();  // PDL: the predecessor's writes are visible (no-op without PDL)
   extern __shared__ __align__(16) unsigned char smem_raw[];
   S* sm = reinterpret_cast<S*>(smem_raw);
   S* Vy = sm;                 // [ld][ld]
@@ -117,6 +118,7 @@ template <typename S>
 __global__ void combine_rows_kernel(const S* __restrict__ base, S* __restrict__ y, const S* __restrict__ ovl,
                                     const int* __restrict__ band_node, const int* __restrict__ node_mult,
                                     int nu, int nbands, LocalArgs a) {
+  pdl_wait();  // PDL: the predecessor's writes are visible (no-op without PDL)
   const int ix = blockIdx.x * blockDim.x + threadIdx.x;
   const int bi = blockIdx.y;
   if (ix >= nu) return;
@@ -139,6 +141,7 @@ template <typename S>
 __global__ void combine_cols_kernel(const S* __restrict__ base, S* __restrict__ y, const S* __restrict__ ovl,
                                     const int* __restrict__ band_node, const int* __restrict__ node_mult,
                                     int nu, int nbands, LocalArgs a) {
+  pdl_wait();  // PDL: the predecessor's writes are visible (no-op without PDL)
   const int bi = blockIdx.x * blockDim.x + threadIdx.x;
   const int iy = blockIdx.y;
   if (bi >= nbands || node_mult[iy] != 1) return;
@@ -187,16 +190,16 @@ void launch_local_sum(const helm_plan* P, const S* x, const S* base, S* y, S* ov
       HELM_CUDA(cudaFuncSetAttribute(local_fdm_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
       attr_set[Sc<S>::cplx] = true;
     }
-    local_fdm_kernel<S><<<grd, 256, smem, st>>>(x, base, y, ovl, (const S*)d.class_V, (const S*)d.class_lambda, a,
+    launch_pdl(local_fdm_kernel<S>, grd, 256, smem, st, x, base, y, ovl, (const S*)d.class_V, (const S*)d.class_lambda, a,
                                                 ld);
     HELM_LAUNCH_CHECK();
   }
   if (d.nbands > 0) {
     dim3 g1((a.nu + 127) / 128, d.nbands, batch);
-    combine_rows_kernel<S><<<g1, 128, 0, st>>>(base, y, ovl, band_node, d.node_mult, a.nu, d.nbands, a);
+    launch_pdl(combine_rows_kernel<S>, g1, 128, 0, st, base, y, ovl, band_node, d.node_mult, a.nu, d.nbands, a);
     HELM_LAUNCH_CHECK();
     dim3 g2((d.nbands + 127) / 128, a.nu, batch);
-    combine_cols_kernel<S><<<g2, 128, 0, st>>>(base, y, ovl, band_node, d.node_mult, a.nu, d.nbands, a);
+    launch_pdl(combine_cols_kernel<S>, g2, 128, 0, st, base, y, ovl, band_node, d.node_mult, a.nu, d.nbands, a);
     HELM_LAUNCH_CHECK();
   }
 }

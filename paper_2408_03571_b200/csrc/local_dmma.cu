@@ -147,6 +147,7 @@ __global__ void __launch_bounds__(DTH, 4) local_fdm_dmma_kernel(const S* __restr
                                                              const double* __restrict__ classVf,
                                                              const double* __restrict__ classInvden, int ncls,
                                                              LocalArgs a) {
+  pdl_wait();  // PDL: the predecessor's writes are visible (no-op without PDL)
   constexpr int NP = Sc<S>::cplx ? 2 : 1;
   constexpr int XL = DmmaDims<NP>::XL;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -290,7 +291,7 @@ void launch_local_dmma(const helm_plan* P, const S* x, const S* base, S* y, S* o
     attr = true;
   }
   dim3 grd(d.n_ff, batch);
-  local_fdm_dmma_kernel<S><<<grd, DTH, smem, st>>>(x, base, y, ovl, d.box_ff, d.class_Vf, d.class_invden,
+  launch_pdl(local_fdm_dmma_kernel<S>, grd, DTH, smem, st, x, base, y, ovl, d.box_ff, d.class_Vf, d.class_invden,
                                                    d.n_classes, a);
   HELM_LAUNCH_CHECK();
 }

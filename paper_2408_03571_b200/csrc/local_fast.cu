@@ -162,6 +162,7 @@ __global__ void __launch_bounds__(LTH) local_fdm_fast_kernel(const S* __restrict
                                                              const double* __restrict__ classVr,
                                                              const int* __restrict__ class_real,
                                                              const S* __restrict__ classLam, LocalArgs a) {
+  pdl_wait();  // PDL: the predecessor's writes are visible (no-op without PDL)
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int sid = boxes[blockIdx.x];
   const int ay = sid / a.p, ax = sid % a.p;
@@ -205,7 +206,7 @@ static void fast_launch(const helm_plan* P, const S* x, const S* base, S* y, S* 
     attr = true;
   }
   dim3 grd(nbox, batch);
-  local_fdm_fast_kernel<S, RR><<<grd, LTH, smem, st>>>(x, base, y, ovl, boxes, (const S*)d.class_V, d.class_Vr,
+  launch_pdl(local_fdm_fast_kernel<S, RR>, grd, LTH, smem, st, x, base, y, ovl, boxes, (const S*)d.class_V, d.class_Vr,
                                                        d.class_real, (const S*)d.class_lambda, a);
   HELM_LAUNCH_CHECK();
 }

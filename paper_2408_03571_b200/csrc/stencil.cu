@@ -17,6 +17,7 @@ namespace helm {
 template <typename S, bool kDeflate>
 __global__ void __launch_bounds__(256) stencil_kernel(const S* __restrict__ x, const S* __restrict__ z,
                                                       S* __restrict__ y, Geo g) {
+  pdl_wait();  // PDL: the predecessor's writes are visible (no-op without PDL)
   const int nu = g.nu;
   const int ix = blockIdx.x * blockDim.x + threadIdx.x;
   const int iy = blockIdx.y * blockDim.y + threadIdx.y;
@@ -61,9 +62,9 @@ template <typename S>
 void launch_stencil(const Geo& g, const S* x, const S* z, S* y, int batch, cudaStream_t st) {
   dim3 blk(32, 8), grd((g.nu + 31) / 32, (g.nu + 7) / 8, batch);
   if (z)
-    stencil_kernel<S, true><<<grd, blk, 0, st>>>(x, z, y, g);
+    launch_pdl(stencil_kernel<S, true>, grd, blk, 0, st, x, z, y, g);
   else
-    stencil_kernel<S, false><<<grd, blk, 0, st>>>(x, nullptr, y, g);
+    launch_pdl(stencil_kernel<S, false>, grd, blk, 0, st, x, nullptr, y, g);
   HELM_LAUNCH_CHECK();
 }
 

@@ -108,6 +108,7 @@ __device__ __forceinline__ int warp_global() { return (blockIdx.x * blockDim.x +
 template <typename S, int off>
 __global__ void __launch_bounds__(256) restrict_sweep_kernel(const S* __restrict__ x, S* __restrict__ c, Geo g,
                                                              int ngroups, int US) {
+  pdl_wait();  // PDL: the predecessor's writes are visible (no-op without PDL)
   const int lane = threadIdx.x & 31;
   const int wg = warp_global();
   const int grp = wg % ngroups, strip = wg / ngroups;
@@ -160,6 +161,7 @@ __device__ __forceinline__ S coarse_at(const S* __restrict__ cb, int m0, int U, 
 template <typename S, int off>
 __global__ void __launch_bounds__(256) prolong_sweep_kernel(const S* __restrict__ c, S* __restrict__ z, Geo g,
                                                             int ngroups, int RS) {
+  pdl_wait();  // PDL: the predecessor's writes are visible (no-op without PDL)
   const int lane = threadIdx.x & 31;
   const int wg = warp_global();
   const int grp = wg % ngroups, strip = wg / ngroups;
@@ -205,6 +207,7 @@ template <typename S, int off>
 __global__ void __launch_bounds__(256, 2) prolong_deflate_sweep_kernel(const S* __restrict__ c,
                                                                     const S* __restrict__ x, S* __restrict__ z,
                                                                     S* __restrict__ d, Geo g, int ngroups, int RS) {
+  pdl_wait();  // PDL: the predecessor's writes are visible (no-op without PDL)
   const int lane = threadIdx.x & 31;
   const int wg = warp_global();
   const int grp = wg % ngroups, strip = wg / ngroups;
@@ -305,9 +308,9 @@ void launch_restrict(const Geo& g, const S* x, S* c, int batch, cudaStream_t st)
   const int warps = groups * ((g.m0 + US - 1) / US);
   dim3 grd((warps + 7) / 8, batch);
   if (g.off)
-    restrict_sweep_kernel<S, 1><<<grd, 256, 0, st>>>(x, c, g, groups, US);
+    launch_pdl(restrict_sweep_kernel<S, 1>, grd, 256, 0, st, x, c, g, groups, US);
   else
-    restrict_sweep_kernel<S, 0><<<grd, 256, 0, st>>>(x, c, g, groups, US);
+    launch_pdl(restrict_sweep_kernel<S, 0>, grd, 256, 0, st, x, c, g, groups, US);
   HELM_LAUNCH_CHECK();
 }
 
@@ -319,9 +322,9 @@ void launch_prolong(const Geo& g, const S* c, S* z, int batch, cudaStream_t st) 
   const int warps = groups * ((npairs + RS - 1) / RS);
   dim3 grd((warps + 7) / 8, batch);
   if (g.off)
-    prolong_sweep_kernel<S, 1><<<grd, 256, 0, st>>>(c, z, g, groups, RS);
+    launch_pdl(prolong_sweep_kernel<S, 1>, grd, 256, 0, st, c, z, g, groups, RS);
   else
-    prolong_sweep_kernel<S, 0><<<grd, 256, 0, st>>>(c, z, g, groups, RS);
+    launch_pdl(prolong_sweep_kernel<S, 0>, grd, 256, 0, st, c, z, g, groups, RS);
   HELM_LAUNCH_CHECK();
 }
 
@@ -334,9 +337,9 @@ void launch_prolong_deflate(const Geo& g, const S* c, const S* x, S* z, S* d, in
   const int warps = groups * ((nsteps + RS - 1) / RS);
   dim3 grd((warps + 7) / 8, batch);
   if (g.off)
-    prolong_deflate_sweep_kernel<S, 1><<<grd, 256, 0, st>>>(c, x, z, d, g, groups, RS);
+    launch_pdl(prolong_deflate_sweep_kernel<S, 1>, grd, 256, 0, st, c, x, z, d, g, groups, RS);
   else
-    prolong_deflate_sweep_kernel<S, 0><<<grd, 256, 0, st>>>(c, x, z, d, g, groups, RS);
+    launch_pdl(prolong_deflate_sweep_kernel<S, 0>, grd, 256, 0, st, c, x, z, d, g, groups, RS);
   HELM_LAUNCH_CHECK();
 }
 

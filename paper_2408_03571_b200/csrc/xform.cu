@@ -142,6 +142,7 @@ template <typename S, int VPT>
 __global__ void __launch_bounds__(256) xform_fft_kernel(const S* __restrict__ in, S* __restrict__ out, XScale sc,
                                                         int rows, int m0, int L, int dct,
                                                         const double2* __restrict__ tw) {
+  pdl_wait();  // PDL: the predecessor's writes are visible (no-op without PDL)
   static_assert(VPT == 8, "one radix-8 butterfly per thread in the first stage");
   // tw: plan-owned table exp(-2 pi i k / L), k < L (read through L1)
   extern __shared__ __align__(16) unsigned char sraw[];
@@ -282,13 +283,14 @@ static void fft_launch(const S* in, S* out, const XScale& sc, int rows, int m0, 
   }
   const int nfft = Sc<S>::cplx ? rows : (rows + 1) / 2;
   const int blocks = std::min((nfft + rpc - 1) / rpc, 148 * 4);
-  xform_fft_kernel<S, VPT><<<blocks, threads, smem, st>>>(in, out, sc, rows, m0, L, dct, tw);
+  launch_pdl(xform_fft_kernel<S, VPT>, blocks, threads, smem, st, in, out, sc, rows, m0, L, dct, tw);
 }
 
 // Direct O(m0^2)-per-row transform for grids whose n - 1 is not a power of two.
 template <typename S>
 __global__ void __launch_bounds__(256) xform_direct_kernel(const S* __restrict__ in, S* __restrict__ out, XScale sc,
                                                            int rows, int m0, int dct) {
+  pdl_wait();  // PDL: the predecessor's writes are visible (no-op without PDL)
   const int a = blockIdx.x * blockDim.x + threadIdx.x;
   const int r = blockIdx.y;
   if (a >= m0 || r >= rows) return;
@@ -310,6 +312,7 @@ __global__ void __launch_bounds__(256) xform_direct_kernel(const S* __restrict__
 // out[b][x][y] = in[b][y][x]  (32 x 32 tiles through shared memory)
 template <typename S>
 __global__ void __launch_bounds__(256) transpose_kernel(const S* __restrict__ in, S* __restrict__ out, int m) {
+  pdl_wait();  // PDL: the predecessor's writes are visible (no-op without PDL)
   __shared__ S tile[32][33];
   const size_t off = (size_t)blockIdx.z * m * m;
   const int x0 = blockIdx.x * 32, y0 = blockIdx.y * 32;
@@ -338,7 +341,7 @@ void launch_xform(const helm_plan* P, const S* in, S* out, const double* sig, bo
     fft_launch<S, 8>(in, out, sc, rows, m0, L, dct, d.twiddle, st);
   } else {
     dim3 grd((m0 + 255) / 256, rows);
-    xform_direct_kernel<S><<<grd, 256, 0, st>>>(in, out, sc, rows, m0, dct);
+    launch_pdl(xform_direct_kernel<S>, grd, 256, 0, st, in, out, sc, rows, m0, dct);
   }
   HELM_LAUNCH_CHECK();
 }
@@ -346,7 +349,7 @@ void launch_xform(const helm_plan* P, const S* in, S* out, const double* sig, bo
 template <typename S>
 void launch_transpose(const S* in, S* out, int m, int batch, cudaStream_t st) {
   dim3 grd((m + 31) / 32, (m + 31) / 32, batch), blk(32, 8);
-  transpose_kernel<S><<<grd, blk, 0, st>>>(in, out, m);
+  launch_pdl(transpose_kernel<S>, grd, blk, 0, st, in, out, m);
   HELM_LAUNCH_CHECK();
 }
 
