@@ -29,8 +29,9 @@
 namespace helm {
 
 constexpr int SEG = 32;  // segments per mode
-constexpr int SMB = 8;   // modes per CTA (8 consecutive modes = one 128-byte row segment)
-constexpr int SEG_THREADS = SEG * SMB;
+// modes per CTA: SMB consecutive modes, SEG * SMB threads (one warp per mode in the scans).
+// 4 modes per CTA spread a batch-1 solve (m0 = 1025: 257 CTAs) over all 148 SMs.
+constexpr int SMB_MAX = 8;
 
 
 struct SegRhs {
@@ -196,8 +197,8 @@ __global__ void band_seg_setup_kernel(const int* __restrict__ piv, const double2
 
 // CF / CB: rows per prefetch chunk of the forward / backward sweeps (the next chunk's
 // loads are in flight while the current one is consumed)
-template <bool NOPIV, int CF, int CB>
-__global__ void __launch_bounds__(SEG_THREADS) band_seg_kernel(
+template <bool NOPIV, int CF, int CB, int SMB>
+__global__ void __launch_bounds__(SEG * SMB) band_seg_kernel(
     const double2* __restrict__ in, double2* __restrict__ out, const int* __restrict__ piv,
     const double2* __restrict__ L, const double2* __restrict__ U, const double2* __restrict__ phi,
     const double2* __restrict__ psi, int m0, int ls, const double2* __restrict__ corr, const double* __restrict__ q,
@@ -359,20 +360,26 @@ void band_seg_launch(const helm_plan* P, const double2* in, double2* out, const 
                      cudaStream_t st, const double2* add) {
   const PlanDev& d = P->dev;
   const int m0 = d.m0, ls = seg_len(m0);
-  const size_t smem = (size_t)ls * SEG * SMB * sizeof(double2);
   const double2* phi = d.band_seg;
   const double2* psi = d.band_seg + (size_t)SEG * 4 * m0;
-  HELM_CHECK(smem <= 200 * 1024, "segmented band solve: segment too long");
+  static const int smb = [] {
+    const char* e = std::getenv("HELM_SEG_SMB");
+    return e && std::atoi(e) == 8 ? 8 : 4;
+  }();
   static bool attr = false;
   if (!attr) {
-    for (auto k : {band_seg_kernel<false, 4, 4>, band_seg_kernel<true, 4, 4>})
+    for (auto k : {band_seg_kernel<false, 4, 4, 4>, band_seg_kernel<true, 4, 4, 4>, band_seg_kernel<false, 4, 4, 8>,
+                   band_seg_kernel<true, 4, 4, 8>})
       HELM_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     attr = true;
   }
   // measured at batch 1, n = 2049: deeper register prefetch chunks (8 / 6 rows) slower
   // (register-bound), L2 prefetches 1-2 chunks further ahead no faster
-  auto kern = d.band_nopiv ? band_seg_kernel<true, 4, 4> : band_seg_kernel<false, 4, 4>;
-  launch_pdl(kern, dim3((m0 + SMB - 1) / SMB, batch), SEG_THREADS, smem, st, in, out, d.band_piv,
+  auto kern = smb == 8 ? (d.band_nopiv ? band_seg_kernel<true, 4, 4, 8> : band_seg_kernel<false, 4, 4, 8>)
+                       : (d.band_nopiv ? band_seg_kernel<true, 4, 4, 4> : band_seg_kernel<false, 4, 4, 4>);
+  const size_t smem = (size_t)ls * SEG * smb * sizeof(double2);
+  HELM_CHECK(smem <= 200 * 1024, "segmented band solve: segment too long");
+  launch_pdl(kern, dim3((m0 + smb - 1) / smb, batch), SEG * smb, smem, st, in, out, d.band_piv,
              (const double2*)d.band_l, (const double2*)d.band_u, phi, psi, m0, ls, corr, d.strip_q, d.coarse_scale,
              batch * 4, add);
   HELM_LAUNCH_CHECK();

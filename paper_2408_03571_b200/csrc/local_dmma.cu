@@ -154,6 +154,7 @@ __global__ void __launch_bounds__(DTH, 4) local_fdm_dmma_kernel(const S* __restr
   double* Xr = reinterpret_cast<double*>(smem_raw);  // [DT][XL]
   int* meta = reinterpret_cast<int*>(Xr + DT * XL);  // [2][3][DT]: multiplicity, first box, band per row / column
   S* cw = reinterpret_cast<S*>(meta + 6 * DT);       // [WIN][WIN] coarse window (coarse-base mode)
+  S* rx = cw + WIN * WIN;                             // [WIN][DT] x-pass of the window prolongation
   const int sid = boxes[blockIdx.x];
   const int ay = sid / a.p, ax = sid % a.p;
   const int nu = a.nu;
@@ -238,6 +239,38 @@ __global__ void __launch_bounds__(DTH, 4) local_fdm_dmma_kernel(const S* __restr
   dmma_right<NP, true>(Xr, Vx, [&](int m, int part, int n, double v) { Xr[m * XL + n * NP + part] = v; });
   cp_wait<0>();
   __syncthreads();
+  // R0^T c at the box's nodes, separably: the x pass (3 taps per window row and fine column,
+  // the same fma order as window_prolong) once per CTA into rx, the y pass per node below --
+  // bitwise the same sums as window_prolong with a third of its FP64 work (which shares the
+  // pipe with the DMMAs)
+  const bool cbase = bb && a.coarse_base;
+  if (cbase) {
+    for (int e = threadIdx.x; e < WIN * Lx; e += DTH) {
+      const int u = e / Lx, j = e % Lx;
+      const int tx = x0 + j - a.off;
+      const bool ex = (tx & 1) == 0;
+      const int V0 = (ex ? tx / 2 - 1 : (tx - 1) >> 1) - Ubx;
+      const double w0 = ex ? 0.125 : 0.5, w1 = ex ? 0.75 : 0.5, w2 = ex ? 0.125 : 0.0;
+      const S* c = cw + u * WIN + V0;
+      S row = Sc<S>::zero();
+      row = fma_(w0, c[0], row);
+      row = fma_(w1, c[1], row);
+      row = fma_(w2, c[2], row);
+      rx[u * DT + j] = row;
+    }
+    __syncthreads();
+  }
+  auto prolong_y = [&](int iy, int q) {
+    const int ty = iy - a.off;
+    const bool ey = (ty & 1) == 0;
+    const int U0 = (ey ? ty / 2 - 1 : (ty - 1) >> 1) - Uby;
+    const S* r = rx + U0 * DT + q;
+    S acc = Sc<S>::zero();
+    acc = fma_(ey ? 0.125 : 0.5, r[0], acc);
+    acc = fma_(ey ? 0.75 : 0.5, r[DT], acc);
+    acc = fma_(ey ? 0.125 : 0.0, r[2 * DT], acc);
+    return acc;
+  };
   // unfold + weight + scatter: x_i = e_i + o_i, x_{L-1-i} = e_i - o_i on both axes
   auto get = [&](int i, int j) -> S {
     if constexpr (NP == 2) return mk(Xr[i * XL + 2 * j], Xr[i * XL + 2 * j + 1]);
@@ -245,11 +278,12 @@ __global__ void __launch_bounds__(DTH, 4) local_fdm_dmma_kernel(const S* __restr
   };
   auto put = [&](int r, int q, S acc) {
     const int my = meta[r], mx = meta[3 * DT + q];
-    if (a.weighted && !a.wbs) acc = scale(acc, 1.0 / (my * mx));
+    // partition-of-unity weight 1 / (my mx) with my, mx in {1, 2}: exact constants, no division
+    if (a.weighted && !a.wbs && my * mx != 1) acc = scale(acc, my * mx == 2 ? 0.5 : 0.25);
     const int iy = y0 + r, ix = x0 + q;
     const size_t pidx = (size_t)iy * nu + ix;
     if (my == 1 && mx == 1) {
-      yb[pidx] = bb ? add(a.coarse_base ? window_prolong(cw, a.off, Uby, Ubx, iy, ix) : bb[pidx], acc) : acc;
+      yb[pidx] = bb ? add(cbase ? prolong_y(iy, q) : bb[pidx], acc) : acc;
     } else if (my == 2) {
       const int ry = ay - meta[DT + r], rx = ax - meta[4 * DT + q];
       ob[((size_t)(ry * 2 + rx) * a.nbands + meta[2 * DT + r]) * nu + ix] = acc;
@@ -281,11 +315,11 @@ void launch_local_dmma(const helm_plan* P, const S* x, const S* base, S* y, S* o
   if (d.n_ff == 0) return;
   constexpr int NP = Sc<S>::cplx ? 2 : 1;
   const size_t smem = (size_t)(DT * DmmaDims<NP>::XL) * sizeof(double) + 6 * DT * sizeof(int) +
-                      (a.coarse_base ? WIN * WIN * sizeof(S) : 0);
+                      (a.coarse_base ? (WIN * WIN + WIN * DT) * sizeof(S) : 0);
   static bool attr = false;
   if (!attr) {
     const size_t smax = (size_t)(DT * DmmaDims<NP>::XL) * sizeof(double) + 6 * DT * sizeof(int) +
-                        WIN * WIN * sizeof(S);
+                        (WIN * WIN + WIN * DT) * sizeof(S);
     HELM_CUDA(cudaFuncSetAttribute(local_fdm_dmma_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)smax));
     attr = true;
