@@ -30,8 +30,9 @@ namespace helm {
 
 constexpr int SEG = 32;  // segments per mode
 // modes per CTA: SMB consecutive modes, SEG * SMB threads (one warp per mode in the scans).
-// 4 modes per CTA spread a batch-1 solve (m0 = 1025: 257 CTAs) over all 148 SMs.
-constexpr int SMB_MAX = 8;
+// 8 (129 CTAs at m0 = 1025); 4 modes per CTA (257 CTAs over all 148 SMs) was measured
+// slower at batch 1 (0.313 vs 0.303 ms per coarse solve).
+constexpr int SMB = 8;
 
 
 struct SegRhs {
@@ -362,24 +363,18 @@ void band_seg_launch(const helm_plan* P, const double2* in, double2* out, const 
   const int m0 = d.m0, ls = seg_len(m0);
   const double2* phi = d.band_seg;
   const double2* psi = d.band_seg + (size_t)SEG * 4 * m0;
-  static const int smb = [] {
-    const char* e = std::getenv("HELM_SEG_SMB");
-    return e && std::atoi(e) == 8 ? 8 : 4;
-  }();
   static bool attr = false;
   if (!attr) {
-    for (auto k : {band_seg_kernel<false, 4, 4, 4>, band_seg_kernel<true, 4, 4, 4>, band_seg_kernel<false, 4, 4, 8>,
-                   band_seg_kernel<true, 4, 4, 8>})
+    for (auto k : {band_seg_kernel<false, 4, 4, SMB>, band_seg_kernel<true, 4, 4, SMB>})
       HELM_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     attr = true;
   }
   // measured at batch 1, n = 2049: deeper register prefetch chunks (8 / 6 rows) slower
   // (register-bound), L2 prefetches 1-2 chunks further ahead no faster
-  auto kern = smb == 8 ? (d.band_nopiv ? band_seg_kernel<true, 4, 4, 8> : band_seg_kernel<false, 4, 4, 8>)
-                       : (d.band_nopiv ? band_seg_kernel<true, 4, 4, 4> : band_seg_kernel<false, 4, 4, 4>);
-  const size_t smem = (size_t)ls * SEG * smb * sizeof(double2);
+  auto kern = d.band_nopiv ? band_seg_kernel<true, 4, 4, SMB> : band_seg_kernel<false, 4, 4, SMB>;
+  const size_t smem = (size_t)ls * SEG * SMB * sizeof(double2);
   HELM_CHECK(smem <= 200 * 1024, "segmented band solve: segment too long");
-  launch_pdl(kern, dim3((m0 + smb - 1) / smb, batch), SEG * smb, smem, st, in, out, d.band_piv,
+  launch_pdl(kern, dim3((m0 + SMB - 1) / SMB, batch), SEG * SMB, smem, st, in, out, d.band_piv,
              (const double2*)d.band_l, (const double2*)d.band_u, phi, psi, m0, ls, corr, d.strip_q, d.coarse_scale,
              batch * 4, add);
   HELM_LAUNCH_CHECK();
