@@ -12,6 +12,8 @@
 // in place through a barrier, twiddles tabulated once per CTA with sincospi.
 // Real rows are packed two per FFT: Q is real, so DST(x + i y) = DST(x) + i DST(y).  Rows are read and written with coalesced
 // 8/16-byte accesses; the transform is HBM-bound at the BASELINE sizes.
+#include <type_traits>
+
 #include "ops.cuh"
 
 namespace helm {
@@ -97,8 +99,8 @@ __device__ __forceinline__ void stockham_stage(double2* buf, const double2* __re
   const int tstep = L / (Ns * R);
 #pragma unroll
   for (int c = 0; c < NBT; ++c) {
-    const int j = tid + c * T;
-    const int k = j % Ns;
+    const int j = tid + c * T;  // >= 0: unsigned division / modulo by the power-of-two Ns
+    const int k = (int)((unsigned)j % (unsigned)Ns);
     if (!FIRST) {  // Ns == 1 on the first stage: all twiddles are 1
       // W^1 and W^2 from the table, the other powers by a depth-2 product tree
       // (2 loads instead of R-1: the load/store queue is this kernel's limiter)
@@ -124,7 +126,7 @@ __device__ __forceinline__ void stockham_stage(double2* buf, const double2* __re
       v[c][0] = add(v[c][0], v[c][1]);
       v[c][1] = t2;
     }
-    const int base = (j / Ns) * Ns * R + k;
+    const int base = (int)((unsigned)j / (unsigned)Ns) * Ns * R + k;
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       if (LAST) store(base + r * Ns, v[c][r]);
@@ -138,27 +140,30 @@ __device__ __forceinline__ void stockham_stage(double2* buf, const double2* __re
 // blockDim threads transforms blockDim/T rows at a time.  The first radix-8 stage
 // takes its inputs from registers that were loaded from HBM while the previous
 // row was in its shared-memory stages (one row of prefetch per thread).
-template <typename S, int VPT>
+// The row length L (a power of two), the transform (DCT-I / DST-I) and hence m0 are
+// template parameters: every index of the Stockham stages is then a shift or a mask
+// (with a runtime L the integer divisions and index arithmetic were ~45 % of the issued
+// instructions).
+constexpr int fft_nst(int L) { return L <= 1 ? 0 : 1 + fft_nst(L >= 8 ? L / 8 : 1); }
+constexpr int fft_rlast(int L) { return L <= 8 ? L : fft_rlast(L / 8); }
+
+template <typename S, int VPT, int LT, bool DCT>
 __global__ void __launch_bounds__(256) xform_fft_kernel(const S* __restrict__ in, S* __restrict__ out, XScale sc,
-                                                        int rows, int m0, int L, int dct,
-                                                        const double2* __restrict__ tw) {
+                                                        int rows, const double2* __restrict__ tw) {
+  constexpr int L = LT, m0 = DCT ? L / 2 + 1 : L / 2 - 1;
+  constexpr bool dct = DCT;
   pdl_wait();  // PDL: the predecessor's writes are visible (no-op without PDL)
   static_assert(VPT == 8, "one radix-8 butterfly per thread in the first stage");
   // tw: plan-owned table exp(-2 pi i k / L), k < L (read through L1)
   extern __shared__ __align__(16) unsigned char sraw[];
-  const int T = L / 8;
+  constexpr int T = L / 8;
   const int g = threadIdx.x / T, tid = threadIdx.x % T;
   const int rpc = blockDim.x / T;
   double2* buf = reinterpret_cast<double2*>(sraw) + (size_t)g * padded_len(L);
   constexpr int RPF = Sc<S>::cplx ? 1 : 2;  // rows per FFT
   const int nfft = (rows + RPF - 1) / RPF;
-  const int K = L / 2;
-  int nst = 0, rlast = 8;
-  for (int rem = L; rem > 1;) {
-    rlast = rem >= 8 ? 8 : rem;
-    ++nst;
-    rem /= rlast;
-  }
+  constexpr int K = L / 2;
+  constexpr int nst = fft_nst(L), rlast = fft_rlast(L);
   // symmetric extension G(j) of FFT f (two real rows packed as re/im)
   auto load = [&](int f, int j) -> double2 {
     if (f >= nfft) return mk(0.0, 0.0);
@@ -244,6 +249,7 @@ __global__ void __launch_bounds__(256) xform_fft_kernel(const S* __restrict__ in
     };
     auto none = [&](int, int, int) { return mk(0.0, 0.0); };
     int Ns = 8;
+#pragma unroll
     for (int s = 1; s < nst; ++s) {
       const bool last = s == nst - 1;
       if (!last) {
@@ -268,22 +274,45 @@ __global__ void __launch_bounds__(256) xform_fft_kernel(const S* __restrict__ in
   }
 }
 
-template <typename S, int VPT>
-static void fft_launch(const S* in, S* out, const XScale& sc, int rows, int m0, int L, int dct, const double2* tw,
-                       cudaStream_t st) {
-  const int T = L / VPT;
+template <typename S, int VPT, int L, bool DCT>
+static void fft_launch_l(const S* in, S* out, const XScale& sc, int rows, const double2* tw, cudaStream_t st) {
+  constexpr int T = L / VPT;
   const int threads = std::max(T, std::min(256, std::max(32, L)));
   const int rpc = threads / T;
   const size_t smem = (size_t)(rpc * padded_len(L)) * sizeof(double2);
   HELM_CHECK(smem <= 200 * 1024 && threads <= 256, "coarse FFT row too long");
   static bool attr = false;
   if (!attr) {
-    HELM_CUDA(cudaFuncSetAttribute(xform_fft_kernel<S, VPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    HELM_CUDA(cudaFuncSetAttribute(xform_fft_kernel<S, VPT, L, DCT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   200 * 1024));
     attr = true;
   }
   const int nfft = Sc<S>::cplx ? rows : (rows + 1) / 2;
   const int blocks = std::min((nfft + rpc - 1) / rpc, 148 * 4);
-  launch_pdl(xform_fft_kernel<S, VPT>, blocks, threads, smem, st, in, out, sc, rows, m0, L, dct, tw);
+  launch_pdl(xform_fft_kernel<S, VPT, L, DCT>, blocks, threads, smem, st, in, out, sc, rows, tw);
+}
+
+template <typename S, int VPT>
+static void fft_launch(const S* in, S* out, const XScale& sc, int rows, int m0, int L, int dct, const double2* tw,
+                       cudaStream_t st) {
+  HELM_CHECK(m0 == (dct ? L / 2 + 1 : L / 2 - 1), "coarse FFT: m0 does not match the row length");
+  auto go = [&](auto lc) {
+    constexpr int LL = decltype(lc)::value;
+    if (dct) fft_launch_l<S, VPT, LL, true>(in, out, sc, rows, tw, st);
+    else fft_launch_l<S, VPT, LL, false>(in, out, sc, rows, tw, st);
+  };
+  switch (L) {
+    case 8: go(std::integral_constant<int, 8>{}); break;
+    case 16: go(std::integral_constant<int, 16>{}); break;
+    case 32: go(std::integral_constant<int, 32>{}); break;
+    case 64: go(std::integral_constant<int, 64>{}); break;
+    case 128: go(std::integral_constant<int, 128>{}); break;
+    case 256: go(std::integral_constant<int, 256>{}); break;
+    case 512: go(std::integral_constant<int, 512>{}); break;
+    case 1024: go(std::integral_constant<int, 1024>{}); break;
+    case 2048: go(std::integral_constant<int, 2048>{}); break;
+    default: HELM_CHECK(false, "coarse FFT: unsupported row length");
+  }
 }
 
 // Direct O(m0^2)-per-row transform for grids whose n - 1 is not a power of two.
