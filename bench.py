@@ -307,6 +307,18 @@ def run_ours(a, rank, world, local_rank):
                    "fixed_ms_per_iter": round(t_iter * 1e3, 4),
                    "roofline": {"T_roof_ms_per_iter": round(t_roof * 1e3, 4), "frac": round(t_roof / t_iter, 4),
                                 "note": "mean over the run of max-phase roofline of M^-1 + A x + CGS2 at basis j+1"}})
+        # (3) multi-right-hand-side GMRES (helm_gmres_multi): 8 seed-0 random
+        # right-hand sides, the same fixed-length run, operators applied to the batch of 8
+        nr = min(8, B)
+        Bm = r0.standard_normal((nr, N)) + 1j * r0.standard_normal((nr, N))
+        hb.gmres_multi(prob.A, M, Bm, cfg)  # warm: maps the interleaved bases
+        reps = hb.gmres_multi(prob.A, M, Bm, cfg)
+        its = sum(q.iterations for q in reps)
+        wall = reps[0].wall_seconds
+        gm["multi"] = {"nrhs": nr, "rhs_iterations": its, "seconds": round(wall, 4),
+                       "rhs_iter_per_s": round(its / wall, 2),
+                       "ms_per_batched_iteration": round(1e3 * wall / max(q.iterations for q in reps), 4),
+                       "roofline_frac": round(t_roof * its / wall, 4)}
 
     return dict(value=value, ms=ms, setup_s=setup_s, clocks=clk.summary(), launches=launches, comp=comp,
                 roof=roof, composite=composite, e2e=e2e, gmres=gm)

@@ -17,6 +17,8 @@
  *   helm_cgs2            <- the MGS + conditional re-orthogonalisation block (gmres.py:112-127)
  *   helm_givens          <- the Givens update + residual estimate (gmres.py:129-148)
  *   helm_gmres           <- `gmres(A, M_inv, b, cfg)` (gmres.py:65-177)
+ *   helm_gmres_multi     <- that loop over several right-hand sides, operators batched
+ *                           (no reference counterpart: SURVEY §8 f4)
  *
  * Conventions
  *  - Every function returns an int status: 0 = OK, nonzero = error; the
@@ -45,7 +47,7 @@
 extern "C" {
 #endif
 
-#define HELM_ABI_VERSION 4
+#define HELM_ABI_VERSION 5
 
 enum helm_bc { HELM_DIRICHLET = 0, HELM_SOMMERFELD = 1 };
 enum helm_kind { HELM_AS2 = 0, HELM_SAS2 = 1, HELM_SHS2 = 2 };
@@ -177,6 +179,13 @@ int helm_givens(const helm_plan* plan, void* H, int32_t ldh, int32_t j, void* cs
 int helm_gmres(const helm_plan* plan, helm_workspace* ws, const void* b, void* x, double rtol,
                int32_t max_iter, int32_t side, int32_t use_precond, double* history,
                helm_gmres_report* report, void* stream);
+
+/* nrhs independent GMRES solves sharing every operator application (each
+ * right-hand side follows helm_gmres's statements).  b, x: device [nrhs][N]; nrhs <= the
+ * workspace's max_batch; history (host, may be NULL): [nrhs][max_iter+1]; reports[nrhs]. */
+int helm_gmres_multi(const helm_plan* plan, helm_workspace* ws, const void* b, void* x, int32_t nrhs,
+                     double rtol, int32_t max_iter, int32_t side, int32_t use_precond, double* history,
+                     helm_gmres_report* reports, void* stream);
 
 #ifdef __cplusplus
 }

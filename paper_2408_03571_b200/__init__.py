@@ -17,7 +17,7 @@ from .discretization import (
     partition,
 )
 from .fdm_setup import SingularMatrixError
-from .gmres import GmresConfig, SolveReport, gmres
+from .gmres import GmresConfig, SolveReport, gmres, gmres_multi
 from .operators import (
     HelmholtzOperator,
     HelmholtzProblem,
@@ -45,6 +45,7 @@ __all__ = [
     "extend_max",
     "galerkin",
     "gmres",
+    "gmres_multi",
     "max_overlap_layers",
     "partition",
 ]

@@ -15,7 +15,7 @@ LIB_PATH = os.path.join(_HERE, "libhelmb200.so")
 
 HELM_DIRICHLET, HELM_SOMMERFELD = 0, 1
 KINDS = {"AS2": 0, "SAS2": 1, "SHS2": 2}
-ABI_VERSION = 4
+ABI_VERSION = 5
 
 c_int32_p = ctypes.POINTER(ctypes.c_int32)
 
@@ -101,6 +101,12 @@ SYMBOLS = [
         "helm_gmres",
         ctypes.c_int,
         [_vp, _vp, _vp, _vp, _dbl, _i32, _i32, _i32, ctypes.POINTER(_dbl), ctypes.POINTER(HelmGmresReport), _vp],
+    ),
+    (
+        "helm_gmres_multi",
+        ctypes.c_int,
+        [_vp, _vp, _vp, _vp, _i32, _dbl, _i32, _i32, _i32, ctypes.POINTER(_dbl), ctypes.POINTER(HelmGmresReport),
+         _vp],
     ),
 ]
 

@@ -298,6 +298,140 @@ static void gmres_impl(const helm_plan* P, helm_workspace* ws, const S* b, S* x,
 }
 
 // ---------------------------------------------------------------------------
+// Multi-right-hand-side GMRES: nrhs independent GMRES runs (gmres.py:65-177
+// each) that share every operator application.  The bases are interleaved, V[j][r][N], so
+// iteration j applies A and M^{-1} to the contiguous batch V[j] (the batched kernels, at
+// batch nrhs) and each right-hand side's CGS2 + Givens runs on its own basis (stride
+// nrhs N) with its own H, cs, sn, g.  A right-hand side that has converged (or broken
+// down) stops its Arnoldi steps; its basis slot is zeroed and still rides along in the
+// batch.  Each right-hand side follows the single-RHS statement order; the batched
+// kernels sum some rows in another order than at batch 1 (rounding-level differences).
+// ---------------------------------------------------------------------------
+template <typename S>
+static void gmres_multi_impl(const helm_plan* P, helm_workspace* ws, const S* B, S* X, int nrhs, double rtol, int mi,
+                             int side, int use_precond, double* history, helm_gmres_report* reps, cudaStream_t st) {
+  const auto t0 = std::chrono::steady_clock::now();
+  HELM_CHECK(nrhs >= 1 && nrhs <= ws->max_batch, "nrhs must be in [1, workspace max_batch]");
+  HELM_CHECK(rtol > 0.0, "relative tolerance must be positive");
+  HELM_CHECK(mi >= 1, "iteration cap must be at least 1");
+  HELM_CHECK(side == 0 || side == 1, "side must be 0 (right) or 1 (left)");
+  HELM_CHECK(krylov_scratch_bytes(mi + 1) <= ws->red_bytes, "iteration cap too large for the workspace scratch");
+  const size_t N = (size_t)P->N, NB = N * nrhs;
+  const bool left = side == 1;
+  const size_t vbytes = N * sizeof(S);
+  S* Vp = nullptr;
+  auto ensure_basis = [&](int nvec) {  // nvec basis vectors per right-hand side
+    Vp = (S*)basis_ensure(ws, (size_t)nvec * nrhs * vbytes, (size_t)(mi + 1) * nrhs * vbytes, 16 * vbytes, st);
+  };
+  ensure_basis(2);
+  const size_t hsz = (size_t)(mi + 1) * mi;
+  DevBuf<S> H(hsz * nrhs, st), cs((size_t)mi * nrhs, st), sn((size_t)mi * nrhs, st), g((size_t)(mi + 1) * nrhs, st),
+      y(mi + 1, st), u(NB, st), r(N, st);
+  DevBuf<double> scal((size_t)16 * nrhs, st);
+  void* scratch = ws->red;
+  HELM_CUDA(cudaMemsetAsync(H.p, 0, hsz * nrhs * sizeof(S), st));
+  HELM_CUDA(cudaMemsetAsync(cs.p, 0, (size_t)mi * nrhs * sizeof(S), st));
+  HELM_CUDA(cudaMemsetAsync(sn.p, 0, (size_t)mi * nrhs * sizeof(S), st));
+  HELM_CUDA(cudaMemsetAsync(g.p, 0, (size_t)(mi + 1) * nrhs * sizeof(S), st));
+  std::vector<double> hs((size_t)16 * nrhs);
+  auto read_all = [&]() {
+    HELM_CUDA(cudaMemcpyAsync(hs.data(), scal.p, hs.size() * sizeof(double), cudaMemcpyDeviceToHost, st));
+    HELM_CUDA(cudaStreamSynchronize(st));
+  };
+  auto vec = [&](int j, int q) { return Vp + ((size_t)j * nrhs + q) * N; };
+  auto applyM = [&](const S* in, S* out, int nb) {
+    if (use_precond) op_apply_M<S>(P, ws, in, out, nb, st);
+    else HELM_CUDA(cudaMemcpyAsync(out, in, (size_t)nb * N * sizeof(S), cudaMemcpyDeviceToDevice, st));
+  };
+  // r0 = b (right) or M b (left), beta, V[0] = r0 / beta, g[0] = beta (gmres.py:77-96)
+  if (left) applyM(B, Vp, nrhs);
+  else HELM_CUDA(cudaMemcpyAsync(Vp, B, NB * sizeof(S), cudaMemcpyDeviceToDevice, st));
+  for (int q = 0; q < nrhs; ++q) {
+    krylov_norm2<S>(B + (size_t)q * N, N, scal.p + 16 * q, scratch, st);
+    krylov_norm2<S>(vec(0, q), N, scal.p + 16 * q + 1, scratch, st);
+  }
+  read_all();
+  std::vector<double> bnorm(nrhs), beta(nrhs);
+  std::vector<char> active(nrhs, 1);
+  for (int q = 0; q < nrhs; ++q) {
+    bnorm[q] = std::sqrt(hs[16 * q]);
+    beta[q] = std::sqrt(hs[16 * q + 1]);
+    HELM_CHECK(bnorm[q] != 0.0, "right-hand side must be nonzero");
+    const double sc = 1.0 / beta[q];
+    HELM_CUDA(cudaMemcpyAsync(scal.p + 16 * q + 6, &sc, sizeof(double), cudaMemcpyHostToDevice, st));
+    krylov_scale<S>(vec(0, q), vec(0, q), scal.p + 16 * q + 6, 0, N, st);
+    const S g0 = Sc<S>::from_real(beta[q]);
+    HELM_CUDA(cudaMemcpyAsync(g.p + (size_t)(mi + 1) * q, &g0, sizeof(S), cudaMemcpyHostToDevice, st));
+    if (history) history[(size_t)q * (mi + 1)] = 1.0;
+    HELM_CUDA(cudaStreamSynchronize(st));  // the host scalars above are read by the copies
+  }
+  auto form = [&](int q, int j) {  // x_q from the first j+1 basis vectors, true relative residual (gmres.py:98-105, 153)
+    S* Hq = H.p + hsz * q;
+    S* gq = g.p + (size_t)(mi + 1) * q;
+    S* xq = X + (size_t)q * N;
+    krylov_backsolve<S>(Hq, mi, j, gq, y.p, st);
+    if (left) {
+      krylov_combine<S>(xq, Vp + (size_t)q * N, j + 1, NB, y.p, N, st);
+    } else {
+      krylov_combine<S>(r.p, Vp + (size_t)q * N, j + 1, NB, y.p, N, st);
+      applyM(r.p, xq, 1);
+    }
+    launch_stencil<S>(P->geo, B + (size_t)q * N, xq, r.p, 1, st);
+    krylov_norm2<S>(r.p, N, scal.p + 16 * q + 8, scratch, st);
+    double t = 0.0;
+    HELM_CUDA(cudaMemcpyAsync(&t, scal.p + 16 * q + 8, sizeof(double), cudaMemcpyDeviceToHost, st));
+    HELM_CUDA(cudaStreamSynchronize(st));
+    return std::sqrt(t) / bnorm[q];
+  };
+  auto record = [&](int q, int it, bool conv, bool brk, double true_rel) {
+    reps[q].iterations = it;
+    reps[q].converged = conv;
+    reps[q].breakdown = brk && !conv;
+    reps[q].final_residual = true_rel;
+    active[q] = 0;
+  };
+  int nact = nrhs;
+  for (int j = 0; j < mi && nact > 0; ++j) {
+    ensure_basis(j + 2);
+    // the whole batch through the operator: right A M V[j], left M A V[j]
+    if (left) {
+      op_apply_A<S>(P, vec(j, 0), u.p, nrhs, st);
+      applyM(u.p, vec(j + 1, 0), nrhs);
+    } else {
+      applyM(vec(j, 0), u.p, nrhs);
+      op_apply_A<S>(P, u.p, vec(j + 1, 0), nrhs, st);
+    }
+    for (int q = 0; q < nrhs; ++q) {
+      if (!active[q]) {
+        HELM_CUDA(cudaMemsetAsync(vec(j + 1, q), 0, vbytes, st));  // keeps the ride-along input finite
+        continue;
+      }
+      S* Hq = H.p + hsz * q;
+      krylov_cgs2_impl<S>(Vp + (size_t)q * N, j, NB, N, Hq + j, (size_t)mi, scal.p + 16 * q + 2, scratch, st, Hq, mi,
+                          cs.p + (size_t)mi * q, sn.p + (size_t)mi * q, g.p + (size_t)(mi + 1) * q, beta[q],
+                          scal.p + 16 * q + 4);
+    }
+    read_all();
+    for (int q = 0; q < nrhs; ++q) {
+      if (!active[q]) continue;
+      const bool brk = hs[16 * q + 3] != 0.0;
+      const double est = hs[16 * q + 4];
+      if (history) history[(size_t)q * (mi + 1) + j + 1] = est;
+      if (est <= rtol || brk) {  // gmres.py:149-165
+        const double true_rel = form(q, j);
+        const bool conv = left ? est <= rtol : true_rel <= rtol;
+        if (conv || brk) record(q, j + 1, conv, brk, true_rel);
+      }
+      if (active[q] && j + 1 == mi) record(q, mi, false, false, form(q, mi - 1));  // gmres.py:173-177
+      if (!active[q]) --nact;
+    }
+  }
+  HELM_CUDA(cudaStreamSynchronize(st));
+  const double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  for (int q = 0; q < nrhs; ++q) reps[q].wall_seconds = wall;
+}
+
+// ---------------------------------------------------------------------------
 // plan construction
 // ---------------------------------------------------------------------------
 static void build_plan(const helm_desc* d, helm_plan* P) {
@@ -768,6 +902,20 @@ int helm_gmres(const helm_plan* P, helm_workspace* ws, const void* b, void* x, d
       using S = decltype(t);
       gmres_impl<S>(P, ws, (const S*)b, (S*)x, rtol, max_iter, side, use_precond, history, report,
                     (cudaStream_t)stream);
+    });
+  });
+}
+
+int helm_gmres_multi(const helm_plan* P, helm_workspace* ws, const void* b, void* x, int32_t nrhs, double rtol,
+                     int32_t max_iter, int32_t side, int32_t use_precond, double* history, helm_gmres_report* reports,
+                     void* stream) {
+  return guarded([&] {
+    HELM_CHECK(P && ws && b && x && reports, "bad arguments");
+    HELM_CHECK(b != x, "gmres: b and x must not alias");
+    dispatch(P, [&](auto t) {
+      using S = decltype(t);
+      gmres_multi_impl<S>(P, ws, (const S*)b, (S*)x, nrhs, rtol, max_iter, side, use_precond, history, reports,
+                          (cudaStream_t)stream);
     });
   });
 }

@@ -20,7 +20,7 @@ import torch
 from . import _lib
 from .operators import HelmholtzOperator, SchwarzPreconditioner, _as_operator, _ptr, _stream, _Vec
 
-__all__ = ["GmresConfig", "SolveReport", "gmres"]
+__all__ = ["GmresConfig", "SolveReport", "gmres", "gmres_multi"]
 
 
 @dataclass(frozen=True)
@@ -92,3 +92,55 @@ def gmres(A, M_inv, b, cfg: GmresConfig = GmresConfig()) -> SolveReport:
         wall_seconds=float(rep.wall_seconds),
         x=v.out(x),
     )
+
+
+def gmres_multi(A, M_inv, B, cfg: GmresConfig = GmresConfig()) -> list:
+    """Solve A x_r = b_r for the rows b_r of ``B`` ([nrhs, N]) with one GMRES per right-hand
+    side (the reference's loop, gmres.py:65-177, for each) sharing every application of A and
+    M^{-1} (``helm_gmres_multi``: the batched kernels at batch nrhs).  ``M_inv`` needs
+    ``max_batch >= nrhs``.  Returns one SolveReport per row; ``wall_seconds`` is the whole
+    call's.  Not in the reference."""
+    if M_inv is not None and not isinstance(M_inv, SchwarzPreconditioner):
+        raise TypeError("device GMRES needs M_inv to be a SchwarzPreconditioner of this package (or None)")
+    if M_inv is not None:
+        plan, use_precond = M_inv.plan, 1
+        op = M_inv.A
+    else:
+        if isinstance(A, HelmholtzOperator):
+            op = A
+        else:
+            raise TypeError("with M_inv=None, A must be a HelmholtzOperator")
+        plan, use_precond = op._stencil_plan(), 0
+    v = _Vec(B, op.N, op.torch_dtype)
+    if v.t.dim() != 2:
+        raise ValueError("gmres_multi expects right-hand sides as rows of a [nrhs, N] array")
+    nrhs = v.batch
+    if M_inv is not None and nrhs > M_inv.max_batch:
+        raise ValueError(f"{nrhs} right-hand sides exceed the preconditioner's max_batch {M_inv.max_batch}")
+    x = torch.empty_like(v.t)
+    hist = np.zeros((nrhs, cfg.max_iter + 1))
+    reps = (_lib.HelmGmresReport * nrhs)()
+    with plan.lock:
+        status = plan.lib.helm_gmres_multi(
+            plan.handle, plan.ws, _ptr(v.t), _ptr(x), nrhs, float(cfg.rtol), int(cfg.max_iter),
+            1 if cfg.side == "left" else 0, use_precond,
+            hist.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), reps, _stream(),
+        )
+    if status != 0:
+        msg = plan.lib.helm_last_error().decode(errors="replace")
+        if "nonzero" in msg:
+            raise ValueError(msg)
+        raise _lib.HelmError(msg)
+    xs = v.out(x)
+    return [
+        SolveReport(
+            iterations=reps[q].iterations,
+            converged=bool(reps[q].converged),
+            residual_history=hist[q, : reps[q].iterations + 1].copy(),
+            final_residual=float(reps[q].final_residual),
+            breakdown=bool(reps[q].breakdown),
+            wall_seconds=float(reps[q].wall_seconds),
+            x=xs[q],
+        )
+        for q in range(nrhs)
+    ]
