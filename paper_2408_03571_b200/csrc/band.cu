@@ -286,14 +286,6 @@ static int band_seg_max_batch() {
   return v;
 }
 
-static int band_cfg() {
-  static int v = [] {
-    const char* e = std::getenv("HELM_BAND_CFG");
-    return e ? std::atoi(e) : 0;
-  }();
-  return v;
-}
-
 void launch_band_solve(const helm_plan* P, const double2* in, double2* out, const double2* corr, int batch,
                        cudaStream_t st, const double2* add) {
   HELM_CHECK(P->dev.band_piv != nullptr, "plan has no band factors");
@@ -306,19 +298,9 @@ void launch_band_solve(const helm_plan* P, const double2* in, double2* out, cons
     band_launch<1, 1, 8, 4>(P, in, out, corr, batch, st, add);  // latency-bound recurrence
   else if (batch <= 4)
     band_launch<2, 2, 8, 3>(P, in, out, corr, batch, st, add);
-  else {
-    switch (band_cfg()) {
-      case 1: band_launch<1, 4, 8, 3>(P, in, out, corr, batch, st, add); break;
-      case 2: band_launch<2, 4, 8, 3>(P, in, out, corr, batch, st, add); break;
-      case 3: band_launch<1, 2, 8, 4>(P, in, out, corr, batch, st, add); break;
-      case 4: band_launch<2, 2, 8, 3>(P, in, out, corr, batch, st, add); break;
-      case 5: band_launch<4, 2, 8, 3>(P, in, out, corr, batch, st, add); break;
-      case 6: band_launch<2, 8, 4, 3>(P, in, out, corr, batch, st, add); break;
-      case 7: band_launch<1, 16, 4, 3>(P, in, out, corr, batch, st, add); break;
-      case 8: band_launch<1, 16, 8, 2>(P, in, out, corr, batch, st, add); break;
-      default: band_launch<1, 8, 8, 3>(P, in, out, corr, batch, st, add);  // 8 warps (8 right-hand sides) share each factor read
-    }
-  }
+  else  // 8 warps (8 right-hand sides) share each factor read; 4-16 per CTA and 4-8 rows per
+        // stage were measured slower
+    band_launch<1, 8, 8, 3>(P, in, out, corr, batch, st, add);
 }
 
 }  // namespace helm
