@@ -344,7 +344,9 @@ class SchwarzPreconditioner:
 
     __call__ = apply
 
-    PIPE_CHUNK = 8
+    # vectors per pipeline chunk; smaller chunks shorten the unoverlapped first H2D and last D2H
+    # (config 5, 32 vectors: 2 -> 627, 4 -> 619, 8 -> 570, 16 -> 494 applies/s, tools/e2e_chunk.py)
+    PIPE_CHUNK = 2
 
     def _apply_pipelined(self, xh: torch.Tensor, yh: torch.Tensor):
         """Host batch -> host batch with the PCIe copies overlapped with the kernels.
