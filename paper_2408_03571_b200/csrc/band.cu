@@ -83,7 +83,7 @@ __global__ void __launch_bounds__(BW* NW) band_solve_kernel(const double2* __res
     for (int rr = w; rr < R; rr += NW) {
       const int j = c * R + rr;
       const bool ok = va && j < m0;
-      const size_t f = (size_t)(j < m0 ? j : 0) * m0 + (va ? a : 0);
+      const size_t f = fac_idx(j < m0 ? j : 0, va ? a : 0, m0);
       cp_async16(&S.L[rr][t][0], L + 2 * f, ok);
       cp_async16(&S.L[rr][t][1], L + 2 * f + 1, ok);
       if (!NOPIV) cp_async4(&S.piv[rr][t], piv + f, ok);
@@ -175,7 +175,7 @@ __global__ void __launch_bounds__(BW* NW) band_solve_kernel(const double2* __res
     for (int rr = w; rr < R; rr += NW) {
       const int j = m0 - 1 - (c * R + rr);
       const bool ok = va && j >= 0;
-      const double2* u = U + UE * ((size_t)(j >= 0 ? j : 0) * m0 + (va ? a : 0));
+      const double2* u = U + UE * fac_idx(j >= 0 ? j : 0, va ? a : 0, m0);
 #pragma unroll
       for (int e = 0; e < UE; ++e) cp_async16(&S.U[rr][t][e], u + e, ok);
     }

@@ -96,7 +96,7 @@ __device__ __forceinline__ void fwd_run(const SegRhs& rhs, const int* __restrict
 #pragma unroll
     for (int c = 0; c < C; ++c) {
       const bool ok = j + c < j1;
-      const size_t e = (size_t)(ok ? j + c : j0) * m0 + a;
+      const size_t e = fac_idx(ok ? j + c : j0, a, m0);
       ch.pv[c] = NOPIV ? 0 : __ldg(piv + e);
       ch.l0[c] = __ldg(L + 2 * e);
       ch.l1[c] = __ldg(L + 2 * e + 1);
@@ -137,7 +137,7 @@ __device__ __forceinline__ void bwd_run(const double2* __restrict__ U, int m0, i
 #pragma unroll
     for (int c = 0; c < C; ++c) {
       const int r = j - c >= j0 ? j - c : j1 - 1;
-      const double2* u = U + UE * ((size_t)r * m0 + a);
+      const double2* u = U + UE * fac_idx(r, a, m0);
 #pragma unroll
       for (int e = 0; e < UE; ++e) ch.u[c][e] = __ldg(u + e);
       ch.ad[c] = addp ? __ldg(addp + (size_t)r * m0) : mk(0.0, 0.0);

@@ -483,30 +483,37 @@ static void build_plan(const helm_desc* d, helm_plan* P) {
     dv.m0_band = upload_bytes(d->m0_band, m0 * 5 * P->elem);
     if (d->bc == HELM_SOMMERFELD) {
       HELM_CHECK(d->band_piv && d->band_l && d->band_u, "Sommerfeld coarse solver needs the band factors");
-      std::vector<int> piv32(d->band_piv, d->band_piv + m0 * m0);
+      // factors re-laid out blocked by 32 modes (fac_idx): entry (j, a) of the host's [j][a]
+      const size_t mm = (size_t)m0 * m0, fe = fac_elems((int)m0);
+      std::vector<int> piv32(fe, 0);
+      for (size_t j = 0; j < m0; ++j)
+        for (size_t a = 0; a < m0; ++a) piv32[fac_idx((int)j, (int)a, (int)m0)] = d->band_piv[j * m0 + a];
       dv.band_piv = upload<int>(piv32.data(), piv32.size());
       // no pivot taken (and hence no fill in U): rows {1/U_jj, U_j,j+1, U_j,j+2} only
-      const size_t mm = (size_t)m0 * m0;
       const double2* uh = static_cast<const double2*>(d->band_u);
-      bool nopiv = P->elem == sizeof(double2) && !env_flag_off("HELM_BAND_NOPIV");
+      const double2* lh = static_cast<const double2*>(d->band_l);
+      HELM_CHECK(P->elem == sizeof(double2), "Sommerfeld band factors are complex128");
+      bool nopiv = !env_flag_off("HELM_BAND_NOPIV");
       for (size_t e = 0; nopiv && e < mm; ++e)
         nopiv = d->band_piv[e] == 0 && uh[5 * e + 3].x == 0.0 && uh[5 * e + 3].y == 0.0 && uh[5 * e + 4].x == 0.0 &&
                 uh[5 * e + 4].y == 0.0;
       const int ue = nopiv ? 3 : 5;
       dv.band_nopiv = nopiv ? 1 : 0;
-      dv.band_fac_bytes = mm * (2 + ue) * P->elem;
+      dv.band_fac_bytes = fe * (2 + ue) * P->elem;
+      std::vector<double2> hb(fe * (2 + ue), make_double2(0.0, 0.0));
+      double2* lb = hb.data();
+      double2* ub = hb.data() + fe * 2;
+      for (size_t j = 0; j < m0; ++j)
+        for (size_t a = 0; a < m0; ++a) {
+          const size_t src = j * m0 + a, dst = fac_idx((int)j, (int)a, (int)m0);
+          lb[2 * dst] = lh[2 * src];
+          lb[2 * dst + 1] = lh[2 * src + 1];
+          for (int i = 0; i < ue; ++i) ub[ue * dst + i] = uh[5 * src + i];
+        }
       HELM_CUDA(cudaMalloc(&dv.band_fac, dv.band_fac_bytes));
       dv.band_l = dv.band_fac;
-      dv.band_u = static_cast<char*>(dv.band_fac) + mm * 2 * P->elem;
-      HELM_CUDA(cudaMemcpy(dv.band_l, d->band_l, mm * 2 * P->elem, cudaMemcpyHostToDevice));
-      if (nopiv) {
-        std::vector<double2> uc(mm * 3);
-        for (size_t e = 0; e < mm; ++e)
-          for (int i = 0; i < 3; ++i) uc[3 * e + i] = uh[5 * e + i];
-        HELM_CUDA(cudaMemcpy(dv.band_u, uc.data(), mm * 3 * sizeof(double2), cudaMemcpyHostToDevice));
-      } else {
-        HELM_CUDA(cudaMemcpy(dv.band_u, d->band_u, mm * 5 * P->elem, cudaMemcpyHostToDevice));
-      }
+      dv.band_u = static_cast<char*>(dv.band_fac) + fe * 2 * P->elem;
+      HELM_CUDA(cudaMemcpy(dv.band_fac, hb.data(), dv.band_fac_bytes, cudaMemcpyHostToDevice));
       if (band_seg_usable(m0)) {
         HELM_CUDA(cudaMalloc(&dv.band_seg, band_seg_table_elems(m0) * sizeof(double2)));
         band_seg_setup(dv, dv.band_seg, 0);

@@ -299,6 +299,14 @@ inline void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t sme
   HELM_CUDA(cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...));
 }
 
+// Band-factor entry (row j, mode a): blocked by 32 modes, so the factors of the modes one
+// CTA owns are contiguous (0.26-0.39 MB per block at m0 = 1025 instead of a 34-50 MB
+// stride-m0 span: a handful of pages per SM at a time)
+__host__ __device__ __forceinline__ size_t fac_idx(int j, int a, int m0) {
+  return ((size_t)(a >> 5) * m0 + j) * 32 + (a & 31);
+}
+__host__ __device__ __forceinline__ size_t fac_elems(int m0) { return (size_t)((m0 + 31) / 32) * 32 * m0; }
+
 // cp.async (Ampere+) helpers: src-size 0 zero-fills without reading
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool pred) {
   const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
