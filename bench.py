@@ -297,7 +297,8 @@ def run_ours(a, rank, world, local_rank):
         # inside the run (below it every iteration also forms x and checks the true residual)
         cfg = hb.GmresConfig(rtol=1e-300, max_iter=a.gmres)
         hb.gmres(prob.A, M, brnd, cfg)  # warm
-        rep = hb.gmres(prob.A, M, brnd, cfg)
+        with ClockSampler(local_rank) as gclk:
+            rep = hb.gmres(prob.A, M, brnd, cfg)
         t_iter = rep.wall_seconds / rep.iterations
         Ns = N * 16
         t_roof = sum(composite_roof(model, bw, FP64_PEAK_TFLOPS) + (2 * Ns + (3 * (j + 1) + 4) * Ns) / (bw * 1e9)
@@ -306,7 +307,8 @@ def run_ours(a, rank, world, local_rank):
                    "fixed_iter_per_s": round(rep.iterations / rep.wall_seconds, 2),
                    "fixed_ms_per_iter": round(t_iter * 1e3, 4),
                    "roofline": {"T_roof_ms_per_iter": round(t_roof * 1e3, 4), "frac": round(t_roof / t_iter, 4),
-                                "note": "mean over the run of max-phase roofline of M^-1 + A x + CGS2 at basis j+1"}})
+                                "note": "mean over the run of max-phase roofline of M^-1 + A x + CGS2 at basis j+1"},
+                   "fixed_clocks": gclk.summary()})
         # (3) multi-right-hand-side GMRES (helm_gmres_multi): 8 seed-0 random
         # right-hand sides, the same fixed-length run, operators applied to the batch of 8
         nr = min(8, B)
