@@ -35,7 +35,7 @@ namespace helm {
 // Woodbury strip step
 // ----------------------------------------------------------------------------
 // Z[y][b*4+i] = sum_a q[a][i] Yh[b][y][a]   (one warp per (batch, row))
-constexpr int SCH = 16;  // row elements per lane in flight (strip kernels)
+constexpr int SCH = 8;  // row elements per lane in flight (strip reduction)
 template <typename S>
 __global__ void __launch_bounds__(256) strip_reduce_kernel(const S* __restrict__ Yh, const double* __restrict__ q,
                                                            S* __restrict__ Z, int m0, int ldz) {
@@ -48,24 +48,23 @@ __global__ void __launch_bounds__(256) strip_reduce_kernel(const S* __restrict__
   S acc[4] = {Sc<S>::zero(), Sc<S>::zero(), Sc<S>::zero(), Sc<S>::zero()};
   // chunks of SCH elements per lane are loaded before they are summed (all loads of a
   // chunk in flight); the summation order per lane is a = lane, lane + 32, ... as before
+  // (q, 33 KB, is read through L1 at use: only the streamed row is held in registers)
   for (int a0 = lane; a0 < m0; a0 += 32 * SCH) {
     S v[SCH];
-    double4 qv[SCH];
+#pragma unroll
+    for (int i = 0; i < SCH; ++i) {
+      const int a = a0 + 32 * i;
+      if (a < m0) v[i] = row[a];
+    }
 #pragma unroll
     for (int i = 0; i < SCH; ++i) {
       const int a = a0 + 32 * i;
       if (a < m0) {
-        v[i] = row[a];
-        qv[i] = *reinterpret_cast<const double4*>(q + (size_t)a * 4);
-      }
-    }
-#pragma unroll
-    for (int i = 0; i < SCH; ++i) {
-      if (a0 + 32 * i < m0) {
-        acc[0] = fma_(qv[i].x, v[i], acc[0]);
-        acc[1] = fma_(qv[i].y, v[i], acc[1]);
-        acc[2] = fma_(qv[i].z, v[i], acc[2]);
-        acc[3] = fma_(qv[i].w, v[i], acc[3]);
+        const double4 qa = *reinterpret_cast<const double4*>(q + (size_t)a * 4);
+        acc[0] = fma_(qa.x, v[i], acc[0]);
+        acc[1] = fma_(qa.y, v[i], acc[1]);
+        acc[2] = fma_(qa.z, v[i], acc[2]);
+        acc[3] = fma_(qa.w, v[i], acc[3]);
       }
     }
   }
