@@ -94,3 +94,24 @@ def test_multi_cap_and_errors():
         Z = B.copy()
         Z[1] = 0
         hb.gmres_multi(prob.A, Ms["SHS2"], Z, hb.GmresConfig())
+
+
+def test_multi_wide_batch_uses_the_batched_coarse_kernels():
+    """Six right-hand sides: the coarse solve runs the lane-per-mode band kernel and the tiled
+    strip GEMMs (batch >= 5) inside GMRES; every right-hand side still matches its own solve."""
+    import paper_2408_03571_b200 as hb
+
+    grid = hb.Grid(129, "sommerfeld")
+    prob = hb.assemble(grid, 30.0, "MP2")
+    dec = hb.extend(hb.partition(grid, 8), 2)
+    M = hb.SchwarzPreconditioner("SHS2", prob.A, dec, hb.galerkin(hb.build_hocs(grid, 2), prob.A), max_batch=8)
+    r = np.random.default_rng(5)
+    B = r.standard_normal((6, prob.A.N)) + 1j * r.standard_normal((6, prob.A.N))
+    cfg = hb.GmresConfig(rtol=1e-6, max_iter=300)
+    reps = hb.gmres_multi(prob.A, M, B, cfg)
+    for q, rep in enumerate(reps):
+        single = hb.gmres(prob.A, M, B[q], cfg)
+        assert rep.converged and single.converged
+        assert abs(rep.iterations - single.iterations) <= 1, (q, rep.iterations, single.iterations)
+        assert rel(rep.x, single.x) <= X_TOL
+        assert rep.final_residual <= 1e-6

@@ -274,3 +274,24 @@ def test_left_preconditioned_gmres_matches_oracle(problem, n, k, p):
     assert rep.converged == orep.converged and rep.iterations == orep.iterations
     assert np.all(np.abs(rep.residual_history - orep.residual_history) <= 1e-6 * orep.residual_history + 1e-14)
     assert rel(rep.x, orep.x) <= X_TOL
+
+
+def test_compact_band_factors_match_the_general_path(monkeypatch):
+    """No pivot taken: the plan stores U rows of 3 entries and skips the pivot reads
+    (PlanDev::band_nopiv).  The skipped terms are exact zeros, so M^-1 is bitwise the same as
+    with the general 5-entry rows and pivots (HELM_BAND_NOPIV=0), at batch 1 (segmented band
+    solve) and batch 6 (lane-per-mode band solve)."""
+    import paper_2408_03571_b200 as hb
+
+    grid = hb.Grid(257, "sommerfeld")
+    prob = hb.assemble(grid, 50.0, "MP2")
+    dec = hb.extend(hb.partition(grid, 8), 2)
+    cs = hb.galerkin(hb.build_hocs(grid, 2), prob.A)
+    rng = np.random.default_rng(3)
+    X = torch.from_numpy(rng.standard_normal((6, prob.A.N)) + 1j * rng.standard_normal((6, prob.A.N))).cuda()
+    M1 = hb.SchwarzPreconditioner("SHS2", prob.A, dec, cs, max_batch=6)
+    monkeypatch.setenv("HELM_BAND_NOPIV", "0")
+    M0 = hb.SchwarzPreconditioner("SHS2", prob.A, dec, cs, max_batch=6)
+    monkeypatch.delenv("HELM_BAND_NOPIV")
+    for Xb in (X[:1], X):
+        assert torch.equal(M1(Xb), M0(Xb))
