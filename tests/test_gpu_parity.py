@@ -295,3 +295,33 @@ def test_compact_band_factors_match_the_general_path(monkeypatch):
     monkeypatch.delenv("HELM_BAND_NOPIV")
     for Xb in (X[:1], X):
         assert torch.equal(M1(Xb), M0(Xb))
+
+
+@pytest.mark.parametrize("problem,n,k,p", [("MP2", 33, 10.0, 4), ("MP1", 33, 6.0, 4), ("MP2", 65, 15.0, 4)])
+def test_maximal_overlap_matches_oracle(problem, n, k, p):
+    """extend_max (decomposition.py:106-108,137-139: m = c // 2, the largest overlap with at most
+    two boxes per node per axis) on the device against the CPU oracle: every
+    preconditioner kind to 1e-12, SHS2-GMRES count and solution."""
+    import sys, os
+
+    sys.path.insert(0, os.path.join(os.path.dirname(__file__), "..", "oracle"))
+    import helmdd_oracle as O  # checker only
+    import paper_2408_03571_b200 as hb
+
+    grid = hb.Grid(n, "dirichlet" if problem == "MP1" else "sommerfeld")
+    prob = hb.assemble(grid, k, problem)
+    part = hb.partition(grid, p)
+    dec = hb.extend_max(part)
+    m = hb.max_overlap_layers(part)
+    cs = hb.galerkin(hb.build_hocs(grid, 2), prob.A)
+    x = operator_input(prob.A.N, problem == "MP2")
+    for kind in ("SHS2", "AS2", "SAS2"):
+        M = hb.SchwarzPreconditioner(kind, prob.A, dec, cs)
+        oprob, odec, ocs, oM = O.build_shs2(n, k, problem, p, m, kind=kind)
+        assert rel(M(x), oM(x)) <= OP_TOL, (kind, rel(M(x), oM(x)))
+    M = hb.SchwarzPreconditioner("SHS2", prob.A, dec, cs)
+    oprob, odec, ocs, oM = O.build_shs2(n, k, problem, p, m)
+    rep = hb.gmres(prob.A, M, prob.f, hb.GmresConfig(rtol=1e-6, max_iter=500))
+    orep = O.gmres(oprob.A, oM, oprob.f, 1e-6, 500)
+    assert rep.converged and rep.iterations == orep.iterations, (rep.iterations, orep.iterations)
+    assert rel(rep.x, orep.x) <= X_TOL
