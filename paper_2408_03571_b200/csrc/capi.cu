@@ -765,7 +765,13 @@ int helm_workspace_create(const helm_plan* P, int32_t max_batch, helm_workspace*
     HELM_CUDA(cudaMalloc(&w->red, w->red_bytes));
     HELM_CUDA(cudaMemset(w->red, 0, w->red_bytes));  // the CGS2 completion counters start at zero
     HELM_CUDA(cudaMallocHost(&w->pinned, 64 * sizeof(double)));
-    HELM_CUDA(cudaStreamCreateWithFlags(&w->side, cudaStreamNonBlocking));
+    // the side stream carries the long-latency boundary-box solves beside the tensor-core
+    // boxes; the highest priority lets their CTAs take SM slots ahead of the many short ones
+    int prio_lo = 0, prio_hi = 0;
+    HELM_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+    const char* pe = std::getenv("HELM_SIDE_PRIO");
+    const int prio = (pe && pe[0] == '0') ? prio_lo : prio_hi;
+    HELM_CUDA(cudaStreamCreateWithPriority(&w->side, cudaStreamNonBlocking, prio));
     HELM_CUDA(cudaEventCreateWithFlags(&w->fork, cudaEventDisableTiming));
     HELM_CUDA(cudaEventCreateWithFlags(&w->join, cudaEventDisableTiming));
     *out = w;
