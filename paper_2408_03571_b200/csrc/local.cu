@@ -115,14 +115,11 @@ __global__ void __launch_bounds__(256) local_fdm_kernel(const S* __restrict__ x,
 // Combine the overlap-band contributions: rows with y-multiplicity 2 (all x),
 // then columns with x-multiplicity 2 in rows of y-multiplicity 1.
 template <typename S>
-__global__ void combine_rows_kernel(const S* __restrict__ base, S* __restrict__ y, const S* __restrict__ ovl,
-                                    const int* __restrict__ band_node, const int* __restrict__ node_mult,
-                                    int nu, int nbands, LocalArgs a) {
-  pdl_wait();  // PDL: the predecessor's writes are visible (no-op without PDL)
-  const int ix = blockIdx.x * blockDim.x + threadIdx.x;
-  const int bi = blockIdx.y;
+__device__ __forceinline__ void combine_row(const S* __restrict__ base, S* __restrict__ y, const S* __restrict__ ovl,
+                                            const int* __restrict__ band_node, const int* __restrict__ node_mult,
+                                            int nu, int nbands, const LocalArgs& a, int bx, int bi, int b) {
+  const int ix = bx * blockDim.x + threadIdx.x;
   if (ix >= nu) return;
-  const int b = blockIdx.z;
   const size_t N = (size_t)nu * nu;
   const S* ob = ovl + (size_t)b * 6 * nbands * nu;
   const int iy = band_node[bi];
@@ -138,14 +135,11 @@ __global__ void combine_rows_kernel(const S* __restrict__ base, S* __restrict__ 
 }
 
 template <typename S>
-__global__ void combine_cols_kernel(const S* __restrict__ base, S* __restrict__ y, const S* __restrict__ ovl,
-                                    const int* __restrict__ band_node, const int* __restrict__ node_mult,
-                                    int nu, int nbands, LocalArgs a) {
-  pdl_wait();  // PDL: the predecessor's writes are visible (no-op without PDL)
-  const int bi = blockIdx.x * blockDim.x + threadIdx.x;
-  const int iy = blockIdx.y;
+__device__ __forceinline__ void combine_col(const S* __restrict__ base, S* __restrict__ y, const S* __restrict__ ovl,
+                                            const int* __restrict__ band_node, const int* __restrict__ node_mult,
+                                            int nu, int nbands, const LocalArgs& a, int bx, int iy, int b) {
+  const int bi = bx * blockDim.x + threadIdx.x;
   if (bi >= nbands || node_mult[iy] != 1) return;
-  const int b = blockIdx.z;
   const size_t N = (size_t)nu * nu;
   const S* ob = ovl + (size_t)b * 6 * nbands * nu + (size_t)4 * nbands * nu;
   S acc = add(ob[((size_t)0 * nu + iy) * nbands + bi], ob[((size_t)1 * nu + iy) * nbands + bi]);
@@ -154,6 +148,21 @@ __global__ void combine_cols_kernel(const S* __restrict__ base, S* __restrict__ 
   y[b * N + pidx] = base ? add(base_at(base + b * base_stride(a), a, iy, ix), acc) : acc;
 }
 
+
+// Both combines in one launch: the row-band and column-band node sets are disjoint (column
+// bands only in rows of y-multiplicity 1), so the first nrb blocks do rows, the rest columns.
+template <typename S>
+__global__ void __launch_bounds__(128) combine_kernel(const S* __restrict__ base, S* __restrict__ y,
+                                                     const S* __restrict__ ovl, const int* __restrict__ band_node,
+                                                     const int* __restrict__ node_mult, int nu, int nbands,
+                                                     LocalArgs a, int rbx, int cbx) {
+  pdl_wait();  // PDL: the predecessor's writes are visible (no-op without PDL)
+  const int b = blockIdx.y;
+  const int nrb = rbx * nbands;
+  const int e = blockIdx.x;
+  if (e < nrb) combine_row(base, y, ovl, band_node, node_mult, nu, nbands, a, e % rbx, e / rbx, b);
+  else combine_col(base, y, ovl, band_node, node_mult, nu, nbands, a, (e - nrb) % cbx, (e - nrb) / cbx, b);
+}
 
 size_t local_smem_bytes(int ld, size_t elem) { return (size_t)(4 * ld * ld + 2 * ld) * elem; }
 
@@ -195,11 +204,9 @@ void launch_local_sum(const helm_plan* P, const S* x, const S* base, S* y, S* ov
     HELM_LAUNCH_CHECK();
   }
   if (d.nbands > 0) {
-    dim3 g1((a.nu + 127) / 128, d.nbands, batch);
-    launch_pdl(combine_rows_kernel<S>, g1, 128, 0, st, base, y, ovl, band_node, d.node_mult, a.nu, d.nbands, a);
-    HELM_LAUNCH_CHECK();
-    dim3 g2((d.nbands + 127) / 128, a.nu, batch);
-    launch_pdl(combine_cols_kernel<S>, g2, 128, 0, st, base, y, ovl, band_node, d.node_mult, a.nu, d.nbands, a);
+    const int rbx = (a.nu + 127) / 128, cbx = (d.nbands + 127) / 128;
+    dim3 g((unsigned)(rbx * d.nbands + cbx * a.nu), batch);
+    launch_pdl(combine_kernel<S>, g, 128, 0, st, base, y, ovl, band_node, d.node_mult, a.nu, d.nbands, a, rbx, cbx);
     HELM_LAUNCH_CHECK();
   }
 }
