@@ -47,7 +47,7 @@
 extern "C" {
 #endif
 
-#define HELM_ABI_VERSION 5
+#define HELM_ABI_VERSION 6
 
 enum helm_bc { HELM_DIRICHLET = 0, HELM_SOMMERFELD = 1 };
 enum helm_kind { HELM_AS2 = 0, HELM_SAS2 = 1, HELM_SHS2 = 2 };
@@ -65,7 +65,7 @@ typedef struct helm_desc {
   int32_t weights_before_solve; /* schwarz.py:69-70                               */
   int32_t p;             /* subdomains per dimension (decomposition.py:89-103)    */
   int32_t overlap_layers;/* m of extend(part, m) (decomposition.py:111-134)       */
-  int32_t ratio;         /* coarse ratio H/h; only 2 is implemented               */
+  int32_t ratio;         /* coarse ratio H/h (coarse.py:77-81)                    */
   double k;              /* wavenumber                                            */
   /* --- 1-D boxes (identical in x and y): box a covers unknowns
    *     [box_start[a], box_start[a] + box_len[a])                               */
@@ -116,6 +116,24 @@ typedef struct helm_desc {
   const void* strip_lm;       /* S [n_strip][n_strip]  (M0 - M~) on the strips    */
   int32_t strip_refine;       /* strip-refinement steps (Sommerfeld; 0..4)        */
   int32_t refine_steps;       /* full iterative-refinement steps r = c - A0 y    */
+  /* --- general coarse spaces (FOCS at any ratio, HOCS at ratio 4/8/16;
+   *     coarse.py:84-151): R0 = P (x) P with a banded 1-D P, and
+   *     A0^{-1} c = (V (x) V) diag(invden) (V (x) V)^T c with T0 V = M0 V diag(lam),
+   *     V^T M0 V = I, followed by refine_steps iterative-refinement steps on
+   *     A0 = T0(x)M0 + M0(x)T0 - k^2 M0(x)M0.  coarse_V == NULL -> the HOCS ratio-2
+   *     fast solver above (coarse_scale ...).                                        */
+  int32_t coarse_kind;        /* 0: HOCS, 1: FOCS                                  */
+  int32_t p_width;            /* taps per row of P                                 */
+  const int32_t* p_start;     /* [m0]  first fine unknown of row I of P            */
+  const double* p_taps;       /* [m0][p_width]  P[I][p_start[I] + t] (zero-padded) */
+  int32_t pt_width;           /* taps per row of P^T                               */
+  const int32_t* pt_start;    /* [nu]  first coarse unknown of row i of P^T        */
+  const double* pt_taps;      /* [nu][pt_width]                                    */
+  int32_t a0_bw;              /* half-bandwidth b of T0 and M0 (1..3)              */
+  const void* a0_t0;          /* S [m0][2b+1]  T0[i][i+d-b]                        */
+  const void* a0_m0;          /* S [m0][2b+1]  M0[i][i+d-b]                        */
+  const void* coarse_V;       /* S [m0][m0]  row-major                             */
+  const void* coarse_invden;  /* S [m0][m0]  1 / (lam[y] + lam[x] - k^2)           */
 } helm_desc;
 
 typedef struct helm_gmres_report {

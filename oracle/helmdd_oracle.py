@@ -228,8 +228,9 @@ class OCoarse:
     lu: object
 
 
-def coarse_space(grid: OGrid, A: sp.csr_matrix, ratio: int = 2, kind: str = "HOCS") -> OCoarse:
-    """build_hocs/build_focs + galerkin — coarse.py:136-167 (symmetrised R0 A R0^T, SuperLU)."""
+def galerkin_matrix(grid: OGrid, A: sp.csr_matrix, ratio: int = 2, kind: str = "HOCS"):
+    """(R0, A0): build_hocs/build_focs + the symmetrised triple product of galerkin —
+    coarse.py:136-139, 154-165 (no factorisation)."""
     P = bezier_1d(grid, ratio) if kind == "HOCS" else hat_1d(grid, ratio)
     R0 = sp.kron(P, P, format="csr")
     R0.sort_indices()
@@ -237,6 +238,12 @@ def coarse_space(grid: OGrid, A: sp.csr_matrix, ratio: int = 2, kind: str = "HOC
     B = sp.csr_matrix(r0c @ A @ r0c.T)
     a0 = ((B + B.T) * 0.5).tocsr()
     a0.sort_indices()
+    return R0, a0
+
+
+def coarse_space(grid: OGrid, A: sp.csr_matrix, ratio: int = 2, kind: str = "HOCS") -> OCoarse:
+    """build_hocs/build_focs + galerkin — coarse.py:136-167 (symmetrised R0 A R0^T, SuperLU)."""
+    R0, a0 = galerkin_matrix(grid, A, ratio, kind)
     return OCoarse(R0, a0, splu(sp.csc_matrix(a0)))
 
 
@@ -298,12 +305,15 @@ class OSchwarz:
     __call__ = apply
 
 
-def build_shs2(n: int, k: float, problem: str, p: int, m: int = 2, ratio: int = 2, kind="SHS2"):
-    """The S1 call stack of SURVEY §3 (README.md:112-121 with extend(part, m), build_hocs(grid, ratio))."""
+def build_shs2(n: int, k: float, problem: str, p: int, m: int = 2, ratio: int = 2, kind="SHS2", coarse="HOCS"):
+    """The S1 call stack of SURVEY §3 (README.md:112-121 with extend(part, m), build_hocs /
+    build_focs(grid, ratio)); m = "max" is extend_max (decomposition.py:137-139)."""
     grid = OGrid(n, "dirichlet" if problem == "MP1" else "sommerfeld")
     prob = assemble(grid, k, problem)
+    if m == "max":
+        m = ((n - 1) // p) // 2
     dec = decompose(grid, p, m)
-    cs = coarse_space(grid, prob.A, ratio)
+    cs = coarse_space(grid, prob.A, ratio, coarse)
     return prob, dec, cs, OSchwarz(kind, prob.A, dec, cs)
 
 

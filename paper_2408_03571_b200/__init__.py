@@ -10,6 +10,7 @@ from .discretization import (
     Decomposition,
     Grid,
     Partition,
+    build_focs,
     build_hocs,
     extend,
     extend_max,
@@ -39,6 +40,7 @@ __all__ = [
     "SingularMatrixError",
     "SolveReport",
     "assemble",
+    "build_focs",
     "build_hocs",
     "coarse_correct",
     "extend",

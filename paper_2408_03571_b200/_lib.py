@@ -15,7 +15,7 @@ LIB_PATH = os.path.join(_HERE, "libhelmb200.so")
 
 HELM_DIRICHLET, HELM_SOMMERFELD = 0, 1
 KINDS = {"AS2": 0, "SAS2": 1, "SHS2": 2}
-ABI_VERSION = 5
+ABI_VERSION = 6
 
 c_int32_p = ctypes.POINTER(ctypes.c_int32)
 
@@ -61,6 +61,18 @@ class HelmDesc(ctypes.Structure):
         ("strip_lm", ctypes.c_void_p),
         ("strip_refine", ctypes.c_int32),
         ("refine_steps", ctypes.c_int32),
+        ("coarse_kind", ctypes.c_int32),
+        ("p_width", ctypes.c_int32),
+        ("p_start", c_int32_p),
+        ("p_taps", ctypes.c_void_p),
+        ("pt_width", ctypes.c_int32),
+        ("pt_start", c_int32_p),
+        ("pt_taps", ctypes.c_void_p),
+        ("a0_bw", ctypes.c_int32),
+        ("a0_t0", ctypes.c_void_p),
+        ("a0_m0", ctypes.c_void_p),
+        ("coarse_V", ctypes.c_void_p),
+        ("coarse_invden", ctypes.c_void_p),
     ]
 
 

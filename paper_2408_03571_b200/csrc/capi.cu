@@ -70,13 +70,35 @@ template <typename S> void op_apply_A(const helm_plan* P, const S* x, S* y, int 
   launch_stencil<S>(P->geo, x, nullptr, y, batch, st);
 }
 
+// R0, R0^T and A0^{-1} for the plan's coarse space: the HOCS ratio-2 kernels (transfer.cu,
+// coarse.cu) or the general banded / dense-FDM ones (coarse_dense.cu)
+template <typename S> static void restrict_any(const helm_plan* P, const S* x, S* c, int batch, cudaStream_t st) {
+  if (P->dev.coarse_dense)
+    launch_restrict_general<S>(P, x, c, batch, st);
+  else
+    launch_restrict<S>(P->geo, x, c, batch, st);
+}
+template <typename S> static void prolong_any(const helm_plan* P, const S* c, S* z, int batch, cudaStream_t st) {
+  if (P->dev.coarse_dense)
+    launch_prolong_general<S>(P, c, z, batch, st);
+  else
+    launch_prolong<S>(P->geo, c, z, batch, st);
+}
+template <typename S>
+static void coarse_solve_any(const helm_plan* P, helm_workspace* ws, const S* c, S* y, int batch, cudaStream_t st) {
+  if (P->dev.coarse_dense)
+    launch_coarse_solve_dense<S>(P, ws, c, y, batch, st);
+  else
+    launch_coarse_solve<S>(P, ws, c, y, batch, st);
+}
+
 template <typename S>
 static void op_coarse_correct(const helm_plan* P, helm_workspace* ws, const S* x, S* z, int batch, cudaStream_t st) {
   S* c = (S*)ws->c;
   S* cy = (S*)ws->y0;  // a distinct output: no copy-back inside the coarse solve
-  launch_restrict<S>(P->geo, x, c, batch, st);
-  launch_coarse_solve<S>(P, ws, c, cy, batch, st);
-  launch_prolong<S>(P->geo, cy, z, batch, st);
+  restrict_any<S>(P, x, c, batch, st);
+  coarse_solve_any<S>(P, ws, c, cy, batch, st);
+  prolong_any<S>(P, cy, z, batch, st);
 }
 
 // SchwarzPreconditioner.apply (schwarz.py:76-103): z = C x shared by every kind
@@ -84,6 +106,21 @@ template <typename S>
 void op_apply_M(const helm_plan* P, helm_workspace* ws, const S* x, S* y, int batch, cudaStream_t st) {
   HELM_CHECK((const void*)x != (const void*)y, "apply_M: input and output must not alias");
   const int kind = P->desc.kind;
+  if (P->dev.coarse_dense) {
+    // general coarse space: z = R0^T A0^{-1} R0 x materialised, then (SHS2) d = x - A z and
+    // y = z + sum_i R_i^T D_i A_i^{-1} R_i d, or (AS2 / SAS2) y = z + sum_i ... x
+    S* z = (S*)ws->z;
+    op_coarse_correct<S>(P, ws, x, z, batch, st);
+    if (kind == HELM_SHS2) {
+      S* d = (S*)ws->d;
+      launch_stencil<S>(P->geo, x, z, d, batch, st);
+      launch_local_sum<S>(P, d, z, y, (S*)ws->ovl, 1, batch, P->dev.band_node, st, /*coarse_base=*/false, ws);
+    } else {
+      launch_local_sum<S>(P, x, z, y, (S*)ws->ovl, kind == HELM_SAS2 ? 1 : 0, batch, P->dev.band_node, st,
+                          /*coarse_base=*/false, ws);
+    }
+    return;
+  }
   if (kind == HELM_SHS2) {
     // z = R0^T A0^{-1} R0 x and d = x - A z (schwarz.py:86-88) with the prolongation
     // and the deflation stencil fused in one pass
@@ -441,7 +478,8 @@ static void build_plan(const helm_desc* d, helm_plan* P) {
   HELM_CHECK(d->is_complex == (d->bc == HELM_SOMMERFELD ? 1 : 0),
              "MP-1 (Dirichlet) plans are fp64, MP-2 (Sommerfeld) plans complex128");
   HELM_CHECK(d->kind >= HELM_AS2 && d->kind <= HELM_SHS2, "unknown preconditioner kind");
-  HELM_CHECK(d->ratio == 2, "only the HOCS coarse ratio 2 (H = 2h) is implemented");
+  HELM_CHECK(d->ratio >= 1 && (d->n - 1) % d->ratio == 0, "the coarse ratio must divide the cell count n-1");
+  HELM_CHECK(!d->coarse_scale || d->ratio == 2, "the fast coarse solver is the HOCS ratio-2 one");
   // p == 0 (no boxes) and coarse_V == NULL (no coarse solver) give an operator-only plan
   HELM_CHECK(d->p == 0 || (d->p >= 1 && (d->n - 1) % d->p == 0), "p must divide the cell count n-1");
   HELM_CHECK(d->refine_steps >= 0 && d->refine_steps <= 8, "refine_steps out of range");
@@ -451,8 +489,12 @@ static void build_plan(const helm_desc* d, helm_plan* P) {
   Geo& g = P->geo;
   const double h = 1.0 / (d->n - 1);
   g.nu = d->bc == HELM_DIRICHLET ? d->n - 2 : d->n;
-  g.m0 = d->bc == HELM_DIRICHLET ? (d->n - 3) / 2 : (d->n + 1) / 2;
-  HELM_CHECK(d->m0 == g.m0, "descriptor m0 does not match the grid");
+  if (d->coarse_V) {  // general coarse space: (n-1)/ratio + 1 coarse nodes, interior ones for Dirichlet
+    g.m0 = (d->n - 1) / d->ratio + (d->bc == HELM_DIRICHLET ? -1 : 1);
+  } else {
+    g.m0 = d->bc == HELM_DIRICHLET ? (d->n - 3) / 2 : (d->n + 1) / 2;
+  }
+  HELM_CHECK(d->m0 == g.m0, "descriptor m0 does not match the grid and ratio");
   g.off = d->bc == HELM_DIRICHLET ? 1 : 0;
   g.sommerfeld = d->bc == HELM_SOMMERFELD;
   g.inv_h2 = 1.0 / (h * h);
@@ -466,6 +508,27 @@ static void build_plan(const helm_desc* d, helm_plan* P) {
   PlanDev& dv = P->dev;
   std::memset(&dv, 0, sizeof(dv));
   const size_t m0 = g.m0;
+  if (d->coarse_V) {
+    HELM_CHECK(!d->coarse_scale, "a plan has one coarse solver");
+    HELM_CHECK(d->p_width >= 1 && d->pt_width >= 1 && d->p_start && d->p_taps && d->pt_start && d->pt_taps,
+               "general coarse space needs the P and P^T bands");
+    HELM_CHECK(d->a0_bw >= 1 && d->a0_bw <= 8 && d->a0_t0 && d->a0_m0 && d->coarse_invden,
+               "general coarse space needs the T0 / M0 bands and the eigenvalue table");
+    HELM_CHECK(m0 >= 1 && m0 <= 4096, "general coarse space: m0 out of range");
+    dv.coarse_dense = 1;
+    dv.m0 = (int)m0;
+    dv.p_width = d->p_width;
+    dv.pt_width = d->pt_width;
+    dv.p_start = upload<int>(d->p_start, m0);
+    dv.p_taps = upload<double>(d->p_taps, m0 * d->p_width);
+    dv.pt_start = upload<int>(d->pt_start, g.nu);
+    dv.pt_taps = upload<double>(d->pt_taps, (size_t)g.nu * d->pt_width);
+    dv.a0_bw = d->a0_bw;
+    dv.a0_t0 = upload_bytes(d->a0_t0, m0 * (2 * d->a0_bw + 1) * P->elem);
+    dv.a0_m0 = upload_bytes(d->a0_m0, m0 * (2 * d->a0_bw + 1) * P->elem);
+    dv.coarse_V = upload_bytes(d->coarse_V, m0 * m0 * P->elem);
+    dv.coarse_invden = upload_bytes(d->coarse_invden, m0 * m0 * P->elem);
+  }
   if (d->coarse_scale) {
     dv.m0 = (int)m0;
     const int L = d->n - 1;
@@ -686,6 +749,9 @@ static void finish_desc(helm_plan* P) {
   P->desc.cap_left = P->desc.cap_right = P->desc.cap_mode = P->desc.cap_vt = P->desc.cap_hg = nullptr;
   P->desc.strip_lt = P->desc.strip_lm = nullptr;
   P->desc.band_piv = nullptr;
+  P->desc.p_start = P->desc.pt_start = nullptr;
+  P->desc.p_taps = P->desc.pt_taps = nullptr;
+  P->desc.a0_t0 = P->desc.a0_m0 = P->desc.coarse_V = P->desc.coarse_invden = nullptr;
 }
 
 static void free_plan(helm_plan* P) {
@@ -694,7 +760,8 @@ static void free_plan(helm_plan* P) {
                   dv.class_V, dv.class_lambda, dv.class_real, dv.class_Vr, dv.box_ff, dv.class_Vf, dv.class_lamf, dv.class_invden, dv.box_rr, dv.box_mix,
                   dv.node_first_box, dv.node_mult, dv.node_band, dv.band_node,
                   dv.coarse_scale, dv.twiddle, dv.coarse_lamT, dv.coarse_lamM, dv.t0_band, dv.m0_band, dv.band_piv, dv.band_fac, dv.band_seg, dv.strip_q,
-                  dv.cap_left, dv.cap_right, dv.cap_mode, dv.cap_vt, dv.cap_hg};
+                  dv.cap_left, dv.cap_right, dv.cap_mode, dv.cap_vt, dv.cap_hg,
+                  dv.p_start, dv.pt_start, dv.p_taps, dv.pt_taps, dv.a0_t0, dv.a0_m0, dv.coarse_V, dv.coarse_invden};
   for (void* q : ptrs)
     if (q) cudaFree(q);
 }
@@ -822,7 +889,7 @@ int helm_restrict(const helm_plan* P, const void* x, void* c, int32_t batch, voi
     HELM_CHECK(P && x && c && batch >= 1, "bad arguments");
     dispatch(P, [&](auto t) {
       using S = decltype(t);
-      launch_restrict<S>(P->geo, (const S*)x, (S*)c, batch, (cudaStream_t)stream);
+      restrict_any<S>(P, (const S*)x, (S*)c, batch, (cudaStream_t)stream);
     });
   });
 }
@@ -832,7 +899,7 @@ int helm_prolong(const helm_plan* P, const void* c, void* z, int32_t batch, void
     HELM_CHECK(P && c && z && batch >= 1, "bad arguments");
     dispatch(P, [&](auto t) {
       using S = decltype(t);
-      launch_prolong<S>(P->geo, (const S*)c, (S*)z, batch, (cudaStream_t)stream);
+      prolong_any<S>(P, (const S*)c, (S*)z, batch, (cudaStream_t)stream);
     });
   });
 }
@@ -843,7 +910,7 @@ int helm_coarse_solve(const helm_plan* P, helm_workspace* ws, const void* c, voi
     HELM_BATCH_CHECK(ws, batch);
     dispatch(P, [&](auto t) {
       using S = decltype(t);
-      launch_coarse_solve<S>(P, ws, (const S*)c, (S*)y, batch, (cudaStream_t)stream);
+      coarse_solve_any<S>(P, ws, (const S*)c, (S*)y, batch, (cudaStream_t)stream);
     });
   });
 }

@@ -266,6 +266,18 @@ struct PlanDev {
   double2 strip_lt[16]; // (T0 - T~), (M0 - M~) on the strip columns [i][j]
   double2 strip_lm[16];
   int strip_refine;
+  // general coarse spaces (coarse_dense.cu): coarse_dense != 0 selects them
+  int coarse_dense;
+  int p_width, pt_width;
+  int* p_start;
+  int* pt_start;
+  double* p_taps;
+  double* pt_taps;
+  int a0_bw;
+  void* a0_t0;
+  void* a0_m0;
+  void* coarse_V;
+  void* coarse_invden;
 };
 
 // ----------------------------------------------------------------------------

@@ -16,6 +16,12 @@ void launch_local_sum(const helm_plan* P, const S* x, const S* base, S* y, S* ov
 template <typename S>
 void launch_coarse_solve(const helm_plan* P, helm_workspace* ws, const S* c, S* y, int batch, cudaStream_t st);
 
+// general coarse spaces (coarse_dense.cu)
+template <typename S> void launch_restrict_general(const helm_plan* P, const S* x, S* c, int batch, cudaStream_t st);
+template <typename S> void launch_prolong_general(const helm_plan* P, const S* c, S* z, int batch, cudaStream_t st);
+template <typename S>
+void launch_coarse_solve_dense(const helm_plan* P, helm_workspace* ws, const S* c, S* y, int batch, cudaStream_t st);
+
 // coarse-solve building blocks (xform.cu, band.cu)
 template <typename S>
 void launch_xform(const helm_plan* P, const S* in, S* out, const double* sig, bool scale2d, int batch,

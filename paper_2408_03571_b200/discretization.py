@@ -43,12 +43,46 @@ class Grid:
         return self.n - 2 if self.bc == "dirichlet" else self.n
 
     @property
+    def num_nodes(self) -> int:
+        return self.n * self.n
+
+    @property
     def num_unknowns(self) -> int:
         return self.unknowns_per_dim**2
 
     def unknown_index(self, ix, iy):
         lo = self.unknown_lo
         return (np.asarray(iy) - lo) * self.unknowns_per_dim + (np.asarray(ix) - lo)
+
+
+@dataclass(frozen=True)
+class RegimeReport:
+    """Mesh-resolution products for (k, h, H) (helmdd discretization.py:97-121)."""
+
+    kappa_h: float
+    kappa_H: float
+    pollution_metric: float
+
+    _EPS = 1e-12
+
+    @property
+    def kappa_h_ok(self) -> bool:
+        return self.kappa_h <= 0.25 + self._EPS
+
+    @property
+    def kappa_H_ok(self) -> bool:
+        return self.kappa_H <= 1.0 + self._EPS
+
+    @property
+    def pollution_ok(self) -> bool:
+        return self.pollution_metric <= 1.0 + self._EPS
+
+
+def regime(k: float, h: float, H: float) -> RegimeReport:
+    """helmdd discretization.py:124-127."""
+    if k <= 0 or h <= 0 or H <= 0:
+        raise ValueError("k, h, H must all be positive")
+    return RegimeReport(kappa_h=k * h, kappa_H=k * H, pollution_metric=k**3 * h**2)
 
 
 def pencil_1d(grid: Grid, k: float):
@@ -168,28 +202,65 @@ def extend_max(part: Partition) -> Decomposition:
     return extend(part, max_overlap_layers(part), enforce_max_multiplicity=True)
 
 
+def _check_ratio(grid: Grid, ratio: int, powers_of_two: bool):
+    """coarse.py:77-81."""
+    if ratio < 1 or (grid.n - 1) % ratio != 0:
+        raise ValueError(f"coarsening ratio {ratio} does not divide {grid.n - 1} cells")
+    if powers_of_two and ratio & (ratio - 1):
+        raise ValueError(f"Bezier coarse space needs a power-of-two ratio, got {ratio}")
+
+
 def bezier_1d(grid: Grid, ratio: int = 2) -> np.ndarray:
-    """Dense 1-D Bezier restriction P (m0 x nu): (1,4,6,4,1)/8 at stride 2, taps
-    outside the unknown set dropped (helmdd coarse.py:102-133).  Ratio 2 only."""
-    if ratio != 2:
-        raise NotImplementedError("only the HOCS ratio H = 2h is implemented on the GPU path")
-    nu = grid.unknowns_per_dim
-    off = grid.unknown_lo
-    m0 = (grid.n - 3) // 2 if grid.bc == "dirichlet" else (grid.n + 1) // 2
+    """Dense 1-D Bezier restriction P (m0 x nu): the one-level (1,4,6,4,1)/8 stride-2 stencil
+    composed through the intermediate grids, taps outside each level's unknown set dropped
+    (helmdd coarse.py:102-133; Dirichlet levels keep their interior nodes only)."""
+    _check_ratio(grid, ratio, powers_of_two=True)
     taps = np.array([1.0, 4.0, 6.0, 4.0, 1.0]) / 8.0
-    P = np.zeros((m0, nu))
-    for d in range(-2, 3):
-        U = np.arange(m0)
-        u = 2 * U + off + d
-        ok = (u >= 0) & (u < nu)
-        P[U[ok], u[ok]] = taps[d + 2]
-    return P
+    dirichlet = grid.bc == "dirichlet"
+    op = None
+    nf = grid.n
+    for _ in range(int(round(np.log2(ratio)))):
+        M = (nf + 1) // 2
+        if dirichlet:  # unknowns: interior nodes 1..nf-2 -> coarse interior 1..M-2
+            S = np.zeros((M - 2, nf - 2))
+            for I in range(1, M - 1):
+                for d in range(-2, 3):
+                    i = 2 * I + d
+                    if 1 <= i <= nf - 2:
+                        S[I - 1, i - 1] = taps[d + 2]
+        else:
+            S = np.zeros((M, nf))
+            for I in range(M):
+                for d in range(-2, 3):
+                    i = 2 * I + d
+                    if 0 <= i < nf:
+                        S[I, i] = taps[d + 2]
+        op = S if op is None else S @ op
+        nf = M
+    return op
+
+
+def hat_1d(grid: Grid, ratio: int) -> np.ndarray:
+    """Dense 1-D hat-function sampling matrix (helmdd coarse.py:84-99): weights 1 - |d|/r
+    around every r-th node; Dirichlet drops the boundary coarse nodes and fine columns."""
+    _check_ratio(grid, ratio, powers_of_two=False)
+    n, r = grid.n, ratio
+    M = (n - 1) // r + 1
+    P = np.zeros((M, n))
+    for J in range(M):
+        for d in range(-r + 1, r):
+            i = r * J + d
+            if 0 <= i < n:
+                P[J, i] = 1.0 - abs(d) / r
+    if grid.bc == "dirichlet":
+        P = P[1:-1, 1:-1]
+    return np.ascontiguousarray(P)
 
 
 @dataclass(frozen=True)
 class CoarseSpace:
-    """HOCS coarse space descriptor (helmdd coarse.py:42-74); ``fdm`` holds the
-    partial-FDM setup once :func:`galerkin` has run."""
+    """Coarse space descriptor (helmdd coarse.py:42-74): kind FOCS / HOCS at H = ratio*h.
+    ``fdm`` holds the coarse-solver setup once :func:`galerkin` has run."""
 
     kind: str
     grid: Grid
@@ -197,21 +268,35 @@ class CoarseSpace:
     fdm: object = field(default=None, compare=False, repr=False)
 
     @property
+    def coarse_nodes_per_dim(self) -> int:
+        return (self.grid.n - 1) // self.ratio + 1
+
+    @property
     def coarse_unknowns_per_dim(self) -> int:
-        g = self.grid
-        return (g.n - 3) // 2 if g.bc == "dirichlet" else (g.n + 1) // 2
+        m = self.coarse_nodes_per_dim
+        return m - 2 if self.grid.bc == "dirichlet" else m
+
+    @property
+    def coarse_size(self) -> int:
+        """All-node count of the coarse grid (coarse.py:61-63)."""
+        return self.coarse_nodes_per_dim**2
 
     @property
     def num_coarse_unknowns(self) -> int:
         return self.coarse_unknowns_per_dim**2
 
+    def restriction_1d(self) -> np.ndarray:
+        """The dense 1-D P with R0 = P (x) P (coarse.py:136-139)."""
+        return bezier_1d(self.grid, self.ratio) if self.kind == "HOCS" else hat_1d(self.grid, self.ratio)
+
 
 def build_hocs(grid: Grid, ratio: int) -> CoarseSpace:
-    """Bezier coarse space with H = ratio*h (helmdd coarse.py:148-151); ratio 2 only."""
-    if ratio < 1 or (grid.n - 1) % ratio != 0:
-        raise ValueError(f"coarsening ratio {ratio} does not divide {grid.n - 1} cells")
-    if ratio & (ratio - 1):
-        raise ValueError(f"Bezier coarse space needs a power-of-two ratio, got {ratio}")
-    if ratio != 2:
-        raise NotImplementedError("only the HOCS ratio H = 2h is implemented on the GPU path")
+    """Bezier coarse space with H = ratio*h, ratio in 2, 4, 8, 16 (helmdd coarse.py:148-151)."""
+    _check_ratio(grid, ratio, powers_of_two=True)
     return CoarseSpace("HOCS", grid, ratio)
+
+
+def build_focs(grid: Grid, ratio: int) -> CoarseSpace:
+    """Linear (bilinear hat) coarse space with H = ratio*h (helmdd coarse.py:142-145)."""
+    _check_ratio(grid, ratio, powers_of_two=False)
+    return CoarseSpace("FOCS", grid, ratio)

@@ -211,6 +211,17 @@ def local_classes(grid: Grid, k: float, boxes) -> LocalClasses:
             Vs.append(V)
             lams.append(lam)
         cls.append(keys[key])
+    # Every pair of 1-D classes occurs in some box (boxes are products of 1-D intervals).
+    # A_i = T_y (x) W_x + W_y (x) T_x - k^2 W_y (x) W_x has the eigenvalues lam_y + lam_x - k^2;
+    # where one is (numerically) zero the reference's splu hits a near-zero pivot and raises
+    # SingularMatrixError (linalg.py:76-86, PIVOT_RTOL 1e-14 of max|A_i|): so does this setup.
+    scale = float(np.abs(T).max() + k**2 * np.abs(w).max())
+    for a in range(len(lams)):
+        for b in range(len(lams)):
+            den = np.abs(lams[a][:, None] + lams[b][None, :] - k**2)
+            if den.min() <= 1e-14 * scale:
+                raise SingularMatrixError(
+                    f"subdomain matrix is singular: eigenvalue {den.min():.3e} (matrix scale {scale:.3e})")
     return LocalClasses(
         np.array([b[0] for b in boxes], np.int32),
         np.array([b[1] for b in boxes], np.int32),
@@ -372,3 +383,70 @@ def coarse_fast(grid: Grid, k: float) -> CoarseFast:
                       L.astype(dt), U.astype(dt), strip, strip_q, cap_left.astype(dt), cap_right.astype(dt),
                       cap_mode.astype(dt), np.ascontiguousarray(cap_vt.astype(dt)), cap_hg.astype(dt),
                       np.asarray(LT, dt), np.asarray(LM, dt))
+
+
+@dataclass
+class CoarseDense:
+    """Setup of the general coarse solver (FOCS any ratio, HOCS ratio 4/8/16; coarse.py:84-167).
+
+    R0 = P (x) P with the banded 1-D P; A0 = T0(x)M0 + M0(x)T0 - k^2 M0(x)M0 (y (x) x) with
+    T0 = P T P^T, M0 = P W P^T (Kronecker identity, exact for any P); the 1-D pencil
+    T0 V = M0 V diag(lam), V^T M0 V = I gives A0^{-1} = (V(x)V) diag(1/(lam_y+lam_x-k^2)) (V(x)V)^T
+    (coarse_dense.cu), refined on the device with the banded A0."""
+
+    m0: int
+    p_start: np.ndarray     # [m0]  int32
+    p_taps: np.ndarray      # [m0][p_width]
+    pt_start: np.ndarray    # [nu]  int32
+    pt_taps: np.ndarray     # [nu][pt_width]
+    bw: int                 # half-bandwidth of T0, M0
+    t0_band: np.ndarray     # [m0][2bw+1]
+    m0_band: np.ndarray
+    V: np.ndarray           # [m0][m0]
+    invden: np.ndarray      # [m0][m0]
+
+
+def _row_band(A: np.ndarray):
+    """(start[r], taps[r][w]) of a banded dense matrix: row r's nonzeros lie in start..start+w-1."""
+    nz = A != 0
+    rows = A.shape[0]
+    first = np.where(nz.any(axis=1), nz.argmax(axis=1), 0)
+    last = np.where(nz.any(axis=1), A.shape[1] - 1 - nz[:, ::-1].argmax(axis=1), 0)
+    w = int(max(1, (last - first).max() + 1))
+    taps = np.zeros((rows, w))
+    for r in range(rows):
+        seg = A[r, first[r]: first[r] + w]
+        taps[r, : len(seg)] = seg
+    return first.astype(np.int32), taps
+
+
+def _sym_band(A: np.ndarray, bw: int) -> np.ndarray:
+    m = len(A)
+    out = np.zeros((m, 2 * bw + 1), dtype=A.dtype)
+    for d in range(-bw, bw + 1):
+        i = np.arange(max(0, -d), min(m, m - d))
+        out[i, d + bw] = A[i, i + d]
+    return out
+
+
+def coarse_dense(grid: Grid, k: float, P: np.ndarray) -> CoarseDense:
+    """Host setup of the general coarse solver for the 1-D restriction P (m0 x nu)."""
+    T, w = pencil_1d(grid, k)
+    T0 = P @ T @ P.T
+    M0 = P @ (w[:, None] * P.T)
+    T0, M0 = 0.5 * (T0 + T0.T), 0.5 * (M0 + M0.T)  # the symmetrisation of coarse.py:165
+    m = len(M0)
+    nzT = np.abs(T0) + np.abs(M0) > 0
+    off = np.abs(np.subtract.outer(np.arange(m), np.arange(m)))
+    bw = int(max(1, off[nzT].max()))
+    lam, V = _general_pencil_eig(T0, M0)
+    den = lam[:, None] + lam[None, :] - k**2
+    scale = float(np.abs(T).max() + k**2 * np.abs(w).max())
+    if np.abs(den).min() <= 1e-14 * scale:
+        # the reference's splu of A0 hits a near-zero pivot here (linalg.py:76-86)
+        raise SingularMatrixError(f"coarse Galerkin matrix is singular: eigenvalue {np.abs(den).min():.3e}")
+    dt = T0.dtype
+    ps, pt = _row_band(P)
+    qs, qt = _row_band(np.ascontiguousarray(P.T))
+    return CoarseDense(m, ps, pt, qs, qt, bw, _sym_band(T0, bw), _sym_band(M0.astype(dt), bw),
+                       np.ascontiguousarray(V.astype(dt)), np.ascontiguousarray((1.0 / den).astype(dt)))

@@ -53,19 +53,33 @@ class SolveReport:
     x: object = None
 
 
-def gmres(A, M_inv, b, cfg: GmresConfig = GmresConfig()) -> SolveReport:
-    """Solve A x = b with the B200 preconditioner ``M_inv`` (a SchwarzPreconditioner or None)."""
+def _resolve(A, M_inv):
+    """(operator, plan, use_precond).  The device loop applies the plan's own stencil, so a
+    given ``A`` must BE that operator (gmres.py:57-62 treats A and M_inv independently): the
+    preconditioner's operator, or one with the same grid, k and problem, or the reference's
+    CSR of it (structure guard)."""
     if M_inv is not None and not isinstance(M_inv, SchwarzPreconditioner):
         raise TypeError("device GMRES needs M_inv to be a SchwarzPreconditioner of this package (or None)")
-    if M_inv is not None:
-        plan, use_precond = M_inv.plan, 1
-        op = M_inv.A
-    else:
-        if isinstance(A, HelmholtzOperator):
-            op = A
-        else:
+    if M_inv is None:
+        if A is None:
+            raise TypeError("A is required")
+        op = A if isinstance(A, HelmholtzOperator) else None
+        if op is None:
             raise TypeError("with M_inv=None, A must be a HelmholtzOperator")
-        plan, use_precond = op._stencil_plan(), 0
+        return op, op._stencil_plan(), 0
+    op = M_inv.A
+    if A is not None and A is not op:
+        given = _as_operator(A, op.grid)  # CSR: structure guard (k recovered, entries compared)
+        if (given.grid.n, given.grid.bc, given.problem) != (op.grid.n, op.grid.bc, op.problem) or \
+                abs(given.k - op.k) > 1e-12 * max(1.0, op.k):
+            raise ValueError("A differs from the operator the preconditioner was built on "
+                             f"(k {given.k} vs {op.k}, n {given.grid.n} vs {op.grid.n}, {given.problem} vs {op.problem})")
+    return op, M_inv.plan, 1
+
+
+def gmres(A, M_inv, b, cfg: GmresConfig = GmresConfig()) -> SolveReport:
+    """Solve A x = b with the B200 preconditioner ``M_inv`` (a SchwarzPreconditioner or None)."""
+    op, plan, use_precond = _resolve(A, M_inv)
     v = _Vec(b, op.N, op.torch_dtype)
     if v.batch != 1 or v.t.dim() != 1:
         raise ValueError("gmres solves one right-hand side")
@@ -100,21 +114,13 @@ def gmres_multi(A, M_inv, B, cfg: GmresConfig = GmresConfig()) -> list:
     M^{-1} (``helm_gmres_multi``: the batched kernels at batch nrhs).  ``M_inv`` needs
     ``max_batch >= nrhs``.  Returns one SolveReport per row; ``wall_seconds`` is the whole
     call's.  Not in the reference."""
-    if M_inv is not None and not isinstance(M_inv, SchwarzPreconditioner):
-        raise TypeError("device GMRES needs M_inv to be a SchwarzPreconditioner of this package (or None)")
-    if M_inv is not None:
-        plan, use_precond = M_inv.plan, 1
-        op = M_inv.A
-    else:
-        if isinstance(A, HelmholtzOperator):
-            op = A
-        else:
-            raise TypeError("with M_inv=None, A must be a HelmholtzOperator")
-        plan, use_precond = op._stencil_plan(), 0
+    op, plan, use_precond = _resolve(A, M_inv)
     v = _Vec(B, op.N, op.torch_dtype)
     if v.t.dim() != 2:
         raise ValueError("gmres_multi expects right-hand sides as rows of a [nrhs, N] array")
     nrhs = v.batch
+    if M_inv is None:
+        plan = op._stencil_plan(max_batch=nrhs)
     if M_inv is not None and nrhs > M_inv.max_batch:
         raise ValueError(f"{nrhs} right-hand sides exceed the preconditioner's max_batch {M_inv.max_batch}")
     x = torch.empty_like(v.t)

@@ -22,7 +22,7 @@ import torch
 
 from . import _lib
 from .discretization import CoarseSpace, Decomposition, Grid, PROBLEMS, build_hocs, extend, partition
-from .fdm_setup import SingularMatrixError, coarse_fast, fold_blocks, local_classes
+from .fdm_setup import CoarseDense, SingularMatrixError, coarse_dense, coarse_fast, fold_blocks, local_classes
 
 __all__ = [
     "HelmholtzOperator",
@@ -87,6 +87,21 @@ class _Vec:
         return y
 
 
+def _check_out(out, shape, dtype, device):
+    """A caller-supplied result buffer: right dtype, shape, contiguity and device (CUDA out) or a
+    host tensor of the same shape and dtype (pinned pipeline / host copy-back)."""
+    if not isinstance(out, torch.Tensor):
+        raise TypeError("out must be a torch tensor")
+    if out.dtype != dtype:
+        raise TypeError(f"out has dtype {out.dtype}, the operator computes in {dtype}")
+    if tuple(out.shape) != tuple(shape):
+        raise ValueError(f"out has shape {tuple(out.shape)}, expected {tuple(shape)}")
+    if not out.is_contiguous():
+        raise ValueError("out must be contiguous")
+    if out.is_cuda and out.device != device:
+        raise ValueError(f"out is on {out.device}, the input on {device}")
+
+
 def _real_split(fn, x, N):
     """Apply a real-coefficient operator to a complex numpy vector by linearity (re, im)."""
     return fn(np.real(x)) + 1j * fn(np.imag(x))
@@ -110,10 +125,12 @@ class HelmholtzOperator:
 
     # the stencil only needs the grid part of a plan; it is created lazily so
     # that setting up an operator does not run the coarse eigen-solves
-    def _stencil_plan(self):
+    def _stencil_plan(self, max_batch: int = 1):
+        """The grid-only plan; its workspace is recreated when a caller needs more batch rows
+        (unpreconditioned multi-RHS GMRES keeps nrhs Krylov bases in it)."""
         with self._lock:
-            if self._plan is None:
-                self._plan = _Plan.create(self.grid, self.k, "SHS2", None, None)
+            if self._plan is None or self._plan.max_batch < max_batch:
+                self._plan = _Plan.create(self.grid, self.k, "SHS2", None, None, max_batch=max_batch)
             return self._plan
 
     def matvec(self, x):
@@ -174,12 +191,24 @@ def assemble(grid: Grid, k: float, problem: str) -> HelmholtzProblem:
     return HelmholtzProblem(grid, float(k), problem, A, f)
 
 
+def _coarse_setup(cs, grid: Grid, k: float):
+    """The coarse-solver setup for a coarse space: the fast transform + Woodbury solver for
+    HOCS at ratio 2, the dense fast diagonalisation for every other space (coarse_dense.cu)."""
+    kind, ratio = getattr(cs, "kind", "HOCS"), int(getattr(cs, "ratio", 2))
+    if kind == "HOCS" and ratio == 2:
+        return coarse_fast(grid, k)
+    own = CoarseSpace(kind, grid, ratio)
+    return coarse_dense(grid, k, own.restriction_1d())
+
+
 def galerkin(cs: CoarseSpace, A) -> CoarseSpace:
-    """Attach the partial-FDM coarse solver (replaces SuperLU of A0, helmdd coarse.py:154-167)."""
+    """Attach the coarse solver (replaces the SuperLU factorisation of A0, helmdd coarse.py:154-167)."""
+    if cs.kind not in ("HOCS", "FOCS"):
+        raise ValueError(f"unknown coarse space {cs.kind!r}")
     op = _as_operator(A, cs.grid)
     from dataclasses import replace
 
-    return replace(cs, fdm=coarse_fast(cs.grid, op.k))
+    return replace(cs, fdm=_coarse_setup(cs, cs.grid, op.k))
 
 
 class _Plan:
@@ -204,6 +233,20 @@ class _Plan:
         d.ratio, d.k = 2, float(k)
         d.m0 = (grid.n - 3) // 2 if grid.bc == "dirichlet" else (grid.n + 1) // 2
         keep = {}
+        if isinstance(cf, CoarseDense):  # general coarse space (coarse_dense.cu)
+            d.ratio = (grid.n - 1) // (cf.m0 + (1 if grid.bc == "dirichlet" else -1))
+            d.m0 = cf.m0
+            for key, (v, t) in dict(ps=(cf.p_start, np.int32), pt=(cf.p_taps, np.float64),
+                                    qs=(cf.pt_start, np.int32), qt=(cf.pt_taps, np.float64),
+                                    t0=(cf.t0_band, dt), m0=(cf.m0_band, dt), V=(cf.V, dt),
+                                    inv=(cf.invden, dt)).items():
+                keep["cd_" + key] = np.ascontiguousarray(v, dtype=t)
+            d.p_width, d.pt_width = cf.p_taps.shape[1], cf.pt_taps.shape[1]
+            d.p_start, d.p_taps = i32(keep["cd_ps"]), vp(keep["cd_pt"])
+            d.pt_start, d.pt_taps = i32(keep["cd_qs"]), vp(keep["cd_qt"])
+            d.a0_bw, d.a0_t0, d.a0_m0 = cf.bw, vp(keep["cd_t0"]), vp(keep["cd_m0"])
+            d.coarse_V, d.coarse_invden = vp(keep["cd_V"]), vp(keep["cd_inv"])
+            cf = None
         if dec is not None:  # subdomain FDM classes
             lc = local_classes(grid, k, dec.boxes)
             keep["classV"] = np.ascontiguousarray(np.concatenate([v.astype(dt).ravel() for v in lc.V]))
@@ -247,7 +290,9 @@ class _Plan:
         except Exception:
             lib.helm_plan_destroy(h)
             raise
-        return _Plan(lib, h, ws, lib.helm_plan_num_unknowns(h), lib.helm_plan_num_coarse(h), None)
+        plan = _Plan(lib, h, ws, lib.helm_plan_num_unknowns(h), lib.helm_plan_num_coarse(h), None)
+        plan.max_batch = int(max_batch)
+        return plan
 
     def __del__(self):
         try:
@@ -297,7 +342,7 @@ class SchwarzPreconditioner:
     KINDS = ("AS2", "SAS2", "SHS2")
 
     def __init__(self, kind, A, decomposition, coarse_space, weights_before_solve=False,
-                 local_factorizations=None, max_batch: int = 1, refine_steps: int = 0, strip_refine: int = 1):
+                 local_factorizations=None, max_batch: int = 1, refine_steps=None, strip_refine: int = 1):
         if kind not in self.KINDS:
             raise ValueError(f"unknown preconditioner {kind!r}, expected one of {self.KINDS}")
         grid = _grid_of(decomposition)
@@ -306,12 +351,15 @@ class SchwarzPreconditioner:
         self.kind = kind
         self.A = _as_operator(A, grid)
         self.decomposition = Decomposition(grid, decomposition.p, decomposition.overlap_layers)
-        if getattr(coarse_space, "kind", "HOCS") != "HOCS" or getattr(coarse_space, "ratio", 2) != 2:
-            raise NotImplementedError("the GPU path implements the HOCS coarse space at ratio 2")
+        ckind, ratio = getattr(coarse_space, "kind", "HOCS"), int(getattr(coarse_space, "ratio", 2))
+        if ckind not in ("HOCS", "FOCS"):
+            raise ValueError(f"unknown coarse space {ckind!r}")
         cf = getattr(coarse_space, "fdm", None)
         if cf is None:
-            cf = coarse_fast(grid, self.A.k)
-        self.coarse_space = CoarseSpace("HOCS", grid, 2, cf)
+            cf = _coarse_setup(coarse_space, grid, self.A.k)
+        self.coarse_space = CoarseSpace(ckind, grid, ratio, cf)
+        if refine_steps is None:  # the dense coarse solve is refined twice (coarse_dense.cu)
+            refine_steps = 2 if isinstance(cf, CoarseDense) else 0
         self.weights_before_solve = bool(weights_before_solve)
         self.max_batch = int(max_batch)
         self.plan = _Plan.create(grid, self.A.k, kind, self.decomposition, cf, weights_before_solve,
@@ -324,6 +372,9 @@ class SchwarzPreconditioner:
         v = _Vec(x, in_len or self.N, self.A.torch_dtype)
         if v.batch > self.max_batch:
             raise ValueError(f"batch {v.batch} exceeds max_batch {self.max_batch}")
+        shape = (*v.t.shape[:-1], out_len or self.N)
+        if out is not None:  # the kernels write through the raw pointer: the buffer must match exactly
+            _check_out(out, shape, self.A.torch_dtype, v.t.device)
         y = out if (out is not None and out.is_cuda) else v.empty_like(out_len or self.N)
         with self.plan.lock:
             _lib.check(fn(v.t, y, v.batch))
@@ -419,6 +470,10 @@ class SchwarzPreconditioner:
         bt = None
         if base is not None:
             bt = _Vec(base, self.N, self.A.torch_dtype).t
+            xb = 1 if (not hasattr(x, "shape") or len(x.shape) == 1) else x.shape[0]
+            bb = 1 if bt.dim() == 1 else bt.shape[0]
+            if bb != xb:  # the kernel reads base + b*N for every batch row b
+                raise ValueError(f"base has {bb} rows, x has {xb}")
         return self._run(
             lambda a, b, n: p.lib.helm_local_sum(p.handle, p.ws, _ptr(a), _ptr(bt) if bt is not None else None,
                                                  _ptr(b), int(weighted), n, _stream()), x)

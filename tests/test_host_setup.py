@@ -150,3 +150,130 @@ def test_desc_layout_matches_header(tmp_path):
         assert got[(cname, "size")] == ctypes.sizeof(py)
         for fname, _ in py._fields_:
             assert got[(cname, fname)] == getattr(py, fname).offset, (cname, fname)
+
+
+def test_resonant_subdomain_raises_singular():
+    """A k^2 on a subdomain eigenvalue: the reference's splu raises SingularMatrixError
+    (linalg.py:76-86); the FDM setup must too instead of dividing by ~0 on the device."""
+    import paper_2408_03571_b200 as hb
+    from paper_2408_03571_b200.discretization import pencil_1d
+    from paper_2408_03571_b200.fdm_setup import _sym_pencil_eig, local_classes
+
+    grid = hb.Grid(17, "dirichlet")
+    dec = hb.extend(hb.partition(grid, 2), 2)
+    T, w = pencil_1d(grid, 0.0)
+    s, L = dec.boxes[0]
+    lam, _ = _sym_pencil_eig(T[s:s + L, s:s + L], w[s:s + L])
+    k = float(np.sqrt(2 * lam[0]))  # lam_y[0] + lam_x[0] - k^2 = 0 on the first box
+    with pytest.raises(hb.SingularMatrixError):
+        local_classes(grid, k, dec.boxes)
+    local_classes(grid, k * 1.01, dec.boxes)  # off resonance: fine
+
+
+def test_out_buffer_is_validated():
+    """A caller-supplied out buffer is checked before its raw pointer reaches a kernel."""
+    import torch
+
+    from paper_2408_03571_b200.operators import _check_out
+
+    ok = torch.empty((2, 10), dtype=torch.complex128)
+    _check_out(ok, (2, 10), torch.complex128, ok.device)
+    with pytest.raises(TypeError):
+        _check_out(torch.empty((2, 10), dtype=torch.float64), (2, 10), torch.complex128, ok.device)
+    with pytest.raises(ValueError):
+        _check_out(torch.empty((2, 9), dtype=torch.complex128), (2, 10), torch.complex128, ok.device)
+    with pytest.raises(ValueError):
+        _check_out(torch.empty((10, 2), dtype=torch.complex128).t(), (2, 10), torch.complex128, ok.device)
+
+
+GENERAL_COARSE = [("MP2", 81, 20.0, "HOCS", 4), ("MP1", 81, 20.0, "HOCS", 4), ("MP2", 81, 20.0, "FOCS", 4),
+                  ("MP1", 65, 10.0, "FOCS", 2), ("MP1", 97, 5.0, "HOCS", 16), ("MP2", 129, 30.0, "HOCS", 8),
+                  ("MP2", 61, 12.0, "FOCS", 3)]
+
+
+@pytest.mark.parametrize("problem,n,k,kind,ratio", GENERAL_COARSE)
+def test_general_coarse_setup_matches_oracle(problem, n, k, kind, ratio):
+    """FOCS / HOCS ratio 4, 8, 16 (coarse.py:84-151): our 1-D P equals the oracle's, and the
+    dense fast diagonalisation, refined twice with the banded A0 exactly as coarse_dense.cu does,
+    solves the oracle's Galerkin matrix to the SuperLU level."""
+    import scipy.sparse as sp
+
+    import paper_2408_03571_b200 as hb
+    from paper_2408_03571_b200.fdm_setup import coarse_dense
+
+    bc = "dirichlet" if problem == "MP1" else "sommerfeld"
+    grid = hb.Grid(n, bc)
+    cs = (hb.build_hocs if kind == "HOCS" else hb.build_focs)(grid, ratio)
+    P = cs.restriction_1d()
+    og = O.OGrid(n, bc)
+    Po = (O.bezier_1d(og, ratio) if kind == "HOCS" else O.hat_1d(og, ratio)).toarray()
+    assert np.array_equal(P, Po)
+    assert P.shape[0] == cs.coarse_unknowns_per_dim
+    cd = coarse_dense(grid, k, P)
+    op = O.assemble(og, k, problem)
+    R0, a0 = O.galerkin_matrix(og, op.A, ratio, kind)
+    m = cd.m0
+    c = np.random.default_rng(3).standard_normal(m * m) + (1j * np.random.default_rng(4).standard_normal(m * m)
+                                                           if problem == "MP2" else 0)
+
+    def band_mat(b):
+        A = np.zeros((m, m), dtype=b.dtype)
+        for d in range(-cd.bw, cd.bw + 1):
+            i = np.arange(max(0, -d), min(m, m - d))
+            A[i, i + d] = b[i, d + cd.bw]
+        return A
+
+    T0, M0 = band_mat(cd.t0_band), band_mat(cd.m0_band)
+    assert np.abs(sp.kron(T0, M0) + sp.kron(M0, T0) - k**2 * sp.kron(M0, M0) - a0).max() <= 1e-12 * abs(a0).max()
+
+    def fdm(C):
+        return cd.V @ ((cd.V.T @ C @ cd.V) * cd.invden) @ cd.V.T
+
+    C = c.reshape(m, m)
+    Y = fdm(C)
+    for _ in range(2):  # coarse_dense.cu: r = C - (T0 Y M0 + M0 Y T0 - k^2 M0 Y M0), Y += solve(r)
+        Y = Y + fdm(C - (T0 @ Y @ M0 + M0 @ Y @ T0 - k**2 * M0 @ Y @ M0))
+    ref = sp.linalg.splu(sp.csc_matrix(a0)).solve(c)
+    assert np.linalg.norm(Y.ravel() - ref) <= 1e-12 * np.linalg.norm(ref)
+    # the banded P / P^T tables reproduce P
+    Pb = np.zeros_like(P)
+    for r in range(m):
+        w = cd.p_taps.shape[1]
+        cols = cd.p_start[r] + np.arange(w)
+        ok = cols < P.shape[1]
+        Pb[r, cols[ok]] = cd.p_taps[r, ok]
+    assert np.array_equal(Pb, P)
+
+
+def test_harness_config_mirror(tmp_path):
+    """The B200 harness reads the reference's config format and emits its CSV layout
+    (harness.py:82-151, 242-263): keys, defaults, errors, warnings."""
+    from paper_2408_03571_b200 import harness as Hh
+
+    cfgf = tmp_path / "sweep.cfg"
+    cfgf.write_text("problem = mp2\nk = 20, 40\nn = 81, 161\ncoarse = hocs, focs\npreconditioners = shs2\n"
+                    "rtol = 1e-6\nprecond_side = left  # comment\n")
+    cfg = Hh.parse_config(cfgf)
+    assert cfg.problem == "MP2" and cfg.k_list == (20, 40) and cfg.n_list == (81, 161)
+    assert cfg.coarse_kinds == ("HOCS", "FOCS") and cfg.gmres.side == "left" and cfg.gmres.rtol == 1e-6
+    assert cfg.coarse_ratio == 4 and cfg.overlap == "max" and cfg.cells() == [(20, 81), (40, 161)]
+    with pytest.raises(Hh.ConfigError):
+        Hh.config_from_dict({"k": "1", "n": "9", "bogus": "1"})
+    with pytest.raises(Hh.ConfigError):
+        Hh.config_from_dict({"k": "1", "n": "9", "coarse": "XYZ"})
+    with pytest.raises(Hh.ConfigError):
+        Hh.validate_config(Hh.config_from_dict({"k": "20", "n": "80"}))  # 4 does not divide 79
+    (_, _, p, rep, warns), = Hh.validate_config(Hh.config_from_dict({"k": "200", "n": "81"}))
+    assert p == 20 and not rep.kappa_h_ok and any("kappa_h" in w for w in warns)
+    t1 = Hh.builtin_table(1)
+    assert t1.problem == "MP2" and t1.coarse_kinds == ("FOCS", "HOCS") and t1.gmres.side == "left"
+    assert Hh.builtin_table(4).coarse_ratio == 16 and Hh.builtin_table(2).problem == "MP1"
+    row = Hh.TableRow(k=20, n=81, subdomains=400, fine_nodes=6561, coarse_nodes=441, kappa_h=0.25, kappa_H=1.0,
+                      iterations={"HOCS_SHS2": 8, "FOCS_SHS2": "x"})
+    out = Hh.emit_csv([row], tmp_path / "t.csv").read_text().splitlines()
+    assert out[0] == "k,n,subdomains,fine_nodes,coarse_nodes,kappa_h,kappa_H,HOCS_SHS2,FOCS_SHS2,setup_seconds,solve_seconds"
+    assert out[1].startswith("20,81,400,6561,441,0.25,1,8,x,")
+    with pytest.raises(ValueError):
+        Hh.emit_csv([], tmp_path / "e.csv")
+    with pytest.raises(Hh.ConfigError):
+        Hh.run_experiment(t1, backend="cpu")

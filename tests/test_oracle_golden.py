@@ -80,10 +80,44 @@ def test_paper_known_answer_hocs_h4():
 def test_oracle_refined_coarse_counts(name):
     """The reference with one refinement step on its SuperLU coarse solve (tests/golden/make_refined.py)
     and the oracle with the same step agree on the GMRES count."""
+    import json
+    import os
+
+    from common import GOLDEN
+
     g = load_golden(name)
-    raw, refined = reference_count(name, g)
-    assert refined is not None
+    with open(os.path.join(GOLDEN, name + "_refined.json")) as f:
+        refined = int(json.load(f)["iterations"])
+    raw = reference_count(name, g)
     prob, dec, cs, _ = build(g)
     M = O.OSchwarz("SHS2", prob.A, dec, cs, coarse_refine=1)
     rep = O.gmres(prob.A, M, prob.f, 1e-6, 1000)
     assert rep.converged and abs(rep.iterations - refined) <= 1, (rep.iterations, refined, raw)
+
+
+def test_oracle_large_goldens_cfg3():
+    """The oracle against the sampled config-3 goldens of the unmodified reference
+    (tests/golden/make_golden_large.py): every operator <= 1e-12 on sample, norm and functional."""
+    import os
+    import sys
+
+    from common import GOLDEN
+
+    sys.path.insert(0, GOLDEN)
+    from make_golden_large import functional, sample_index
+
+    g = dict(np.load(os.path.join(GOLDEN, "cfg3_ops.npz")))
+    prob, dec, cs, M = build(g)
+    x = operator_input(prob.A.shape[0], False)
+    c = cs.r0 @ x
+    y = np.zeros_like(x)
+    outs = {"Ax": prob.A @ x, "R0x": c, "R0T_c": cs.r0.T @ c, "coarse_solve": cs.lu.solve(c),
+            "coarse_correct": O.coarse_correct(cs, x), "local_sum": M.local_sum(x, y, True), "M_shs2": M(x)}
+    nu, m0 = int(g["nu"]), int(g["m0"])
+    for tag, v in outs.items():
+        ref = g[tag]
+        idx = sample_index(m0 if tag in ("R0x", "coarse_solve") else nu)
+        assert rel(v[idx], ref) <= 1e-12, tag
+        assert abs(np.linalg.norm(v) - float(g[tag + "_norm"])) <= 1e-12 * float(g[tag + "_norm"]), tag
+        w = functional(len(v))
+        assert abs(w @ v - float(g[tag + "_dot"])) <= 1e-12 * np.linalg.norm(w) * float(g[tag + "_norm"]), tag
