@@ -279,6 +279,27 @@ def run_ours(a, rank, world, local_rank):
     e2e = {"value": round(e2e_value, 3), "unit": UNIT, "h2d_bytes_per_step": int(Xh.numel() * 16),
            "d2h_bytes_per_step": int(Yh.numel() * 16)}
 
+    # ---- the benchmarked output against the unmodified reference (tests/golden/cfg5_ops.npz:
+    # rows 0 and 31 of this batch through the reference's SHS2 apply, make_golden_large.py) ----
+    parity = None
+    gpath = os.path.join(ROOT, "tests", "golden", "cfg5_ops.npz")
+    if os.path.exists(gpath) and (a.n, a.k, a.p) == (CFG["n"], CFG["k"], CFG["p"]) and B == 32:
+        sys.path.insert(0, os.path.join(ROOT, "tests", "golden"))
+        from make_golden_large import sample_index
+
+        g = np.load(gpath)
+        idx = sample_index(grid.unknowns_per_dim)
+        errs = []
+        for v, row in enumerate((0, 31)):
+            if f"M_shs2_v{v}" in g.files:
+                ref = g[f"M_shs2_v{v}"]
+                y = Yh[row].numpy()[idx]
+                errs.append(float(np.linalg.norm(y - ref) / np.linalg.norm(ref)))
+        if errs:
+            parity = {"check": "M^-1 rows 0 and 31 of the timed batch vs the unmodified reference's SHS2 apply "
+                               "(sampled, tests/golden/cfg5_ops.npz)", "max_rel_err": max(errs), "bar": 1e-12,
+                      "ok": max(errs) <= 1e-12}
+
     # ---- GMRES on the config-5 operator ----
     # (1) the centre point source to rtol 1e-6 (6 iterations); (2) a fixed-length run on the
     # seed-0 random complex right-hand side (config 4(b)'s recipe; it reaches 1e-6 in 6
@@ -323,7 +344,7 @@ def run_ours(a, rank, world, local_rank):
                        "roofline_frac": round(t_roof * its / wall, 4)}
 
     return dict(value=value, ms=ms, setup_s=setup_s, clocks=clk.summary(), launches=launches, comp=comp,
-                roof=roof, composite=composite, e2e=e2e, gmres=gm)
+                roof=roof, composite=composite, e2e=e2e, gmres=gm, parity=parity)
 
 
 def cpu_sample(a, budget_s=30.0):
@@ -574,7 +595,7 @@ def main():
             "vs_baseline": None, "dtype": "c128", "data": "synthetic", "config": config,
             "roofline": r["roof"], "roofline_composite": r["composite"], "phases": r["comp"],
             "cpu_baseline": cpu, "e2e": r["e2e"], "gpu_launches": int(r["launches"]), "clocks": r["clocks"],
-            "gmres": r["gmres"], "setup_s": round(r["setup_s"], 2),
+            "gmres": r["gmres"], "setup_s": round(r["setup_s"], 2), "parity": r["parity"],
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -119,9 +119,11 @@ typedef struct helm_desc {
   /* --- general coarse spaces (FOCS at any ratio, HOCS at ratio 4/8/16;
    *     coarse.py:84-151): R0 = P (x) P with a banded 1-D P, and
    *     A0^{-1} c = (V (x) V) diag(invden) (V (x) V)^T c with T0 V = M0 V diag(lam),
-   *     V^T M0 V = I, followed by refine_steps iterative-refinement steps on
-   *     A0 = T0(x)M0 + M0(x)T0 - k^2 M0(x)M0.  coarse_V == NULL -> the HOCS ratio-2
-   *     fast solver above (coarse_scale ...).                                        */
+   *     V^T M0 V = I (T0 = P T P^T, M0 = P W P^T), followed by refine_steps
+   *     iterative-refinement steps r = c - A0 y on the reference's own Galerkin matrix
+   *     A0 = (B + B^T)/2, B = R0 A R0^T (coarse.py:154-165), passed as a 2-D stencil of
+   *     (2b+1)^2 coefficients per coarse unknown.  coarse_V == NULL -> the HOCS ratio-2
+   *     fast solver above (coarse_scale ...).                                         */
   int32_t coarse_kind;        /* 0: HOCS, 1: FOCS                                  */
   int32_t p_width;            /* taps per row of P                                 */
   const int32_t* p_start;     /* [m0]  first fine unknown of row I of P            */
@@ -129,9 +131,9 @@ typedef struct helm_desc {
   int32_t pt_width;           /* taps per row of P^T                               */
   const int32_t* pt_start;    /* [nu]  first coarse unknown of row i of P^T        */
   const double* pt_taps;      /* [nu][pt_width]                                    */
-  int32_t a0_bw;              /* half-bandwidth b of T0 and M0 (1..3)              */
-  const void* a0_t0;          /* S [m0][2b+1]  T0[i][i+d-b]                        */
-  const void* a0_m0;          /* S [m0][2b+1]  M0[i][i+d-b]                        */
+  int32_t a0_bw;              /* half-bandwidth b of A0 along each axis (1..8)      */
+  const void* a0_stencil;     /* S [m0*m0][(2b+1)^2]  A0[(Iy,Ix)][(Iy+dy,Ix+dx)],
+                                 (dy+b)(2b+1) + dx+b (zero outside the grid)          */
   const void* coarse_V;       /* S [m0][m0]  row-major                             */
   const void* coarse_invden;  /* S [m0][m0]  1 / (lam[y] + lam[x] - k^2)           */
 } helm_desc;

@@ -69,8 +69,7 @@ class HelmDesc(ctypes.Structure):
         ("pt_start", c_int32_p),
         ("pt_taps", ctypes.c_void_p),
         ("a0_bw", ctypes.c_int32),
-        ("a0_t0", ctypes.c_void_p),
-        ("a0_m0", ctypes.c_void_p),
+        ("a0_stencil", ctypes.c_void_p),
         ("coarse_V", ctypes.c_void_p),
         ("coarse_invden", ctypes.c_void_p),
     ]

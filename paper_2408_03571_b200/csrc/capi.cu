@@ -512,8 +512,8 @@ static void build_plan(const helm_desc* d, helm_plan* P) {
     HELM_CHECK(!d->coarse_scale, "a plan has one coarse solver");
     HELM_CHECK(d->p_width >= 1 && d->pt_width >= 1 && d->p_start && d->p_taps && d->pt_start && d->pt_taps,
                "general coarse space needs the P and P^T bands");
-    HELM_CHECK(d->a0_bw >= 1 && d->a0_bw <= 8 && d->a0_t0 && d->a0_m0 && d->coarse_invden,
-               "general coarse space needs the T0 / M0 bands and the eigenvalue table");
+    HELM_CHECK(d->a0_bw >= 1 && d->a0_bw <= 8 && d->a0_stencil && d->coarse_invden,
+               "general coarse space needs the A0 stencil and the eigenvalue table");
     HELM_CHECK(m0 >= 1 && m0 <= 4096, "general coarse space: m0 out of range");
     dv.coarse_dense = 1;
     dv.m0 = (int)m0;
@@ -524,8 +524,8 @@ static void build_plan(const helm_desc* d, helm_plan* P) {
     dv.pt_start = upload<int>(d->pt_start, g.nu);
     dv.pt_taps = upload<double>(d->pt_taps, (size_t)g.nu * d->pt_width);
     dv.a0_bw = d->a0_bw;
-    dv.a0_t0 = upload_bytes(d->a0_t0, m0 * (2 * d->a0_bw + 1) * P->elem);
-    dv.a0_m0 = upload_bytes(d->a0_m0, m0 * (2 * d->a0_bw + 1) * P->elem);
+    const size_t taps = (size_t)(2 * d->a0_bw + 1) * (2 * d->a0_bw + 1);
+    dv.a0_stencil = upload_bytes(d->a0_stencil, m0 * m0 * taps * P->elem);
     dv.coarse_V = upload_bytes(d->coarse_V, m0 * m0 * P->elem);
     dv.coarse_invden = upload_bytes(d->coarse_invden, m0 * m0 * P->elem);
   }
@@ -751,7 +751,7 @@ static void finish_desc(helm_plan* P) {
   P->desc.band_piv = nullptr;
   P->desc.p_start = P->desc.pt_start = nullptr;
   P->desc.p_taps = P->desc.pt_taps = nullptr;
-  P->desc.a0_t0 = P->desc.a0_m0 = P->desc.coarse_V = P->desc.coarse_invden = nullptr;
+  P->desc.a0_stencil = P->desc.coarse_V = P->desc.coarse_invden = nullptr;
 }
 
 static void free_plan(helm_plan* P) {
@@ -761,7 +761,7 @@ static void free_plan(helm_plan* P) {
                   dv.node_first_box, dv.node_mult, dv.node_band, dv.band_node,
                   dv.coarse_scale, dv.twiddle, dv.coarse_lamT, dv.coarse_lamM, dv.t0_band, dv.m0_band, dv.band_piv, dv.band_fac, dv.band_seg, dv.strip_q,
                   dv.cap_left, dv.cap_right, dv.cap_mode, dv.cap_vt, dv.cap_hg,
-                  dv.p_start, dv.pt_start, dv.p_taps, dv.pt_taps, dv.a0_t0, dv.a0_m0, dv.coarse_V, dv.coarse_invden};
+                  dv.p_start, dv.pt_start, dv.p_taps, dv.pt_taps, dv.a0_stencil, dv.coarse_V, dv.coarse_invden};
   for (void* q : ptrs)
     if (q) cudaFree(q);
 }

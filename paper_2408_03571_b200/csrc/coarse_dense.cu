@@ -9,9 +9,9 @@
 //     T0 V = M0 V diag(lam),  V^T M0 V = I           (host setup, fdm_setup.coarse_dense)
 //
 //   i.e. Y = V ((V^T C V) .* invden) V^T on the m0 x m0 coarse array C: four dense GEMMs,
-//   followed by refine_steps iterative-refinement steps r = C - A0 Y (two banded passes per
-//   step, A0 applied in Kronecker form) that take the solve to the rounding level of the
-//   reference's SuperLU solve (linalg.py:90-95).  The sizes where these spaces are used (the
+//   followed by refine_steps iterative-refinement steps r = C - A0 Y with the reference's own
+//   Galerkin matrix (a 2-D stencil, a0_residual_kernel) that take the solve to the rounding
+//   level of the reference's SuperLU solve (linalg.py:90-95).  The sizes where these spaces are used (the
 //   paper's tables, n <= 801, m0 <= 201) make this a latency-bound path, not a roofline one.
 #include "ops.cuh"
 
@@ -145,49 +145,33 @@ static void dense_gemm(GemmOp A, GemmOp B, S* C, const S* scale_by, bool accumul
   HELM_LAUNCH_CHECK();
 }
 
-// A0 residual r = c - A0 y with A0 y = T0 Y M0 + M0 Y T0 - k^2 M0 Y M0 (T0, M0 symmetric):
-//   U1 = Y M0, W = Y T0 - k^2 U1 (x passes), r = c - T0 U1 - M0 W (y passes)
+// A0 residual r = c - A0 y with the reference's own Galerkin matrix as a 2-D stencil
+// ((2b+1)^2 coefficients per coarse unknown, coarse.py:161-165): the refinement then converges
+// to the solution of exactly the matrix SuperLU factorises (linalg.py:64-95), not of its
+// Kronecker form T0(x)M0 + M0(x)T0 - k^2 M0(x)M0, which differs from it at the rounding level
+// (amplified by cond(A0) near a coarse resonance).
 template <typename S>
-__global__ void __launch_bounds__(256) a0_rows_kernel(const S* __restrict__ y, S* __restrict__ u1,
-                                                      S* __restrict__ wv, const S* __restrict__ t0,
-                                                      const S* __restrict__ m0b, int bw, double k2, int m) {
+__global__ void __launch_bounds__(256) a0_residual_kernel(const S* __restrict__ c, const S* __restrict__ y,
+                                                          S* __restrict__ res, const S* __restrict__ st, int bw,
+                                                          int m) {
   pdl_wait();
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  const int r = blockIdx.y * blockDim.y + threadIdx.y;
-  if (j >= m || r >= m) return;
-  const size_t base = ((size_t)blockIdx.z * m + r) * m;
-  const int wd = 2 * bw + 1;
-  S a = Sc<S>::zero(), t = Sc<S>::zero();
-  for (int q = 0; q < wd; ++q) {
-    const int i = j + q - bw;
-    if (i < 0 || i >= m) continue;
-    const S v = y[base + i];
-    a = fma_(m0b[(size_t)j * wd + q], v, a);
-    t = fma_(t0[(size_t)j * wd + q], v, t);
-  }
-  u1[base + j] = a;
-  wv[base + j] = sub(t, scale(a, k2));
-}
-
-template <typename S>
-__global__ void __launch_bounds__(256) a0_cols_kernel(const S* __restrict__ c, const S* __restrict__ u1,
-                                                      const S* __restrict__ wv, S* __restrict__ res,
-                                                      const S* __restrict__ t0, const S* __restrict__ m0b, int bw,
-                                                      int m) {
-  pdl_wait();
-  const int col = blockIdx.x * blockDim.x + threadIdx.x;
-  const int j = blockIdx.y * blockDim.y + threadIdx.y;
-  if (col >= m || j >= m) return;
+  const int ix = blockIdx.x * blockDim.x + threadIdx.x;
+  const int iy = blockIdx.y * blockDim.y + threadIdx.y;
+  if (ix >= m || iy >= m) return;
   const size_t bo = (size_t)blockIdx.z * m * m;
   const int wd = 2 * bw + 1;
+  const S* a = st + ((size_t)iy * m + ix) * wd * wd;
   S acc = Sc<S>::zero();
-  for (int q = 0; q < wd; ++q) {
-    const int i = j + q - bw;
-    if (i < 0 || i >= m) continue;
-    acc = fma_(t0[(size_t)j * wd + q], u1[bo + (size_t)i * m + col], acc);
-    acc = fma_(m0b[(size_t)j * wd + q], wv[bo + (size_t)i * m + col], acc);
+  for (int dy = -bw; dy <= bw; ++dy) {
+    const int jy = iy + dy;
+    if (jy < 0 || jy >= m) continue;
+    for (int dx = -bw; dx <= bw; ++dx) {
+      const int jx = ix + dx;
+      if (jx < 0 || jx >= m) continue;
+      acc = fma_(a[(dy + bw) * wd + dx + bw], y[bo + (size_t)jy * m + jx], acc);
+    }
   }
-  const size_t o = bo + (size_t)j * m + col;
+  const size_t o = bo + (size_t)iy * m + ix;
   res[o] = sub(c[o], acc);
 }
 
@@ -221,13 +205,10 @@ void launch_coarse_solve_dense(const helm_plan* P, helm_workspace* ws, const S* 
     src = cc;
   }
   fdm_solve<S>(P, src, y, t1, t2, false, batch, st);
-  const S* t0 = static_cast<const S*>(d.a0_t0);
-  const S* m0b = static_cast<const S*>(d.a0_m0);
+  const S* a0 = static_cast<const S*>(d.a0_stencil);
   for (int it = 0; it < P->desc.refine_steps; ++it) {
     dim3 blk(32, 8), grd((m + 31) / 32, (m + 7) / 8, batch);
-    launch_pdl(a0_rows_kernel<S>, grd, blk, 0, st, (const S*)y, t1, t2, t0, m0b, d.a0_bw, P->geo.k2, m);
-    HELM_LAUNCH_CHECK();
-    launch_pdl(a0_cols_kernel<S>, grd, blk, 0, st, src, (const S*)t1, (const S*)t2, rr, t0, m0b, d.a0_bw, m);
+    launch_pdl(a0_residual_kernel<S>, grd, blk, 0, st, src, (const S*)y, rr, a0, d.a0_bw, m);
     HELM_LAUNCH_CHECK();
     fdm_solve<S>(P, rr, y, t1, t2, true, batch, st);
   }

@@ -274,8 +274,7 @@ struct PlanDev {
   double* p_taps;
   double* pt_taps;
   int a0_bw;
-  void* a0_t0;
-  void* a0_m0;
+  void* a0_stencil;
   void* coarse_V;
   void* coarse_invden;
 };

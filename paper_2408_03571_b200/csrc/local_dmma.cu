@@ -152,8 +152,14 @@ __global__ void __launch_bounds__(DTH, 4) local_fdm_dmma_kernel(const S* __restr
   constexpr int XL = DmmaDims<NP>::XL;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double* Xr = reinterpret_cast<double*>(smem_raw);  // [DT][XL]
-  int* meta = reinterpret_cast<int*>(Xr + DT * XL);  // [2][3][DT]: multiplicity, first box, band per row / column
-  S* cw = reinterpret_cast<S*>(meta + 6 * DT);       // [WIN][WIN] coarse window (coarse-base mode)
+  // per row (y) / column (x) of the box: the output address terms and weights of every node
+  // (decomposition.py:111-134), so the scatter does no per-node index arithmetic:
+  //   multiplicity 1 x 1 -> y[ry_c + cx_c];  my = 2 -> ovl[ry_a + cx_a];  my = 1, mx = 2 -> ovl[ry_b + cx_b]
+  int* meta = reinterpret_cast<int*>(Xr + DT * XL);  // [8][DT]
+  int* m_my = meta, *m_mx = meta + DT;
+  int* ry_a = meta + 2 * DT, *ry_b = meta + 3 * DT, *ry_c = meta + 4 * DT;
+  int* cx_a = meta + 5 * DT, *cx_b = meta + 6 * DT, *py = meta + 7 * DT;  // py: prolongation row offset | parity
+  S* cw = reinterpret_cast<S*>(meta + 8 * DT);       // [WIN][WIN] coarse window (coarse-base mode)
   S* rx = cw + WIN * WIN;                             // [WIN][DT] x-pass of the window prolongation
   const int sid = boxes[blockIdx.x];
   const int ay = sid / a.p, ax = sid % a.p;
@@ -168,59 +174,88 @@ __global__ void __launch_bounds__(DTH, 4) local_fdm_dmma_kernel(const S* __restr
   const S* bb = base ? base + (size_t)b * base_stride(a) : nullptr;
   S* yb = y + (size_t)b * N;
   S* ob = ovl + (size_t)b * 6 * a.nbands * nu;
+  // the raw box streams into the X tile with cp.async (row r at Xr + r XL, scalars in place):
+  // every thread has all its copies in flight at once instead of a chain of dependent loads
+  {
+    const int q = threadIdx.x % DT;  // column of this thread (constant divisor: no runtime division)
+    if (q < Lx)
+      for (int r = threadIdx.x / DT; r < Ly; r += DTH / DT) {
+        const S* src = xb + (size_t)(y0 + r) * nu + x0 + q;
+        if constexpr (NP == 2) cp_async16(&Xr[r * XL + 2 * q], src, true);
+        else cp_async8(&Xr[r * XL + q], src, true);
+      }
+  }
+  cp_commit();
   // coarse-base mode: the box's window of c streams into shared memory behind the products
   const int Uby = window_base(y0, a.off), Ubx = window_base(x0, a.off);
   if (bb && a.coarse_base) window_load(cw, bb, a, Uby, Ubx, DTH);
-  // gather + fold both axes: pair (i, j) of the half-box -> the 4 folded entries
-  // (s_y s_x) [i][j], (s_y d_x) [i][DB+j], (d_y s_x) [DB+i][j], (d_y d_x) [DB+i][DB+j]
+  // fold both axes in place: pair (i, j) of the half-box -> the 4 folded entries
+  // (s_y s_x) [i][j], (s_y d_x) [i][DB+j], (d_y s_x) [DB+i][j], (d_y d_x) [DB+i][DB+j];
+  // all raw values are read (registers) before any folded value is written
   const bool wb = a.weighted && a.wbs;
-  auto ld = [&](int r, int q) {
-    S v = xb[(size_t)(y0 + r) * nu + x0 + q];
+  auto raw = [&](int r, int q) -> S {
+    S v;
+    if constexpr (NP == 2) v = mk(Xr[r * XL + 2 * q], Xr[r * XL + 2 * q + 1]);
+    else v = Xr[r * XL + q];
     if (wb) v = scale(v, 1.0 / (a.node_mult[y0 + r] * a.node_mult[x0 + q]));
     return v;
   };
   auto put_s = [&](int i, int j, S v) {
     if constexpr (NP == 2) {
-      Xr[i * XL + 2 * j] = v.x;
-      Xr[i * XL + 2 * j + 1] = v.y;
+      *reinterpret_cast<double2*>(&Xr[i * XL + 2 * j]) = v;
     } else {
       Xr[i * XL + j] = v;
     }
   };
-  for (int e = threadIdx.x; e < DB * DB; e += DTH) {
+  constexpr int QPT = (DB * DB + DTH - 1) / DTH;  // quads per thread
+  S qv[QPT][4];
+  if (bb && a.coarse_base) cp_wait<1>();  // the box copies (the window may still be in flight)
+  else cp_wait<0>();
+  __syncthreads();
+#pragma unroll
+  for (int u = 0; u < QPT; ++u) {
+    const int e = threadIdx.x + u * DTH;
     const int i = e / DB, j = e % DB;
-    S f0 = Sc<S>::zero(), f1 = f0, f2 = f0, f3 = f0;
-    if (i < hpy && j < hpx) {
+    qv[u][0] = qv[u][1] = qv[u][2] = qv[u][3] = Sc<S>::zero();
+    if (e < DB * DB && i < hpy && j < hpx) {
       const bool ci = i == hy, cj = j == hx;  // centre row / column (odd length)
-      const S a00 = ld(i, j);
-      const S a10 = ci ? Sc<S>::zero() : ld(Ly - 1 - i, j);
-      const S a01 = cj ? Sc<S>::zero() : ld(i, Lx - 1 - j);
-      const S a11 = (ci || cj) ? Sc<S>::zero() : ld(Ly - 1 - i, Lx - 1 - j);
-      const S sy0 = add(a00, a10), dy0 = sub(a00, a10), sy1 = add(a01, a11), dy1 = sub(a01, a11);
-      // the d components of a centre row / column are exactly zero (the padded blocks read them)
-      f0 = add(sy0, sy1);
-      f1 = cj ? Sc<S>::zero() : sub(sy0, sy1);
-      f2 = ci ? Sc<S>::zero() : add(dy0, dy1);
-      f3 = (ci || cj) ? Sc<S>::zero() : sub(dy0, dy1);
+      qv[u][0] = raw(i, j);
+      if (!ci) qv[u][1] = raw(Ly - 1 - i, j);
+      if (!cj) qv[u][2] = raw(i, Lx - 1 - j);
+      if (!ci && !cj) qv[u][3] = raw(Ly - 1 - i, Lx - 1 - j);
     }
-    put_s(i, j, f0);
-    put_s(i, DB + j, f1);
-    put_s(DB + i, j, f2);
-    put_s(DB + i, DB + j, f3);
+  }
+  __syncthreads();
+#pragma unroll
+  for (int u = 0; u < QPT; ++u) {
+    const int e = threadIdx.x + u * DTH;
+    if (e >= DB * DB) break;
+    const int i = e / DB, j = e % DB;
+    const bool ci = i == hy, cj = j == hx;
+    const S a00 = qv[u][0], a10 = qv[u][1], a01 = qv[u][2], a11 = qv[u][3];
+    const S sy0 = add(a00, a10), dy0 = sub(a00, a10), sy1 = add(a01, a11), dy1 = sub(a01, a11);
+    // the d components of a centre row / column are exactly zero (the padded blocks read them)
+    put_s(i, j, add(sy0, sy1));
+    put_s(i, DB + j, cj ? Sc<S>::zero() : sub(sy0, sy1));
+    put_s(DB + i, j, ci ? Sc<S>::zero() : add(dy0, dy1));
+    put_s(DB + i, DB + j, (ci || cj) ? Sc<S>::zero() : sub(dy0, dy1));
   }
   const double* Vy = classVf + (size_t)cy * DT * DT;  // folded V tables (zero padded by the plan)
   const double* Vx = classVf + (size_t)cx * DT * DT;
-  {
-    // the box's per-row / per-column overlap bookkeeping (decomposition.py:111-134)
-    for (int e = threadIdx.x; e < DT; e += DTH) {
-      const int iy = y0 + (e < Ly ? e : 0), ix = x0 + (e < Lx ? e : 0);
-      meta[0 * DT + e] = a.node_mult[iy];
-      meta[1 * DT + e] = a.node_first_box[iy];
-      meta[2 * DT + e] = a.node_band[iy];
-      meta[3 * DT + e] = a.node_mult[ix];
-      meta[4 * DT + e] = a.node_first_box[ix];
-      meta[5 * DT + e] = a.node_band[ix];
-    }
+  for (int e = threadIdx.x; e < DT; e += DTH) {
+    const int iy = y0 + (e < Ly ? e : 0), ix = x0 + (e < Lx ? e : 0);
+    const int my = a.node_mult[iy], mx = a.node_mult[ix];
+    const int ry = ay - a.node_first_box[iy], rxb = ax - a.node_first_box[ix];
+    m_my[e] = my;
+    m_mx[e] = mx;
+    ry_a[e] = (ry * 2 * a.nbands + a.node_band[iy]) * nu;           // band rows: slot (ry, rx), band, x
+    ry_b[e] = iy * a.nbands;                                        // band columns: slot rx, y, band
+    ry_c[e] = iy * nu;
+    cx_a[e] = rxb * a.nbands * nu + ix;
+    cx_b[e] = 4 * a.nbands * nu + rxb * nu * a.nbands + a.node_band[ix];
+    const int ty = iy - a.off;
+    const int U0 = ((ty & 1) == 0 ? ty / 2 - 1 : (ty - 1) >> 1) - window_base(y0, a.off);
+    py[e] = (U0 * DT) * 2 + ((ty & 1) == 0 ? 1 : 0);
   }
   const double* invden = classInvden + (size_t)(cy * ncls + cx) * DT * DT;
   __syncthreads();
@@ -245,66 +280,70 @@ __global__ void __launch_bounds__(DTH, 4) local_fdm_dmma_kernel(const S* __restr
   // pipe with the DMMAs)
   const bool cbase = bb && a.coarse_base;
   if (cbase) {
-    for (int e = threadIdx.x; e < WIN * Lx; e += DTH) {
-      const int u = e / Lx, j = e % Lx;
+    const int j = threadIdx.x % DT;
+    if (j < Lx) {
       const int tx = x0 + j - a.off;
       const bool ex = (tx & 1) == 0;
       const int V0 = (ex ? tx / 2 - 1 : (tx - 1) >> 1) - Ubx;
       const double w0 = ex ? 0.125 : 0.5, w1 = ex ? 0.75 : 0.5, w2 = ex ? 0.125 : 0.0;
-      const S* c = cw + u * WIN + V0;
-      S row = Sc<S>::zero();
-      row = fma_(w0, c[0], row);
-      row = fma_(w1, c[1], row);
-      row = fma_(w2, c[2], row);
-      rx[u * DT + j] = row;
+      for (int u = threadIdx.x / DT; u < WIN; u += DTH / DT) {
+        const S* c = cw + u * WIN + V0;
+        S row = Sc<S>::zero();
+        row = fma_(w0, c[0], row);
+        row = fma_(w1, c[1], row);
+        row = fma_(w2, c[2], row);
+        rx[u * DT + j] = row;
+      }
     }
     __syncthreads();
   }
-  auto prolong_y = [&](int iy, int q) {
-    const int ty = iy - a.off;
-    const bool ey = (ty & 1) == 0;
-    const int U0 = (ey ? ty / 2 - 1 : (ty - 1) >> 1) - Uby;
-    const S* r = rx + U0 * DT + q;
+  auto prolong_y = [&](int r, int q) {  // the y pass of R0^T c at box node (r, q), taps from py[r]
+    const int code = py[r];
+    const bool ey = code & 1;
+    const S* t = rx + (code >> 1) + q;
     S acc = Sc<S>::zero();
-    acc = fma_(ey ? 0.125 : 0.5, r[0], acc);
-    acc = fma_(ey ? 0.75 : 0.5, r[DT], acc);
-    acc = fma_(ey ? 0.125 : 0.0, r[2 * DT], acc);
+    acc = fma_(ey ? 0.125 : 0.5, t[0], acc);
+    acc = fma_(ey ? 0.75 : 0.5, t[DT], acc);
+    acc = fma_(ey ? 0.125 : 0.0, t[2 * DT], acc);
     return acc;
   };
   // unfold + weight + scatter: x_i = e_i + o_i, x_{L-1-i} = e_i - o_i on both axes
   auto get = [&](int i, int j) -> S {
-    if constexpr (NP == 2) return mk(Xr[i * XL + 2 * j], Xr[i * XL + 2 * j + 1]);
+    if constexpr (NP == 2) return *reinterpret_cast<const double2*>(&Xr[i * XL + 2 * j]);
     else return Xr[i * XL + j];
   };
+  const bool wpu = a.weighted && !a.wbs;
   auto put = [&](int r, int q, S acc) {
-    const int my = meta[r], mx = meta[3 * DT + q];
+    const int my = m_my[r], mx = m_mx[q];
     // partition-of-unity weight 1 / (my mx) with my, mx in {1, 2}: exact constants, no division
-    if (a.weighted && !a.wbs && my * mx != 1) acc = scale(acc, my * mx == 2 ? 0.5 : 0.25);
-    const int iy = y0 + r, ix = x0 + q;
-    const size_t pidx = (size_t)iy * nu + ix;
+    if (wpu && my * mx != 1) acc = scale(acc, my * mx == 2 ? 0.5 : 0.25);
     if (my == 1 && mx == 1) {
-      yb[pidx] = bb ? add(cbase ? prolong_y(iy, q) : bb[pidx], acc) : acc;
+      const int pidx = ry_c[r] + x0 + q;
+      yb[pidx] = bb ? add(cbase ? prolong_y(r, q) : bb[pidx], acc) : acc;
     } else if (my == 2) {
-      const int ry = ay - meta[DT + r], rx = ax - meta[4 * DT + q];
-      ob[((size_t)(ry * 2 + rx) * a.nbands + meta[2 * DT + r]) * nu + ix] = acc;
+      ob[ry_a[r] + cx_a[q]] = acc;
     } else {
-      const int rx = ax - meta[4 * DT + q];
-      ob[(size_t)4 * a.nbands * nu + ((size_t)rx * nu + iy) * a.nbands + meta[5 * DT + q]] = acc;
+      ob[ry_b[r] + cx_b[q]] = acc;
     }
   };
-  for (int e = threadIdx.x; e < hpy * hpx; e += DTH) {
-    const int i = e / hpx, j = e % hpx;
-    const bool ci = i == hy, cj = j == hx;
-    const S ee = get(i, j);
-    const S eo = cj ? Sc<S>::zero() : get(i, DB + j);
-    const S oe = ci ? Sc<S>::zero() : get(DB + i, j);
-    const S oo = (ci || cj) ? Sc<S>::zero() : get(DB + i, DB + j);
-    const S ry0 = add(ee, oe), ry1 = sub(ee, oe);  // row i / row L-1-i, still split in x
-    const S rz0 = add(eo, oo), rz1 = sub(eo, oo);
-    put(i, j, add(ry0, rz0));
-    if (!cj) put(i, Lx - 1 - j, sub(ry0, rz0));
-    if (!ci) put(Ly - 1 - i, j, add(ry1, rz1));
-    if (!ci && !cj) put(Ly - 1 - i, Lx - 1 - j, sub(ry1, rz1));
+  {
+    const int j = threadIdx.x % DB;  // half-box column of this thread (constant divisor)
+    if (j < hpx) {
+      const bool cj = j == hx;
+      for (int i = threadIdx.x / DB; i < hpy; i += DTH / DB) {
+        const bool ci = i == hy;
+        const S ee = get(i, j);
+        const S eo = cj ? Sc<S>::zero() : get(i, DB + j);
+        const S oe = ci ? Sc<S>::zero() : get(DB + i, j);
+        const S oo = (ci || cj) ? Sc<S>::zero() : get(DB + i, DB + j);
+        const S ry0 = add(ee, oe), ry1 = sub(ee, oe);  // row i / row L-1-i, still split in x
+        const S rz0 = add(eo, oo), rz1 = sub(eo, oo);
+        put(i, j, add(ry0, rz0));
+        if (!cj) put(i, Lx - 1 - j, sub(ry0, rz0));
+        if (!ci) put(Ly - 1 - i, j, add(ry1, rz1));
+        if (!ci && !cj) put(Ly - 1 - i, Lx - 1 - j, sub(ry1, rz1));
+      }
+    }
   }
 }
 
@@ -314,11 +353,11 @@ void launch_local_dmma(const helm_plan* P, const S* x, const S* base, S* y, S* o
   const PlanDev& d = P->dev;
   if (d.n_ff == 0) return;
   constexpr int NP = Sc<S>::cplx ? 2 : 1;
-  const size_t smem = (size_t)(DT * DmmaDims<NP>::XL) * sizeof(double) + 6 * DT * sizeof(int) +
+  const size_t smem = (size_t)(DT * DmmaDims<NP>::XL) * sizeof(double) + 8 * DT * sizeof(int) +
                       (a.coarse_base ? (WIN * WIN + WIN * DT) * sizeof(S) : 0);
   static bool attr = false;
   if (!attr) {
-    const size_t smax = (size_t)(DT * DmmaDims<NP>::XL) * sizeof(double) + 6 * DT * sizeof(int) +
+    const size_t smax = (size_t)(DT * DmmaDims<NP>::XL) * sizeof(double) + 8 * DT * sizeof(int) +
                         (WIN * WIN + WIN * DT) * sizeof(S);
     HELM_CUDA(cudaFuncSetAttribute(local_fdm_dmma_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)smax));

@@ -399,9 +399,8 @@ class CoarseDense:
     p_taps: np.ndarray      # [m0][p_width]
     pt_start: np.ndarray    # [nu]  int32
     pt_taps: np.ndarray     # [nu][pt_width]
-    bw: int                 # half-bandwidth of T0, M0
-    t0_band: np.ndarray     # [m0][2bw+1]
-    m0_band: np.ndarray
+    bw: int                 # half-bandwidth of A0 along each axis
+    a0_stencil: np.ndarray  # [m0*m0][(2bw+1)^2]  the reference's Galerkin matrix, row by row
     V: np.ndarray           # [m0][m0]
     invden: np.ndarray      # [m0][m0]
 
@@ -429,6 +428,61 @@ def _sym_band(A: np.ndarray, bw: int) -> np.ndarray:
     return out
 
 
+def assembled_matrix(grid: Grid, k: float):
+    """The reference's CSR system matrix, built with the same sparse operations in the same
+    order as helmdd discretization.py:128-188 (so its entries, and the Galerkin product below,
+    carry the same rounding)."""
+    import scipy.sparse as sp
+
+    n, h = grid.n, grid.h
+    if grid.bc == "dirichlet":
+        m = n - 2
+        ones = np.ones(m - 1)
+        T = sp.diags([-ones, 2 * np.ones(m), -ones], [-1, 0, 1], format="csr") / h**2
+        I = sp.identity(m, format="csr")
+        A = sp.kron(T, I) + sp.kron(I, T) - k**2 * sp.identity(m * m)
+    else:
+        ones = np.ones(n - 1)
+        T = sp.diags([-ones, 2 * np.ones(n), -ones], [-1, 0, 1], format="csr").astype(complex).tolil()
+        T[0, 0] = 1.0
+        T[n - 1, n - 1] = 1.0
+        T = (T / h**2).tolil()
+        T[0, 0] -= 1j * k / h
+        T[n - 1, n - 1] -= 1j * k / h
+        T = T.tocsr()
+        w = np.ones(n)
+        w[0] = w[-1] = 0.5
+        W = sp.diags(w)
+        A = sp.kron(T, W) + sp.kron(W, T) - k**2 * sp.kron(W, W)
+    A = sp.csr_matrix(A)
+    A.sort_indices()
+    return A
+
+
+def galerkin_stencil(grid: Grid, k: float, P: np.ndarray, bw: int) -> np.ndarray:
+    """A0 = (B + B^T)/2 with B = R0 A R0^T, R0 = P (x) P, as helmdd coarse.py:136-139,154-165
+    computes it, rearranged as a 2-D stencil [m0*m0][(2bw+1)^2]."""
+    import scipy.sparse as sp
+
+    A = assembled_matrix(grid, k)
+    P1 = sp.csr_matrix(P)
+    R0 = sp.kron(P1, P1, format="csr")
+    R0.sort_indices()
+    r0 = R0.astype(A.dtype)
+    B = sp.csr_matrix(r0 @ A @ r0.T)
+    a0 = ((B + B.T) * 0.5).tocoo()
+    m = P.shape[0]
+    wd = 2 * bw + 1
+    iy, ix = np.divmod(a0.row, m)
+    jy, jx = np.divmod(a0.col, m)
+    dy, dx = jy - iy, jx - ix
+    if np.abs(dy).max(initial=0) > bw or np.abs(dx).max(initial=0) > bw:
+        raise ValueError("Galerkin matrix wider than the stencil half-width")
+    st = np.zeros((m * m, wd * wd), dtype=A.dtype)
+    st[a0.row, (dy + bw) * wd + dx + bw] = a0.data
+    return st
+
+
 def coarse_dense(grid: Grid, k: float, P: np.ndarray) -> CoarseDense:
     """Host setup of the general coarse solver for the 1-D restriction P (m0 x nu)."""
     T, w = pencil_1d(grid, k)
@@ -448,5 +502,5 @@ def coarse_dense(grid: Grid, k: float, P: np.ndarray) -> CoarseDense:
     dt = T0.dtype
     ps, pt = _row_band(P)
     qs, qt = _row_band(np.ascontiguousarray(P.T))
-    return CoarseDense(m, ps, pt, qs, qt, bw, _sym_band(T0, bw), _sym_band(M0.astype(dt), bw),
+    return CoarseDense(m, ps, pt, qs, qt, bw, galerkin_stencil(grid, k, P, bw),
                        np.ascontiguousarray(V.astype(dt)), np.ascontiguousarray((1.0 / den).astype(dt)))

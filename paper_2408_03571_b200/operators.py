@@ -238,13 +238,12 @@ class _Plan:
             d.m0 = cf.m0
             for key, (v, t) in dict(ps=(cf.p_start, np.int32), pt=(cf.p_taps, np.float64),
                                     qs=(cf.pt_start, np.int32), qt=(cf.pt_taps, np.float64),
-                                    t0=(cf.t0_band, dt), m0=(cf.m0_band, dt), V=(cf.V, dt),
-                                    inv=(cf.invden, dt)).items():
+                                    st=(cf.a0_stencil, dt), V=(cf.V, dt), inv=(cf.invden, dt)).items():
                 keep["cd_" + key] = np.ascontiguousarray(v, dtype=t)
             d.p_width, d.pt_width = cf.p_taps.shape[1], cf.pt_taps.shape[1]
             d.p_start, d.p_taps = i32(keep["cd_ps"]), vp(keep["cd_pt"])
             d.pt_start, d.pt_taps = i32(keep["cd_qs"]), vp(keep["cd_qt"])
-            d.a0_bw, d.a0_t0, d.a0_m0 = cf.bw, vp(keep["cd_t0"]), vp(keep["cd_m0"])
+            d.a0_bw, d.a0_stencil = cf.bw, vp(keep["cd_st"])
             d.coarse_V, d.coarse_invden = vp(keep["cd_V"]), vp(keep["cd_inv"])
             cf = None
         if dec is not None:  # subdomain FDM classes

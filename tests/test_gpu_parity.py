@@ -348,3 +348,31 @@ def test_maximal_overlap_matches_oracle(problem, n, k, p):
     orep = O.gmres(oprob.A, oM, oprob.f, 1e-6, 500)
     assert rep.converged and rep.iterations == orep.iterations, (rep.iterations, orep.iterations)
     assert rel(rep.x, orep.x) <= X_TOL
+
+
+@pytest.mark.parametrize("name", ["cfg1", "small_mp2_n65_p8", "cfg2"])
+def test_reference_gmres_drives_device_preconditioner(name):
+    """The drop-in as INTEGRATION.md §1 wires it: the reference's own GMRES loop (the oracle's
+    restatement of gmres.py:65-177, numpy vectors, the assembled CSR A) calling the device
+    SchwarzPreconditioner for every M^{-1} apply (host->device->host per call).  Same count as the
+    reference's golden run (+-1) and the device GMRES, same solution."""
+    import os
+    import sys
+
+    sys.path.insert(0, os.path.join(os.path.dirname(__file__), "..", "oracle"))
+    import helmdd_oracle as O  # the reference's loop, restated (checker)
+
+    import paper_2408_03571_b200 as hb
+
+    g, prob, Ms = build(name)
+    n, k, problem = int(g["n"]), float(g["k"]), str(g["problem"])
+    oprob = O.assemble(O.OGrid(n, "dirichlet" if problem == "MP1" else "sommerfeld"), k, problem)
+    b = oprob.f if str(g["gmres_rhs"]) == "point" else random_rhs(oprob.A.shape[0])
+    rep = O.gmres(oprob.A, Ms["SHS2"], b, 1e-6, 1000)  # M: the device preconditioner, numpy in / out
+    dev = hb.gmres(prob.A, Ms["SHS2"], b, hb.GmresConfig(rtol=1e-6, max_iter=1000))
+    raw = reference_count(name, g)
+    print(name, "reference loop + device M:", rep.iterations, "device GMRES:", dev.iterations, "reference:", raw)
+    assert rep.converged and count_matches(rep.iterations, raw)
+    assert abs(rep.iterations - dev.iterations) <= 1
+    tol = UNREPRODUCIBLE.get(name, X_TOL)
+    assert rel(rep.x, g["gmres_x"]) <= tol

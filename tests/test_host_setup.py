@@ -216,23 +216,21 @@ def test_general_coarse_setup_matches_oracle(problem, n, k, kind, ratio):
     c = np.random.default_rng(3).standard_normal(m * m) + (1j * np.random.default_rng(4).standard_normal(m * m)
                                                            if problem == "MP2" else 0)
 
-    def band_mat(b):
-        A = np.zeros((m, m), dtype=b.dtype)
-        for d in range(-cd.bw, cd.bw + 1):
-            i = np.arange(max(0, -d), min(m, m - d))
-            A[i, i + d] = b[i, d + cd.bw]
-        return A
-
-    T0, M0 = band_mat(cd.t0_band), band_mat(cd.m0_band)
-    assert np.abs(sp.kron(T0, M0) + sp.kron(M0, T0) - k**2 * sp.kron(M0, M0) - a0).max() <= 1e-12 * abs(a0).max()
+    # the stencil IS the oracle's (= the reference's) Galerkin matrix, bit for bit
+    wd = 2 * cd.bw + 1
+    rows, taps = np.nonzero(cd.a0_stencil)
+    iy, ix = np.divmod(rows, m)
+    dy, dx = np.divmod(taps, wd)
+    A0 = sp.csr_matrix((cd.a0_stencil[rows, taps], (rows, (iy + dy - cd.bw) * m + ix + dx - cd.bw)), shape=(m * m, m * m))
+    assert (A0 != a0).nnz == 0
 
     def fdm(C):
         return cd.V @ ((cd.V.T @ C @ cd.V) * cd.invden) @ cd.V.T
 
     C = c.reshape(m, m)
     Y = fdm(C)
-    for _ in range(2):  # coarse_dense.cu: r = C - (T0 Y M0 + M0 Y T0 - k^2 M0 Y M0), Y += solve(r)
-        Y = Y + fdm(C - (T0 @ Y @ M0 + M0 @ Y @ T0 - k**2 * M0 @ Y @ M0))
+    for _ in range(2):  # coarse_dense.cu: r = C - A0 Y (the stencil), Y += solve(r)
+        Y = Y + fdm(C - (a0 @ Y.ravel()).reshape(m, m))
     ref = sp.linalg.splu(sp.csc_matrix(a0)).solve(c)
     assert np.linalg.norm(Y.ravel() - ref) <= 1e-12 * np.linalg.norm(ref)
     # the banded P / P^T tables reproduce P
