@@ -47,17 +47,28 @@ __device__ __forceinline__ S base_at(const S* __restrict__ bb, const LocalArgs& 
   double wy[3], wx[3];
   prolong_taps_off(iy, a.off, Uy, ny, wy);
   prolong_taps_off(ix, a.off, Ux, nx, wx);
-  S acc = Sc<S>::zero();
-  for (int p = 0; p < ny; ++p) {
-    const int U = Uy + p;
-    if (U < 0 || U >= a.m0) continue;
-    S row = Sc<S>::zero();
-    for (int q = 0; q < nx; ++q) {
-      const int V = Ux + q;
-      if (V < 0 || V >= a.m0) continue;
-      row = fma_(wx[q], __ldg(bb + (size_t)U * a.m0 + V), row);
+  // all 9 taps unrolled with clamped indices and zero weights for the absent ones, so every
+  // load is in flight at once; fma(0, v, r) == r keeps the sums of prolong_kernel bit for bit
+  S v[3][3];
+#pragma unroll
+  for (int p = 0; p < 3; ++p)
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      const int U = min(max(Uy + p, 0), a.m0 - 1), V = min(max(Ux + q, 0), a.m0 - 1);
+      v[p][q] = __ldg(bb + (size_t)U * a.m0 + V);
     }
-    acc = fma_(wy[p], row, acc);
+  S acc = Sc<S>::zero();
+#pragma unroll
+  for (int p = 0; p < 3; ++p) {
+    const int U = Uy + p;
+    const bool uin = p < ny && U >= 0 && U < a.m0;
+    S row = Sc<S>::zero();
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      const int V = Ux + q;
+      row = fma_((q < nx && V >= 0 && V < a.m0) ? wx[q] : 0.0, v[p][q], row);
+    }
+    acc = fma_(uin ? wy[p] : 0.0, row, acc);
   }
   return acc;
 }

@@ -78,10 +78,7 @@ __device__ __forceinline__ void dmma_left(double* Xr, const double* __restrict__
       const int ml = r * 8 + g;
       if (ml < DB) {
 #pragma unroll
-        for (int t = 0; t < TPW; ++t) {
-          epi(b * DB + ml, c0 + t * 8 + 2 * q, acc[r][t][0]);
-          epi(b * DB + ml, c0 + t * 8 + 2 * q + 1, acc[r][t][1]);
-        }
+        for (int t = 0; t < TPW; ++t) epi(b * DB + ml, c0 + t * 8 + 2 * q, acc[r][t][0], acc[r][t][1]);
       }
     }
     __syncwarp();
@@ -141,7 +138,7 @@ __device__ __forceinline__ void dmma_right(double* Xr, const double* __restrict_
 }
 
 template <typename S>
-__global__ void __launch_bounds__(DTH, 4) local_fdm_dmma_kernel(const S* __restrict__ x, const S* __restrict__ base,
+__global__ void __launch_bounds__(DTH, 5) local_fdm_dmma_kernel(const S* __restrict__ x, const S* __restrict__ base,
                                                              S* __restrict__ y, S* __restrict__ ovl,
                                                              const int* __restrict__ boxes,
                                                              const double* __restrict__ classVf,
@@ -159,8 +156,7 @@ __global__ void __launch_bounds__(DTH, 4) local_fdm_dmma_kernel(const S* __restr
   int* m_my = meta, *m_mx = meta + DT;
   int* ry_a = meta + 2 * DT, *ry_b = meta + 3 * DT, *ry_c = meta + 4 * DT;
   int* cx_a = meta + 5 * DT, *cx_b = meta + 6 * DT, *py = meta + 7 * DT;  // py: prolongation row offset | parity
-  S* cw = reinterpret_cast<S*>(meta + 8 * DT);       // [WIN][WIN] coarse window (coarse-base mode)
-  S* rx = cw + WIN * WIN;                             // [WIN][DT] x-pass of the window prolongation
+  S* rx = reinterpret_cast<S*>(meta + 8 * DT);       // [WIN][DT] x-pass of the window prolongation
   const int sid = boxes[blockIdx.x];
   const int ay = sid / a.p, ax = sid % a.p;
   const int nu = a.nu;
@@ -188,7 +184,7 @@ __global__ void __launch_bounds__(DTH, 4) local_fdm_dmma_kernel(const S* __restr
   cp_commit();
   // coarse-base mode: the box's window of c streams into shared memory behind the products
   const int Uby = window_base(y0, a.off), Ubx = window_base(x0, a.off);
-  if (bb && a.coarse_base) window_load(cw, bb, a, Uby, Ubx, DTH);
+
   // fold both axes in place: pair (i, j) of the half-box -> the 4 folded entries
   // (s_y s_x) [i][j], (s_y d_x) [i][DB+j], (d_y s_x) [DB+i][j], (d_y d_x) [DB+i][DB+j];
   // all raw values are read (registers) before any folded value is written
@@ -209,8 +205,7 @@ __global__ void __launch_bounds__(DTH, 4) local_fdm_dmma_kernel(const S* __restr
   };
   constexpr int QPT = (DB * DB + DTH - 1) / DTH;  // quads per thread
   S qv[QPT][4];
-  if (bb && a.coarse_base) cp_wait<1>();  // the box copies (the window may still be in flight)
-  else cp_wait<0>();
+  cp_wait<0>();
   __syncthreads();
 #pragma unroll
   for (int u = 0; u < QPT; ++u) {
@@ -260,7 +255,9 @@ __global__ void __launch_bounds__(DTH, 4) local_fdm_dmma_kernel(const S* __restr
   const double* invden = classInvden + (size_t)(cy * ncls + cx) * DT * DT;
   __syncthreads();
   // X <- Vfy^T X
-  dmma_left<NP, true>(Xr, Vy, [&](int m, int c, double v) { Xr[m * XL + c] = v; });
+  // (the two accumulators of a lane are adjacent columns: one 16-byte store)
+  auto store2 = [&](int m, int c, double v0, double v1) { *reinterpret_cast<double2*>(&Xr[m * XL + c]) = mk(v0, v1); };
+  dmma_left<NP, true>(Xr, Vy, store2);
   __syncthreads();
   // X <- (X Vfx) ./ (lfy (+) lfx - k^2)
   dmma_right<NP, false>(Xr, Vx, [&](int m, int part, int n, double v) {
@@ -268,7 +265,7 @@ __global__ void __launch_bounds__(DTH, 4) local_fdm_dmma_kernel(const S* __restr
   });
   __syncthreads();
   // X <- Vfy X
-  dmma_left<NP, false>(Xr, Vy, [&](int m, int c, double v) { Xr[m * XL + c] = v; });
+  dmma_left<NP, false>(Xr, Vy, store2);
   __syncthreads();
   // X <- X Vfx^T
   dmma_right<NP, true>(Xr, Vx, [&](int m, int part, int n, double v) { Xr[m * XL + n * NP + part] = v; });
@@ -286,8 +283,16 @@ __global__ void __launch_bounds__(DTH, 4) local_fdm_dmma_kernel(const S* __restr
       const bool ex = (tx & 1) == 0;
       const int V0 = (ex ? tx / 2 - 1 : (tx - 1) >> 1) - Ubx;
       const double w0 = ex ? 0.125 : 0.5, w1 = ex ? 0.75 : 0.5, w2 = ex ? 0.125 : 0.0;
+      // the window of c straight from L2 (zero outside [0, m0)), same taps and order as window_prolong
+      const int Vc = Ubx + V0;
       for (int u = threadIdx.x / DT; u < WIN; u += DTH / DT) {
-        const S* c = cw + u * WIN + V0;
+        const int U = Uby + u;
+        S c[3];
+#pragma unroll
+        for (int t = 0; t < 3; ++t) {
+          const int V = Vc + t;
+          c[t] = (U >= 0 && U < a.m0 && V >= 0 && V < a.m0) ? __ldg(bb + (size_t)U * a.m0 + V) : Sc<S>::zero();
+        }
         S row = Sc<S>::zero();
         row = fma_(w0, c[0], row);
         row = fma_(w1, c[1], row);
@@ -354,11 +359,11 @@ void launch_local_dmma(const helm_plan* P, const S* x, const S* base, S* y, S* o
   if (d.n_ff == 0) return;
   constexpr int NP = Sc<S>::cplx ? 2 : 1;
   const size_t smem = (size_t)(DT * DmmaDims<NP>::XL) * sizeof(double) + 8 * DT * sizeof(int) +
-                      (a.coarse_base ? (WIN * WIN + WIN * DT) * sizeof(S) : 0);
+                      (a.coarse_base ? (WIN * DT) * sizeof(S) : 0);
   static bool attr = false;
   if (!attr) {
     const size_t smax = (size_t)(DT * DmmaDims<NP>::XL) * sizeof(double) + 8 * DT * sizeof(int) +
-                        (WIN * WIN + WIN * DT) * sizeof(S);
+                        (WIN * DT) * sizeof(S);
     HELM_CUDA(cudaFuncSetAttribute(local_fdm_dmma_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)smax));
     attr = true;
