@@ -322,13 +322,26 @@ def run_ours(a, rank, world, local_rank):
             rep = hb.gmres(prob.A, M, brnd, cfg)
         t_iter = rep.wall_seconds / rep.iterations
         Ns = N * 16
-        t_roof = sum(composite_roof(model, bw, FP64_PEAK_TFLOPS) + (2 * Ns + (3 * (j + 1) + 4) * Ns) / (bw * 1e9)
-                     for j in range(rep.iterations)) / rep.iterations
+        # CGS2 at basis j+1 moves (3(j+1)+4) N s.  The device applies the second
+        # pass only where the reference's test asks for it (gmres.py:117-120); without it an
+        # Arnoldi step moves (2(j+1)+4) N s -- the roofline of the bytes actually required
+        p_re = rep.reorth_iterations / rep.iterations
+        base_t = composite_roof(model, bw, FP64_PEAK_TFLOPS) + 2 * Ns / (bw * 1e9)
+        t_roof = sum(base_t + (3 * (j + 1) + 4) * Ns / (bw * 1e9) for j in range(rep.iterations)) / rep.iterations
+        t_roof_act = sum(base_t + ((3 if p_re >= 1 else 2 + p_re) * (j + 1) + 4) * Ns / (bw * 1e9)
+                         for j in range(rep.iterations)) / rep.iterations
         gm.update({"fixed_rhs": "seed-0 random complex", "fixed_iterations": rep.iterations,
                    "fixed_iter_per_s": round(rep.iterations / rep.wall_seconds, 2),
                    "fixed_ms_per_iter": round(t_iter * 1e3, 4),
                    "roofline": {"T_roof_ms_per_iter": round(t_roof * 1e3, 4), "frac": round(t_roof / t_iter, 4),
-                                "note": "mean over the run of max-phase roofline of M^-1 + A x + CGS2 at basis j+1"},
+                                "note": "mean over the run of max-phase roofline of M^-1 + A x + CGS2 at basis j+1 "
+                                        "(SURVEY §8(d): 3 basis sweeps)",
+                                "reorth_iterations": rep.reorth_iterations,
+                                "T_roof_actual_ms_per_iter": round(t_roof_act * 1e3, 4),
+                                "frac_actual": round(t_roof_act / t_iter, 4),
+                                "note_actual": "the same with the basis sweeps the run actually needed (the "
+                                               "conditional re-orthogonalisation of gmres.py:117-120 ran in "
+                                               f"{rep.reorth_iterations} of {rep.iterations} iterations)"},
                    "fixed_clocks": gclk.summary()})
         # (3) multi-right-hand-side GMRES (helm_gmres_multi): 8 seed-0 random
         # right-hand sides, the same fixed-length run, operators applied to the batch of 8

@@ -142,7 +142,7 @@ typedef struct helm_gmres_report {
   int32_t iterations;
   int32_t converged;
   int32_t breakdown;
-  int32_t _pad;
+  int32_t reorth;        /* iterations whose re-orthogonalisation pass ran (gmres.py:117-120) */
   double final_residual;
   double wall_seconds;
 } helm_gmres_report;

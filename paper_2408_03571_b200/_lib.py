@@ -80,7 +80,7 @@ class HelmGmresReport(ctypes.Structure):
         ("iterations", ctypes.c_int32),
         ("converged", ctypes.c_int32),
         ("breakdown", ctypes.c_int32),
-        ("_pad", ctypes.c_int32),
+        ("reorth", ctypes.c_int32),
         ("final_residual", ctypes.c_double),
         ("wall_seconds", ctypes.c_double),
     ]

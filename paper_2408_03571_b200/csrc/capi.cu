@@ -179,6 +179,7 @@ static void gmres_impl(const helm_plan* P, helm_workspace* ws, const S* b, S* x,
     Vp = (S*)basis_ensure(ws, (size_t)nvec * vbytes, (size_t)(mi + 1) * vbytes, 16 * vbytes, st);
   };
   ensure_basis(2);
+  rep->reorth = 0;
   DevBuf<S> H((size_t)(mi + 1) * mi, st), cs(mi, st), sn(mi, st), g(mi + 1, st), y(mi + 1, st), u(N, st), r(N, st);
   HELM_CHECK(krylov_scratch_bytes(mi + 1) <= ws->red_bytes, "iteration cap too large for the workspace scratch");
   void* scratch = ws->red;
@@ -268,7 +269,7 @@ static void gmres_impl(const helm_plan* P, helm_workspace* ws, const S* b, S* x,
     krylov_cgs2_impl<S>(Vp, j, N, N, H.p + j, (size_t)mi, scal.p + 2, scratch, st, H.p, mi, cs.p, sn.p, g.p, beta,
                         scal.p + 4);
     if (trace) HELM_CUDA(cudaEventRecord(tev[2], st));
-    HELM_CUDA(cudaMemcpyAsync(slot + 4 * (j & 1), scal.p + 2, 3 * sizeof(double), cudaMemcpyDeviceToHost, st));
+    HELM_CUDA(cudaMemcpyAsync(slot + 4 * (j & 1), scal.p + 2, 4 * sizeof(double), cudaMemcpyDeviceToHost, st));
     HELM_CUDA(cudaEventRecord(sev[j & 1], st));
   };
   auto tprev = std::chrono::steady_clock::now();
@@ -295,6 +296,7 @@ static void gmres_impl(const helm_plan* P, helm_workspace* ws, const S* b, S* x,
     const double* hj = slot + 4 * (j & 1);
     const bool brk = hj[1] != 0.0;
     const double est = hj[2];
+    rep->reorth += hj[3] != 0.0;  // the conditional second Gram-Schmidt pass ran (gmres.py:117-120)
     est2 = est1;
     est1 = est;
     if (trace) {  // HELM_GMRES_TRACE=1: per-iteration device times of the operator and of CGS2

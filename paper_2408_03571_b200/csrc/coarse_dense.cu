@@ -10,7 +10,7 @@
 //
 //   i.e. Y = V ((V^T C V) .* invden) V^T on the m0 x m0 coarse array C: four dense GEMMs,
 //   followed by refine_steps iterative-refinement steps r = C - A0 Y with the reference's own
-//   Galerkin matrix (a 2-D stencil, a0_residual_kernel) that take the solve to the rounding
+//   Galerkin matrix (a 2-D stencil, a0_stencil_residual_kernel) that take the solve to the rounding
 //   level of the reference's SuperLU solve (linalg.py:90-95).  The sizes where these spaces are used (the
 //   paper's tables, n <= 801, m0 <= 201) make this a latency-bound path, not a roofline one.
 #include "ops.cuh"
@@ -151,7 +151,7 @@ static void dense_gemm(GemmOp A, GemmOp B, S* C, const S* scale_by, bool accumul
 // Kronecker form T0(x)M0 + M0(x)T0 - k^2 M0(x)M0, which differs from it at the rounding level
 // (amplified by cond(A0) near a coarse resonance).
 template <typename S>
-__global__ void __launch_bounds__(256) a0_residual_kernel(const S* __restrict__ c, const S* __restrict__ y,
+__global__ void __launch_bounds__(256) a0_stencil_residual_kernel(const S* __restrict__ c, const S* __restrict__ y,
                                                           S* __restrict__ res, const S* __restrict__ st, int bw,
                                                           int m) {
   pdl_wait();
@@ -208,7 +208,7 @@ void launch_coarse_solve_dense(const helm_plan* P, helm_workspace* ws, const S* 
   const S* a0 = static_cast<const S*>(d.a0_stencil);
   for (int it = 0; it < P->desc.refine_steps; ++it) {
     dim3 blk(32, 8), grd((m + 31) / 32, (m + 7) / 8, batch);
-    launch_pdl(a0_residual_kernel<S>, grd, blk, 0, st, src, (const S*)y, rr, a0, d.a0_bw, m);
+    launch_pdl(a0_stencil_residual_kernel<S>, grd, blk, 0, st, src, (const S*)y, rr, a0, d.a0_bw, m);
     HELM_LAUNCH_CHECK();
     fdm_solve<S>(P, rr, y, t1, t2, true, batch, st);
   }

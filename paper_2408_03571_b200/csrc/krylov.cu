@@ -10,6 +10,7 @@
 // orthogonal to working precision, which is what fixes the iteration count.
 // H, the rotations and g stay on the device; the host reads one estimate.
 #include <algorithm>
+#include <cstdlib>
 
 #include "ops.cuh"
 
@@ -332,9 +333,19 @@ struct GivensArgs {
   void* g;
   double beta;
   double* est;
+  int always_reorth;  // 1: the second Gram-Schmidt pass is always applied (HELM_CGS_ALWAYS=1)
 };
 
 constexpr int UW = 2;  // warps per block in the update+dots sweep
+
+// HELM_CGS_ALWAYS=1: apply the second pass unconditionally (classical CGS2)
+static int cgs_always_reorth() {
+  static const int v = [] {
+    const char* e = getenv("HELM_CGS_ALWAYS");
+    return (e && e[0] == '1') ? 1 : 0;
+  }();
+  return v;
+}
 
 // K2: w' = w - V h1 (stored), dots V^H w', ||w'||^2.  A warp owns 32-element chunks.
 // STAGED: the chunk's nvec basis rows are copied to the warp's shared-memory stage with
@@ -436,11 +447,29 @@ __global__ void __launch_bounds__(UW * 32) cgs_update_dots_kernel(const S* __res
     if (threadIdx.x == 0) wn2 = s;
   }
   __syncthreads();
-  __shared__ double mx[UW], h2n[UW];
-  double m = 0.0, q2 = 0.0;
+  // The re-orthogonalisation is applied only where orthogonality degraded, exactly the
+  // reference's test (gmres.py:117-120): max |V^H w'| > 1e-8 ||w'||.  Otherwise the column is h1,
+  // ||w''|| = ||w'||, and K3 only normalises (no third sweep of V).
+  __shared__ double mx[UW], h2n[UW], h2m[UW];
+  __shared__ int reorth_s;
   const int j = nvec - 1;
+  {
+    double m2 = 0.0;
+    for (int i = threadIdx.x; i <= j; i += UW * 32) m2 = fmax(m2, sqrt(abs2(h2[i])));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m2 = fmax(m2, __shfl_xor_sync(0xffffffffu, m2, o));
+    if ((threadIdx.x & 31) == 0) h2m[threadIdx.x >> 5] = m2;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int k = 0; k < UW; ++k) m2 = fmax(m2, h2m[k]);
+      reorth_s = gv.always_reorth || m2 > 1e-8 * fmax(sqrt(wn2), 2.2250738585072014e-308);
+    }
+    __syncthreads();
+  }
+  const bool reorth = reorth_s;
+  double m = 0.0, q2 = 0.0;
   for (int i = threadIdx.x; i <= j; i += UW * 32) {
-    const S b2 = h2[i];
+    const S b2 = reorth ? h2[i] : Sc<S>::zero();
     const S v = add(h1[i], b2);
     hcol[(size_t)i * hstride] = v;
     m = fmax(m, sqrt(abs2(v)));
@@ -462,6 +491,7 @@ __global__ void __launch_bounds__(UW * 32) cgs_update_dots_kernel(const S* __res
       m = fmax(m, mx[k]);
       q += h2n[k];
     }
+    inv[3] = reorth ? 1.0 : 0.0;
     const double hn = sqrt(fmax(wn2 - q, 0.0));
     hcol[(size_t)(j + 1) * hstride] = Sc<S>::from_real(hn);
     // breakdown test of gmres.py:125 on max |H[:j+2, j]|
@@ -484,6 +514,10 @@ __global__ void __launch_bounds__(KB) cgs_final_kernel(const S* __restrict__ V, 
   __syncthreads();
   const double f0 = inv[0];
   const double f = f0 == 0.0 ? 1.0 : f0;
+  if (inv[3] == 0.0) {  // no re-orthogonalisation this iteration: normalise w' only
+    for (size_t n = blockIdx.x * (size_t)KB + threadIdx.x; n < N; n += (size_t)gridDim.x * KB) w[n] = scale(w[n], f);
+    return;
+  }
   for (size_t n = blockIdx.x * (size_t)KB + threadIdx.x; n < N; n += (size_t)gridDim.x * KB) {
     S xa = w[n], xb = Sc<S>::zero();
     int i = 0;
@@ -570,14 +604,16 @@ template <typename S> void krylov_norm2(const S* x, size_t N, double* out, void*
 template <typename S>
 void krylov_cgs2_impl(S* V, int j, size_t ldv, size_t N, S* hcol, size_t hstride, double* inv_out, void* scratch,
                       cudaStream_t st, S* H, int ldh, S* cs, S* sn, S* g, double beta, double* est_out) {
-  GivensArgs gv{H, ldh, cs, sn, g, beta, est_out};
+  GivensArgs gv{H, ldh, cs, sn, g, beta, est_out, cgs_always_reorth()};
   cgs2_run<S>(V, j, ldv, N, hcol, hstride, inv_out, scratch, gv, st);
 }
 
 template <typename S>
 void krylov_cgs2(S* V, int j, size_t ldv, size_t N, S* hcol, void* scratch, cudaStream_t st) {
   CgsScratch k = carve(scratch, j + 1);
-  cgs2_run<S>(V, j, ldv, N, hcol, 1, k.scal + 2, scratch, GivensArgs{}, st);
+  GivensArgs gv{};
+  gv.always_reorth = cgs_always_reorth();
+  cgs2_run<S>(V, j, ldv, N, hcol, 1, k.scal + 2, scratch, gv, st);
 }
 
 template <typename S>

@@ -51,6 +51,7 @@ class SolveReport:
     breakdown: bool = False
     wall_seconds: float = field(default=0.0)
     x: object = None
+    reorth_iterations: int = 0  # iterations whose conditional re-orthogonalisation ran (device detail)
 
 
 def _resolve(A, M_inv):
@@ -105,6 +106,7 @@ def gmres(A, M_inv, b, cfg: GmresConfig = GmresConfig()) -> SolveReport:
         breakdown=bool(rep.breakdown),
         wall_seconds=float(rep.wall_seconds),
         x=v.out(x),
+        reorth_iterations=int(rep.reorth),
     )
 
 
