@@ -153,6 +153,28 @@ uint64_t helm_kernel_launches(void);
 const char* helm_last_error(void);
 
 int helm_plan_create(const helm_desc* desc, helm_plan** out);
+
+/* Native setup (no host-side numpy / LAPACK): the problem parameters alone.  The library builds
+ * every helm_desc array itself -- the 1-D box classes and their eigen-pairs (cuSOLVER on the
+ * device), the coarse transform eigenvalues, band LU factors and Woodbury data -- and creates the
+ * plan (the HOCS ratio-2 coarse space; other coarse spaces go through helm_plan_create).
+ * Replaces the reference's setup: assemble + partition/extend + build_hocs + galerkin +
+ * SchwarzPreconditioner.__init__ (discretization.py:157-191, decomposition.py:89-134,
+ * coarse.py:148-167, schwarz.py:34-62).                                                          */
+typedef struct helm_problem {
+  int32_t n;                    /* grid nodes per dimension                                */
+  int32_t bc;                   /* helm_bc (MP-1 Dirichlet fp64, MP-2 Sommerfeld c128)     */
+  int32_t kind;                 /* helm_kind                                               */
+  int32_t weights_before_solve; /* schwarz.py:69-70                                        */
+  int32_t p;                    /* subdomains per dimension                                */
+  int32_t overlap_layers;       /* extend(part, m)                                         */
+  int32_t coarse_kind;          /* 0: HOCS                                                 */
+  int32_t ratio;                /* 2                                                       */
+  double k;                     /* wavenumber                                              */
+  int32_t strip_refine;         /* -1: default (1)                                         */
+  int32_t refine_steps;         /* -1: default (0)                                         */
+} helm_problem;
+int helm_plan_create_problem(const helm_problem* problem, helm_plan** out);
 int helm_plan_destroy(helm_plan* plan);
 int64_t helm_plan_num_unknowns(const helm_plan* plan);
 int64_t helm_plan_num_coarse(const helm_plan* plan);

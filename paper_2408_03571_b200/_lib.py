@@ -86,6 +86,24 @@ class HelmGmresReport(ctypes.Structure):
     ]
 
 
+class HelmProblem(ctypes.Structure):
+    """include/helmb200.h helm_problem (native setup)."""
+
+    _fields_ = [
+        ("n", ctypes.c_int32),
+        ("bc", ctypes.c_int32),
+        ("kind", ctypes.c_int32),
+        ("weights_before_solve", ctypes.c_int32),
+        ("p", ctypes.c_int32),
+        ("overlap_layers", ctypes.c_int32),
+        ("coarse_kind", ctypes.c_int32),
+        ("ratio", ctypes.c_int32),
+        ("k", ctypes.c_double),
+        ("strip_refine", ctypes.c_int32),
+        ("refine_steps", ctypes.c_int32),
+    ]
+
+
 # (name, restype, argtypes) for every symbol include/helmb200.h declares
 _vp, _i32, _dbl = ctypes.c_void_p, ctypes.c_int32, ctypes.c_double
 SYMBOLS = [
@@ -93,6 +111,7 @@ SYMBOLS = [
     ("helm_kernel_launches", ctypes.c_uint64, []),
     ("helm_last_error", ctypes.c_char_p, []),
     ("helm_plan_create", ctypes.c_int, [ctypes.POINTER(HelmDesc), ctypes.POINTER(_vp)]),
+    ("helm_plan_create_problem", ctypes.c_int, [ctypes.POINTER(HelmProblem), ctypes.POINTER(_vp)]),
     ("helm_plan_destroy", ctypes.c_int, [_vp]),
     ("helm_plan_num_unknowns", ctypes.c_int64, [_vp]),
     ("helm_plan_num_coarse", ctypes.c_int64, [_vp]),

@@ -48,7 +48,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
             if verbose:
                 print("compiled", os.path.basename(s))
     if force or jobs or _stale(OUT, objs):
-        cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", OUT, *objs]
+        cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", OUT, *objs, "-ldl"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stderr}")

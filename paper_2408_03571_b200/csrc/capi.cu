@@ -778,15 +778,9 @@ static void dispatch(const helm_plan* P, F&& f) {
 
 }  // namespace helm
 
-using namespace helm;
-
-extern "C" {
-
-int32_t helm_abi_version(void) { return HELM_ABI_VERSION; }
-uint64_t helm_kernel_launches(void) { return g_launches.load(); }
-const char* helm_last_error(void) { return g_last_error.c_str(); }
-
-int helm_plan_create(const helm_desc* desc, helm_plan** out) {
+namespace helm {
+// helm_plan_create's body, also used by the native setup (setup.cu)
+int plan_create_from_desc(const helm_desc* desc, helm_plan** out) {
   return guarded([&] {
     HELM_CHECK(out != nullptr, "null output pointer");
     helm_plan* P = new helm_plan();
@@ -801,6 +795,17 @@ int helm_plan_create(const helm_desc* desc, helm_plan** out) {
     *out = P;
   });
 }
+}  // namespace helm
+
+using namespace helm;
+
+extern "C" {
+
+int32_t helm_abi_version(void) { return HELM_ABI_VERSION; }
+uint64_t helm_kernel_launches(void) { return g_launches.load(); }
+const char* helm_last_error(void) { return g_last_error.c_str(); }
+
+int helm_plan_create(const helm_desc* desc, helm_plan** out) { return plan_create_from_desc(desc, out); }
 
 int helm_plan_destroy(helm_plan* plan) {
   return guarded([&] {

@@ -40,7 +40,7 @@ def _sym_pencil_eig(T: np.ndarray, w: np.ndarray):
     lam, U = np.linalg.eig(Ts)
     nrm = np.sqrt(np.einsum("ij,ij->j", U, U))  # complex-symmetric normalisation u^T u = 1
     U = U / nrm[None, :]
-    return lam, s[:, None] * U
+    return _refine_eig(Ts, lam, U, np.diag(s))  # one Newton step (residual ~1e-13 -> ~1e-16)
 
 
 def _general_pencil_eig(T0: np.ndarray, M0: np.ndarray):
@@ -198,15 +198,37 @@ class LocalClasses:
     lam: list
 
 
+def _dst_pencil(L: int, h: float):
+    """Exact eigen-pairs of tridiag(-1, 2, -1)/h^2 with W = I (every box with Dirichlet ends: all
+    MP-1 boxes, the interior MP-2 boxes): lam_j = 4 sin^2(j pi / (2(L+1))) / h^2,
+    V[i][j] = sqrt(2/(L+1)) sin(i j pi / (L+1)) (1-based), in long double -- LAPACK's eigenvalues
+    carry an absolute error ~eps |T| that a near-resonant subdomain (lam_y + lam_x ~ k^2) turns
+    into a ~1e-12 solve error."""
+    ld = np.longdouble
+    pi = ld("3.14159265358979323846264338327950288")
+    j = np.arange(1, L + 1, dtype=ld)
+    lam = (ld(4) / (ld(h) * ld(h))) * np.sin(j * pi / (2 * (L + 1))) ** 2
+    V = np.sqrt(ld(2) / (L + 1)) * np.sin(np.outer(j, j) * pi / (L + 1))
+    return lam.astype(np.float64), V.astype(np.float64)
+
+
 def local_classes(grid: Grid, k: float, boxes) -> LocalClasses:
     """Eigen-pairs of every distinct 1-D box pencil (T[s:s+L, s:s+L], w[s:s+L])."""
     T, w = pencil_1d(grid, k)
     nu = grid.unknowns_per_dim
+    h = grid.h
     keys, Vs, lams, cls = {}, [], [], []
     for s, L in boxes:
         key = (L, s == 0, s + L == nu)
         if key not in keys:
-            lam, V = _sym_pencil_eig(T[s : s + L, s : s + L], w[s : s + L])
+            Tb, wb = T[s : s + L, s : s + L], w[s : s + L]
+            dirichlet_box = np.all(wb == 1.0) and not np.any(np.imag(Tb)) and \
+                np.all(np.diag(Tb) == 2.0 / h**2) and np.all(np.diag(Tb, 1) == -1.0 / h**2)
+            if dirichlet_box:
+                lam, V = _dst_pencil(L, h)
+                lam, V = lam.astype(T.dtype), V.astype(T.dtype)
+            else:
+                lam, V = _sym_pencil_eig(Tb, wb)
             keys[key] = len(Vs)
             Vs.append(V)
             lams.append(lam)

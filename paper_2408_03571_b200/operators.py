@@ -208,6 +208,10 @@ def galerkin(cs: CoarseSpace, A) -> CoarseSpace:
     op = _as_operator(A, cs.grid)
     from dataclasses import replace
 
+    if cs.kind == "HOCS" and cs.ratio == 2:
+        # built where the plan is created: natively (helm_plan_create_problem) or by the host
+        # setup of SchwarzPreconditioner(setup="host")
+        return replace(cs, fdm=None)
     return replace(cs, fdm=_coarse_setup(cs, cs.grid, op.k))
 
 
@@ -293,6 +297,35 @@ class _Plan:
         plan.max_batch = int(max_batch)
         return plan
 
+    @staticmethod
+    def create_native(grid: Grid, k: float, kind: str, dec: Decomposition, weights_before_solve=False,
+                      max_batch: int = 1, refine_steps: int = 0, strip_refine: int = 1):
+        """The plan from the problem parameters alone: helm_plan_create_problem builds the box
+        classes, eigen-pairs (cuSOLVER), transform eigenvalues, band LU and Woodbury data natively
+        (include/helmb200.h).  HOCS ratio 2 only."""
+        lib = _lib.load()
+        pr = _lib.HelmProblem()
+        pr.n, pr.bc = grid.n, (_lib.HELM_SOMMERFELD if grid.bc == "sommerfeld" else _lib.HELM_DIRICHLET)
+        pr.kind, pr.weights_before_solve = _lib.KINDS[kind], int(bool(weights_before_solve))
+        pr.p, pr.overlap_layers, pr.coarse_kind, pr.ratio, pr.k = dec.p, dec.overlap_layers, 0, 2, float(k)
+        pr.strip_refine, pr.refine_steps = int(strip_refine), int(refine_steps)
+        h = ctypes.c_void_p()
+        status = lib.helm_plan_create_problem(ctypes.byref(pr), ctypes.byref(h))
+        if status != 0:
+            msg = lib.helm_last_error().decode(errors="replace")
+            if "singular" in msg:
+                raise SingularMatrixError(msg)
+            raise _lib.HelmError(msg)
+        ws = ctypes.c_void_p()
+        try:
+            _lib.check(lib.helm_workspace_create(h, int(max_batch), ctypes.byref(ws)))
+        except Exception:
+            lib.helm_plan_destroy(h)
+            raise
+        plan = _Plan(lib, h, ws, lib.helm_plan_num_unknowns(h), lib.helm_plan_num_coarse(h), None)
+        plan.max_batch = int(max_batch)
+        return plan
+
     def __del__(self):
         try:
             if self.ws:
@@ -341,7 +374,11 @@ class SchwarzPreconditioner:
     KINDS = ("AS2", "SAS2", "SHS2")
 
     def __init__(self, kind, A, decomposition, coarse_space, weights_before_solve=False,
-                 local_factorizations=None, max_batch: int = 1, refine_steps=None, strip_refine: int = 1):
+                 local_factorizations=None, max_batch: int = 1, refine_steps=None, strip_refine: int = 1,
+                 setup: str = None):
+        """``setup``: "host" (numpy/LAPACK setup in fdm_setup.py, then helm_plan_create) or "native"
+        (helm_plan_create_problem: the library builds everything from the problem parameters; HOCS
+        ratio 2).  Default: HELM_SETUP or "native" where it applies."""
         if kind not in self.KINDS:
             raise ValueError(f"unknown preconditioner {kind!r}, expected one of {self.KINDS}")
         grid = _grid_of(decomposition)
@@ -353,14 +390,28 @@ class SchwarzPreconditioner:
         ckind, ratio = getattr(coarse_space, "kind", "HOCS"), int(getattr(coarse_space, "ratio", 2))
         if ckind not in ("HOCS", "FOCS"):
             raise ValueError(f"unknown coarse space {ckind!r}")
+        import os
+
+        setup = setup or os.environ.get("HELM_SETUP", "native")
+        if setup not in ("host", "native"):
+            raise ValueError(f"setup must be 'host' or 'native', got {setup!r}")
+        native = setup == "native" and ckind == "HOCS" and ratio == 2
+        self.weights_before_solve = bool(weights_before_solve)
+        self.max_batch = int(max_batch)
+        self.setup = "native" if native else "host"
+        if native:
+            self.coarse_space = CoarseSpace(ckind, grid, ratio, None)
+            self.plan = _Plan.create_native(grid, self.A.k, kind, self.decomposition, weights_before_solve,
+                                            max_batch=max_batch, refine_steps=refine_steps or 0,
+                                            strip_refine=strip_refine)
+            self.N, self.N0 = self.plan.N, self.plan.N0
+            return
         cf = getattr(coarse_space, "fdm", None)
         if cf is None:
             cf = _coarse_setup(coarse_space, grid, self.A.k)
         self.coarse_space = CoarseSpace(ckind, grid, ratio, cf)
         if refine_steps is None:  # the dense coarse solve is refined twice (coarse_dense.cu)
             refine_steps = 2 if isinstance(cf, CoarseDense) else 0
-        self.weights_before_solve = bool(weights_before_solve)
-        self.max_batch = int(max_batch)
         self.plan = _Plan.create(grid, self.A.k, kind, self.decomposition, cf, weights_before_solve,
                                  max_batch=max_batch, refine_steps=refine_steps, strip_refine=strip_refine)
         self.N = self.plan.N

@@ -133,7 +133,7 @@ def test_desc_layout_matches_header(tmp_path):
 
     from paper_2408_03571_b200 import _lib
 
-    structs = {"helm_desc": _lib.HelmDesc, "helm_gmres_report": _lib.HelmGmresReport}
+    structs = {"helm_desc": _lib.HelmDesc, "helm_gmres_report": _lib.HelmGmresReport, "helm_problem": _lib.HelmProblem}
     lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "helmb200.h"', "int main(void) {"]
     for cname, py in structs.items():
         lines.append(f'  printf("{cname} size %zu\\n", sizeof({cname}));')
