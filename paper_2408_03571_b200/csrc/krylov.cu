@@ -564,7 +564,11 @@ static void cgs2_run(S* V, int j, size_t ldv, size_t N, S* hcol, size_t hstride,
     launch_pdl(kern, grid, UW * 32, smem, st, V, nvec, ldv, w, N, (const S*)k.h1, (S*)k.partial, k.npart, (S*)k.h2,
                                       k.count + 1, hcol, hstride, inv_out, gv);
   };
-  if (sm2s <= SMEM_MAX) {
+  static const bool staged_ok = [] {
+    const char* e = getenv("HELM_CGS_STAGED");
+    return !(e && e[0] == '0');
+  }();
+  if (staged_ok && sm2s <= SMEM_MAX) {
     const int bps = (int)std::min<size_t>(8, std::max<size_t>(1, (SMEM_MAX + 1024) / (sm2s + 1024)));
     if (E == 8) launch2(cgs_update_dots_kernel<S, true, 8>, 148 * bps, sm2s);
     else if (E == 4) launch2(cgs_update_dots_kernel<S, true, 4>, 148 * bps, sm2s);
