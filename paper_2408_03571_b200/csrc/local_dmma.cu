@@ -16,9 +16,52 @@
 // feeds three DMMAs and the products update the shared tile in place with warp-level
 // synchronisation only.  Shared strides are chosen so every fragment load is two
 // wavefronts (the minimum for 32 x 8-byte accesses).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cstdlib>
+#include <cstring>
+
 #include "local.cuh"
 
 namespace helm {
+
+// ---------------------------------------------------------------------------------------
+// TMA box load (complex boxes): one cp.async.bulk.tensor.3d per (box, right-hand side) moves
+// the whole 35 x 35 complex box (rows of 70 doubles) into shared memory, tracked by an mbarrier.
+// Real (MP-1) rows are nu x 8 bytes, not a multiple of 16 for odd nu, so they keep cp.async.
+// ---------------------------------------------------------------------------------------
+struct TmaBox {
+  CUtensorMap map;  // dims {2 nu, nu, batch} doubles, box {2 BX, BY, 1}
+  int bx, by;       // box extent in complex columns / rows (0: TMA off)
+};
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"((unsigned)__cvta_generic_to_shared(bar)), "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(
+                   (unsigned)__cvta_generic_to_shared(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n LAB_WAIT:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra LAB_WAIT;\n}\n" ::"r"((unsigned)__cvta_generic_to_shared(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+      "[%5];\n" ::"r"((unsigned)__cvta_generic_to_shared(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"((unsigned)__cvta_generic_to_shared(bar))
+      : "memory");
+}
 
 constexpr int DB = 20;      // folded block (even / odd modes)
 constexpr int DT = 2 * DB;  // tile side
@@ -143,11 +186,11 @@ __global__ void __launch_bounds__(DTH, 5) local_fdm_dmma_kernel(const S* __restr
                                                              const int* __restrict__ boxes,
                                                              const double* __restrict__ classVf,
                                                              const double* __restrict__ classInvden, int ncls,
-                                                             LocalArgs a) {
+                                                             LocalArgs a, const __grid_constant__ TmaBox tma) {
   pdl_wait();  // PDL: the predecessor's writes are visible (no-op without PDL)
   constexpr int NP = Sc<S>::cplx ? 2 : 1;
   constexpr int XL = DmmaDims<NP>::XL;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  extern __shared__ __align__(128) unsigned char smem_raw[];  // 128-byte aligned: the TMA destination
   double* Xr = reinterpret_cast<double*>(smem_raw);  // [DT][XL]
   // per row (y) / column (x) of the box: the output address terms and weights of every node
   // (decomposition.py:111-134), so the scatter does no per-node index arithmetic:
@@ -172,7 +215,18 @@ __global__ void __launch_bounds__(DTH, 5) local_fdm_dmma_kernel(const S* __restr
   S* ob = ovl + (size_t)b * 6 * a.nbands * nu;
   // the raw box streams into the X tile with cp.async (row r at Xr + r XL, scalars in place):
   // every thread has all its copies in flight at once instead of a chain of dependent loads
-  {
+  __shared__ __align__(8) uint64_t box_bar;
+  const bool use_tma = NP == 2 && tma.bx >= Lx && tma.by >= Ly;
+  const int RS = use_tma ? 2 * tma.bx : XL;  // row stride (doubles) of the raw box in Xr
+  if (use_tma) {
+    if (threadIdx.x == 0) {
+      mbar_init(&box_bar, 1);
+      asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+      mbar_expect_tx(&box_bar, (unsigned)(2 * tma.bx * tma.by * sizeof(double)));
+      tma_load_3d(Xr, &tma.map, 2 * x0, y0, b, &box_bar);
+    }
+    __syncthreads();  // the barrier is initialised before any thread waits on it
+  } else {
     const int q = threadIdx.x % DT;  // column of this thread (constant divisor: no runtime division)
     if (q < Lx)
       for (int r = threadIdx.x / DT; r < Ly; r += DTH / DT) {
@@ -191,8 +245,8 @@ __global__ void __launch_bounds__(DTH, 5) local_fdm_dmma_kernel(const S* __restr
   const bool wb = a.weighted && a.wbs;
   auto raw = [&](int r, int q) -> S {
     S v;
-    if constexpr (NP == 2) v = mk(Xr[r * XL + 2 * q], Xr[r * XL + 2 * q + 1]);
-    else v = Xr[r * XL + q];
+    if constexpr (NP == 2) v = mk(Xr[r * RS + 2 * q], Xr[r * RS + 2 * q + 1]);
+    else v = Xr[r * RS + q];
     if (wb) v = scale(v, 1.0 / (a.node_mult[y0 + r] * a.node_mult[x0 + q]));
     return v;
   };
@@ -206,6 +260,7 @@ __global__ void __launch_bounds__(DTH, 5) local_fdm_dmma_kernel(const S* __restr
   constexpr int QPT = (DB * DB + DTH - 1) / DTH;  // quads per thread
   S qv[QPT][4];
   cp_wait<0>();
+  if (use_tma) mbar_wait(&box_bar, 0);
   __syncthreads();
 #pragma unroll
   for (int u = 0; u < QPT; ++u) {
@@ -352,6 +407,24 @@ __global__ void __launch_bounds__(DTH, 5) local_fdm_dmma_kernel(const S* __restr
   }
 }
 
+static PFN_cuTensorMapEncodeTiled_v12000 encode_tiled() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    HELM_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+    HELM_CHECK(p != nullptr && q == cudaDriverEntryPointSuccess, "driver entry point missing: cuTensorMapEncodeTiled");
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }();
+  return fn;
+}
+static bool tma_enabled() {  // HELM_TMA=0: cp.async box loads everywhere (A/B)
+  static const bool on = [] {
+    const char* e = getenv("HELM_TMA");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 template <typename S>
 void launch_local_dmma(const helm_plan* P, const S* x, const S* base, S* y, S* ovl, const LocalArgs& a, int batch,
                        cudaStream_t st) {
@@ -368,9 +441,27 @@ void launch_local_dmma(const helm_plan* P, const S* x, const S* base, S* y, S* o
                                    (int)smax));
     attr = true;
   }
+  TmaBox tma;
+  std::memset(&tma, 0, sizeof(tma));
+  if (NP == 2 && tma_enabled()) {
+    // box extent = the largest folded box (every folded MP-2 box is an interior one)
+    int bx = 0;
+    for (int c = 0; c < (int)P->h_class_len.size(); ++c) bx = std::max(bx, P->h_class_len[c]);
+    if (bx <= DB * 2 && 2 * bx <= 256 && bx <= 256) {
+      const cuuint64_t dims[3] = {(cuuint64_t)2 * a.nu, (cuuint64_t)a.nu, (cuuint64_t)batch};
+      const cuuint64_t strides[2] = {(cuuint64_t)a.nu * 16, (cuuint64_t)a.nu * a.nu * 16};
+      const cuuint32_t box[3] = {(cuuint32_t)(2 * bx), (cuuint32_t)bx, 1};
+      const cuuint32_t es[3] = {1, 1, 1};
+      const CUresult r = encode_tiled()(&tma.map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<S*>(x), dims, strides,
+                                        box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      HELM_CHECK(r == CUDA_SUCCESS, "cuTensorMapEncodeTiled failed for the local box load");
+      tma.bx = tma.by = bx;
+    }
+  }
   dim3 grd(d.n_ff, batch);
   launch_pdl(local_fdm_dmma_kernel<S>, grd, DTH, smem, st, x, base, y, ovl, d.box_ff, d.class_Vf, d.class_invden,
-                                                   d.n_classes, a);
+                                                   d.n_classes, a, tma);
   HELM_LAUNCH_CHECK();
 }
 
