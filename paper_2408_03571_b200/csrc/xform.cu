@@ -12,6 +12,7 @@
 // in place through a barrier, twiddles tabulated once per CTA with sincospi.
 // Real rows are packed two per FFT: Q is real, so DST(x + i y) = DST(x) + i DST(y).  Rows are read and written with coalesced
 // 8/16-byte accesses; the transform is HBM-bound at the BASELINE sizes.
+#include <cstdlib>
 #include <type_traits>
 
 #include "ops.cuh"
@@ -72,11 +73,41 @@ __device__ __forceinline__ void dft4(double2 v[4]) {
   v[3] = mk(b.x - d.y, b.y + d.x);  // b + i d
 }
 
+// In-register 16-point DFT (natural order in and out) as 4 x 4: DFT4 over the stride-4
+// subsequences, twiddles W16^(n2 k1), DFT4 across them.
+__device__ __forceinline__ void dft16(double2 v[16]) {
+  constexpr double c1 = 0.92387953251128675613, s1 = 0.38268343236508977173, h = 0.70710678118654752440;
+  // W16^m = exp(-2 pi i m / 16), m = 0 .. 9
+  const double2 w[10] = {mk(1.0, 0.0), mk(c1, -s1), mk(h, -h), mk(s1, -c1), mk(0.0, -1.0),
+                         mk(-s1, -c1), mk(-h, -h), mk(-c1, -s1), mk(-1.0, 0.0), mk(-c1, s1)};
+  double2 y[4][4];
+#pragma unroll
+  for (int n2 = 0; n2 < 4; ++n2) {
+#pragma unroll
+    for (int n1 = 0; n1 < 4; ++n1) y[n2][n1] = v[4 * n1 + n2];
+    dft4(y[n2]);
+#pragma unroll
+    for (int k1 = 1; k1 < 4; ++k1)
+      if (n2) y[n2][k1] = mul(y[n2][k1], w[n2 * k1]);
+  }
+#pragma unroll
+  for (int k1 = 0; k1 < 4; ++k1) {
+    double2 z[4] = {y[0][k1], y[1][k1], y[2][k1], y[3][k1]};
+    dft4(z);
+#pragma unroll
+    for (int k2 = 0; k2 < 4; ++k2) v[k1 + 4 * k2] = z[k2];
+  }
+}
+
 // Padded shared-memory index: one spare slot every 8 and every 64 elements, so the
 // strided Stockham stores of the first stages (stride 8 and 64 double2) hit
 // distinct bank groups.
 __device__ __forceinline__ int pidx(int i) { return i + (i >> 3) + (i >> 6); }
 __host__ __device__ constexpr int padded_len(int L) { return L + L / 8 + L / 64 + 1; }
+// radix-16 stages store at stride 16 (first stage) and 256: one spare slot every 16 and 256
+__device__ __forceinline__ int pidx16(int i) { return i + (i >> 4) + (i >> 8); }
+__host__ __device__ constexpr int padded_len16(int L) { return L + L / 16 + L / 256 + 1; }
+template <int VPT> __device__ __forceinline__ int pix(int i) { return VPT == 16 ? pidx16(i) : pidx(i); }
 
 // One Stockham stage of radix R over a row of length L (T threads, NBT = 8/R butterflies
 // each).  Butterfly j: inputs X[j + r L/R], twiddles W^r with W = W_{Ns R}^{j mod Ns}
@@ -93,7 +124,7 @@ __device__ __forceinline__ void stockham_stage(double2* buf, const double2* __re
   for (int c = 0; c < NBT; ++c) {
     const int j = tid + c * T;
 #pragma unroll
-    for (int r = 0; r < R; ++r) v[c][r] = FIRST ? load(c, r, j + r * nb) : buf[pidx(j + r * nb)];
+    for (int r = 0; r < R; ++r) v[c][r] = FIRST ? load(c, r, j + r * nb) : buf[pix<VPT>(j + r * nb)];
   }
   if (!FIRST) __syncthreads();
   const int tstep = L / (Ns * R);
@@ -104,7 +135,7 @@ __device__ __forceinline__ void stockham_stage(double2* buf, const double2* __re
     if (!FIRST) {  // Ns == 1 on the first stage: all twiddles are 1
       // W^1 and W^2 from the table, the other powers by a depth-2 product tree
       // (2 loads instead of R-1: the load/store queue is this kernel's limiter)
-      double2 w[8];
+      double2 w[16];
       w[1] = tw[k * tstep];
       if (R > 2) w[2] = tw[2 * k * tstep];
       if (R > 3) w[3] = mul(w[1], w[2]);
@@ -114,10 +145,17 @@ __device__ __forceinline__ void stockham_stage(double2* buf, const double2* __re
         w[6] = mul(w[2], w[4]);
         w[7] = mul(w[3], w[4]);
       }
+      if (R > 8) {  // W^8 from the table, the rest by one product each
+        w[8] = tw[8 * k * tstep];
+#pragma unroll
+        for (int r = 9; r < 16; ++r) w[r] = mul(w[r - 8], w[8]);
+      }
 #pragma unroll
       for (int r = 1; r < R; ++r) v[c][r] = mul(v[c][r], w[r]);
     }
-    if constexpr (R == 8) {
+    if constexpr (R == 16) {
+      dft16(v[c]);
+    } else if constexpr (R == 8) {
       dft8(v[c]);
     } else if constexpr (R == 4) {
       dft4(v[c]);
@@ -130,7 +168,7 @@ __device__ __forceinline__ void stockham_stage(double2* buf, const double2* __re
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       if (LAST) store(base + r * Ns, v[c][r]);
-      else buf[pidx(base + r * Ns)] = v[c][r];
+      else buf[pix<VPT>(base + r * Ns)] = v[c][r];
     }
   }
   if (!LAST) __syncthreads();
@@ -146,6 +184,10 @@ __device__ __forceinline__ void stockham_stage(double2* buf, const double2* __re
 // instructions).
 constexpr int fft_nst(int L) { return L <= 1 ? 0 : 1 + fft_nst(L >= 8 ? L / 8 : 1); }
 constexpr int fft_rlast(int L) { return L <= 8 ? L : fft_rlast(L / 8); }
+// VPT = 16 (L >= 256): a first radix-16 stage, radix-16 middle stages, a last stage of radix
+// fft16_rlast (2..16): 2048 = 16 x 16 x 8 -- two shared-memory round trips instead of three
+constexpr int fft16_nmid(int rem) { return rem <= 16 ? 0 : 1 + fft16_nmid(rem / 16); }
+constexpr int fft16_rlast(int rem) { return rem <= 16 ? rem : fft16_rlast(rem / 16); }
 
 template <typename S, int VPT, int LT, bool DCT>
 __global__ void __launch_bounds__(256) xform_fft_kernel(const S* __restrict__ in, S* __restrict__ out, XScale sc,
@@ -153,13 +195,13 @@ __global__ void __launch_bounds__(256) xform_fft_kernel(const S* __restrict__ in
   constexpr int L = LT, m0 = DCT ? L / 2 + 1 : L / 2 - 1;
   constexpr bool dct = DCT;
   pdl_wait();  // PDL: the predecessor's writes are visible (no-op without PDL)
-  static_assert(VPT == 8, "one radix-8 butterfly per thread in the first stage");
+  static_assert(VPT == 8 || VPT == 16, "one radix-VPT butterfly per thread in the first stage");
   // tw: plan-owned table exp(-2 pi i k / L), k < L (read through L1)
   extern __shared__ __align__(16) unsigned char sraw[];
-  constexpr int T = L / 8;
+  constexpr int T = L / VPT;
   const int g = threadIdx.x / T, tid = threadIdx.x % T;
   const int rpc = blockDim.x / T;
-  double2* buf = reinterpret_cast<double2*>(sraw) + (size_t)g * padded_len(L);
+  double2* buf = reinterpret_cast<double2*>(sraw) + (size_t)g * (VPT == 16 ? padded_len16(L) : padded_len(L));
   constexpr int RPF = Sc<S>::cplx ? 1 : 2;  // rows per FFT
   const int nfft = (rows + RPF - 1) / RPF;
   constexpr int K = L / 2;
@@ -188,25 +230,25 @@ __global__ void __launch_bounds__(256) xform_fft_kernel(const S* __restrict__ in
       return mk(sg * row0[J], (r0 + 1 < rows) ? sg * row0[m0 + J] : 0.0);
     }
   };
-  double2 cur[8];
+  double2 cur[VPT];
   int f = blockIdx.x * rpc + g;
 #pragma unroll
-  for (int r = 0; r < 8; ++r) cur[r] = load(f, tid + r * T);
+  for (int r = 0; r < VPT; ++r) cur[r] = load(f, tid + r * T);
   for (int f0 = blockIdx.x * rpc; f0 < nfft; f0 += gridDim.x * rpc) {
     f = f0 + g;
     const bool active = f < nfft;
     const int r0 = (active ? f : 0) * RPF;
     const bool two = active && (RPF == 2) && (r0 + 1 < rows);
     // stage 1 from the prefetched registers, then prefetch the next row
-    double2 nxt[8];
+    double2 nxt[VPT];
     {
       const double2* c = cur;
-      stockham_stage<8, 8, true, false>(buf, tw, L, 1, tid, T, [&](int, int r, int) { return c[r]; },
-                                        [&](int, double2) {});
+      stockham_stage<VPT, VPT, true, false>(buf, tw, L, 1, tid, T, [&](int, int r, int) { return c[r]; },
+                                            [&](int, double2) {});
     }
     const int fn = f + gridDim.x * rpc;
 #pragma unroll
-    for (int r = 0; r < 8; ++r) nxt[r] = load(fn, tid + r * T);
+    for (int r = 0; r < VPT; ++r) nxt[r] = load(fn, tid + r * T);
     // DFT index e -> transform output (sum_J Q[J][a] x_J, then the scale)
     const S* row0 = in + (size_t)r0 * m0;
     double2 x0 = mk(0.0, 0.0), xm = mk(0.0, 0.0);
@@ -248,29 +290,43 @@ __global__ void __launch_bounds__(256) xform_fft_kernel(const S* __restrict__ in
       }
     };
     auto none = [&](int, int, int) { return mk(0.0, 0.0); };
-    int Ns = 8;
+    if constexpr (VPT == 8) {
+      int Ns = 8;
 #pragma unroll
-    for (int s = 1; s < nst; ++s) {
-      const bool last = s == nst - 1;
-      if (!last) {
-        stockham_stage<8, 8, false, false>(buf, tw, L, Ns, tid, T, none, store);
-        Ns *= 8;
-      } else if (rlast == 8) {
-        stockham_stage<8, 8, false, true>(buf, tw, L, Ns, tid, T, none, store);
-      } else if (rlast == 4) {
-        stockham_stage<8, 4, false, true>(buf, tw, L, Ns, tid, T, none, store);
-      } else {
-        stockham_stage<8, 2, false, true>(buf, tw, L, Ns, tid, T, none, store);
+      for (int s = 1; s < nst; ++s) {
+        const bool last = s == nst - 1;
+        if (!last) {
+          stockham_stage<8, 8, false, false>(buf, tw, L, Ns, tid, T, none, store);
+          Ns *= 8;
+        } else if (rlast == 8) {
+          stockham_stage<8, 8, false, true>(buf, tw, L, Ns, tid, T, none, store);
+        } else if (rlast == 4) {
+          stockham_stage<8, 4, false, true>(buf, tw, L, Ns, tid, T, none, store);
+        } else {
+          stockham_stage<8, 2, false, true>(buf, tw, L, Ns, tid, T, none, store);
+        }
       }
-    }
-    if (nst == 1) {  // L == 8: the first stage was also the last; emit from smem
-      __syncthreads();
-      if (tid == 0)
-        for (int e = 0; e < 8; ++e) store(e, buf[pidx(e)]);
+      if (nst == 1) {  // L == 8: the first stage was also the last; emit from smem
+        __syncthreads();
+        if (tid == 0)
+          for (int e = 0; e < 8; ++e) store(e, buf[pidx(e)]);
+      }
+    } else {
+      constexpr int nmid = fft16_nmid(L / 16), rl = fft16_rlast(L / 16);
+      int Ns = 16;
+#pragma unroll
+      for (int s = 0; s < nmid; ++s) {
+        stockham_stage<16, 16, false, false>(buf, tw, L, Ns, tid, T, none, store);
+        Ns *= 16;
+      }
+      if constexpr (rl == 16) stockham_stage<16, 16, false, true>(buf, tw, L, Ns, tid, T, none, store);
+      else if constexpr (rl == 8) stockham_stage<16, 8, false, true>(buf, tw, L, Ns, tid, T, none, store);
+      else if constexpr (rl == 4) stockham_stage<16, 4, false, true>(buf, tw, L, Ns, tid, T, none, store);
+      else stockham_stage<16, 2, false, true>(buf, tw, L, Ns, tid, T, none, store);
     }
     __syncthreads();
 #pragma unroll
-    for (int r = 0; r < 8; ++r) cur[r] = nxt[r];
+    for (int r = 0; r < VPT; ++r) cur[r] = nxt[r];
   }
 }
 
@@ -279,7 +335,7 @@ static void fft_launch_l(const S* in, S* out, const XScale& sc, int rows, const 
   constexpr int T = L / VPT;
   const int threads = std::max(T, std::min(256, std::max(32, L)));
   const int rpc = threads / T;
-  const size_t smem = (size_t)(rpc * padded_len(L)) * sizeof(double2);
+  const size_t smem = (size_t)(rpc * (VPT == 16 ? padded_len16(L) : padded_len(L))) * sizeof(double2);
   HELM_CHECK(smem <= 200 * 1024 && threads <= 256, "coarse FFT row too long");
   static bool attr = false;
   if (!attr) {
@@ -298,8 +354,12 @@ static void fft_launch(const S* in, S* out, const XScale& sc, int rows, int m0, 
   HELM_CHECK(m0 == (dct ? L / 2 + 1 : L / 2 - 1), "coarse FFT: m0 does not match the row length");
   auto go = [&](auto lc) {
     constexpr int LL = decltype(lc)::value;
-    if (dct) fft_launch_l<S, VPT, LL, true>(in, out, sc, rows, tw, st);
-    else fft_launch_l<S, VPT, LL, false>(in, out, sc, rows, tw, st);
+    if constexpr (VPT == 16 && LL < 256) {
+      HELM_CHECK(false, "the radix-16 coarse FFT needs rows of at least 256");
+    } else {
+      if (dct) fft_launch_l<S, VPT, LL, true>(in, out, sc, rows, tw, st);
+      else fft_launch_l<S, VPT, LL, false>(in, out, sc, rows, tw, st);
+    }
   };
   switch (L) {
     case 8: go(std::integral_constant<int, 8>{}); break;
@@ -367,7 +427,14 @@ void launch_xform(const helm_plan* P, const S* in, S* out, const double* sig, bo
   if (scale2d) sc = XScale{accumulate ? 1 : 0, nullptr, d.coarse_lamT, d.coarse_lamM, P->geo.k2, d.coarse_qn};
   if (d.fft_len) {
     const int L = d.fft_len;
-    fft_launch<S, 8>(in, out, sc, rows, m0, L, dct, d.twiddle, st);
+    static const bool r16 = [] {  // HELM_FFT16=0: radix-8 everywhere (A/B)
+      const char* e = getenv("HELM_FFT16");
+      return !(e && e[0] == '0');
+    }();
+    if (r16 && L >= 256)
+      fft_launch<S, 16>(in, out, sc, rows, m0, L, dct, d.twiddle, st);
+    else
+      fft_launch<S, 8>(in, out, sc, rows, m0, L, dct, d.twiddle, st);
   } else {
     dim3 grd((m0 + 255) / 256, rows);
     launch_pdl(xform_direct_kernel<S>, grd, 256, 0, st, in, out, sc, rows, m0, dct);
