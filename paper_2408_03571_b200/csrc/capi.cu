@@ -5,6 +5,7 @@
 #include <atomic>
 #include <chrono>
 #include <cmath>
+#include <complex>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -709,12 +710,137 @@ static void build_plan(const helm_desc* d, helm_plan* P) {
     }
     cfold[c] = ok && ne == hp && no == h;
   }
-  std::vector<int> ff, rr, mix;
+  // Dirichlet middle-pencil classes (tridiag(-1, 2, -1)/h^2, W = I) of length L = 4Q - 1,
+  // Q in {5, 9}: every eigenvector is +-sqrt(2/N) sin(pi (j+1) m / N), N = L + 1, with
+  // lambda_m = (2 - 2 cos(pi m / N)) / h^2 -- checked column by column against the plan's
+  // pairs; such boxes take the fast-sine kernel (local_dst.cu).  HELM_DST=0 keeps them on
+  // the DMMA kernel (A/B).
+  const char* dst_env = getenv("HELM_DST");
+  const bool dst_on = !(dst_env && dst_env[0] == '0');
+  std::vector<int> cdst(d->n_classes, 0);
+  int dst_q = 0;
+  const long double pi_l = 3.14159265358979323846264338327950288L;
+  for (int c = 0; c < d->n_classes && dst_on; ++c) {
+    const int L = P->h_class_len[c];
+    const int Q = (L + 1) / 4;
+    if (!cfold[c] || (L + 1) % 4 != 0 || (Q != 5 && Q != 9) || (dst_q && Q != dst_q)) continue;
+    const double* V = vr.data() + offV[c];
+    const double* lam = (const double*)d->class_lambda;
+    const long double nrm = sqrtl(2.0L / (L + 1));
+    std::vector<int> used(L + 1, 0);
+    bool ok = true;
+    for (int k = 0; k < L && ok; ++k) {
+      // the sine mode of column k: the largest projection
+      int best = 0;
+      long double bp = 0;
+      for (int m = 1; m <= L; ++m) {
+        long double pr = 0;
+        for (int j = 0; j < L; ++j) pr += (long double)V[j * L + k] * nrm * sinl(pi_l * (j + 1) * m / (L + 1));
+        if (fabsl(pr) > fabsl(bp)) bp = pr, best = m;
+      }
+      const long double sg = bp >= 0 ? 1.0L : -1.0L;
+      for (int j = 0; j < L && ok; ++j)
+        if (fabsl(V[j * L + k] - sg * nrm * sinl(pi_l * (j + 1) * best / (L + 1))) > 1e-12L) ok = false;
+      const long double lx = (2.0L - 2.0L * cosl(pi_l * best / (L + 1))) * P->geo.inv_h2;
+      const long double lp = d->is_complex ? lam[2 * (offL[c] + k)] : lam[offL[c] + k];
+      if (fabsl(lp - lx) > 1e-12L * fabsl(4.0L * P->geo.inv_h2) || used[best]) ok = false;
+      used[best] = 1;
+    }
+    if (ok) {
+      cdst[c] = 1;
+      dst_q = Q;
+    }
+  }
+  // MP-2 Sommerfeld-end classes (one boundary node at either end of the box): the pencil is
+  // T = tridiag(-1, 2, -1)/h^2 with tb = 1/h^2 - ik/h at the boundary node, W = I with 1/2
+  // there (discretization.py:136-148), checked against the plan's eigen-pairs; for every sine
+  // mode mu of the middle class, the Thomas factors of K_mu = T + (lam_mu - k^2) W (edge boxes,
+  // local_dst.cu).  A pivot below 1e-6/h^2 in modulus keeps the class on the dense kernel.
+  std::vector<int> ctri(d->n_classes, -1);
+  std::vector<double2> tri;
+  const bool edge_on = dst_q && d->is_complex && !env_flag_off("HELM_EDGE");
+  for (int c = 0; c < d->n_classes && edge_on; ++c) {
+    const int L = P->h_class_len[c];
+    if (creal[c] || L > 40) continue;
+    int s = -1;
+    for (int a = 0; a < p; ++a)
+      if (P->h_box_class[a] == c) s = P->h_box_start[a];
+    const bool lo = s == 0, hi = s + L == nu;
+    if (lo == hi) continue;  // both ends or neither: not an edge class
+    const int ib = lo ? 0 : L - 1;
+    typedef std::complex<long double> cl;
+    const long double ih2 = P->geo.inv_h2;
+    const cl tb((long double)P->geo.tb.x, (long double)P->geo.tb.y);
+    auto Tdiag = [&](int i) { return i == ib ? tb : cl(2.0L * ih2); };
+    auto Wd = [&](int i) { return i == ib ? 0.5L : 1.0L; };
+    // the plan's pairs must be this pencil's: |T v - lam W v| small for every column
+    const double2* V = (const double2*)d->class_V + offV[c];
+    const double2* lam = (const double2*)d->class_lambda + offL[c];
+    long double res = 0, vmax = 0;
+    for (int k = 0; k < L; ++k) {
+      const cl lk(lam[k].x, lam[k].y);
+      for (int i = 0; i < L; ++i) {
+        auto v = [&](int j) { return cl(V[j * L + k].x, V[j * L + k].y); };
+        cl tv = Tdiag(i) * v(i);
+        if (i > 0) tv -= ih2 * v(i - 1);
+        if (i + 1 < L) tv -= ih2 * v(i + 1);
+        res = std::max(res, std::abs(tv - lk * Wd(i) * v(i)));
+        vmax = std::max(vmax, std::abs(v(i)));
+      }
+    }
+    if (!(res <= 1e-9L * 4.0L * ih2 * vmax)) continue;
+    const int N4 = 4 * dst_q;
+    std::vector<double2> t((size_t)2 * 40 * N4, mk(0.0, 0.0));
+    bool ok = true;
+    for (int mu = 1; mu < N4 && ok; ++mu) {
+      const long double sh = (2.0L - 2.0L * cosl(pi_l * mu / N4)) * ih2 - (long double)d->k * d->k;
+      cl piv = Tdiag(0) + sh * Wd(0);
+      for (int i = 0; i < L; ++i) {
+        if (i > 0) {
+          const cl l = -ih2 / piv;  // e / d_{i-1}
+          piv = Tdiag(i) + sh * Wd(i) - l * (-ih2);
+          t[(size_t)i * N4 + mu - 1] = mk((double)l.real(), (double)l.imag());
+        }
+        if (std::abs(piv) < 1e-6L * ih2) ok = false;
+        const cl inv = 1.0L / piv;
+        t[((size_t)40 + i) * N4 + mu - 1] = mk((double)inv.real(), (double)inv.imag());
+      }
+    }
+    if (!ok) continue;
+    ctri[c] = (int)(tri.size() / t.size());
+    tri.insert(tri.end(), t.begin(), t.end());
+  }
+  std::vector<int> ff, rr, mix, dst, edge;
   for (int ay = 0; ay < p; ++ay)
     for (int ax = 0; ax < p; ++ax) {
       const int cy = P->h_box_class[ay], cx = P->h_box_class[ax];
-      (cfold[cy] && cfold[cx] ? ff : creal[cy] && creal[cx] ? rr : mix).push_back(ay * p + ax);
+      const bool ed = (cdst[cy] && ctri[cx] >= 0) || (ctri[cy] >= 0 && cdst[cx]);
+      (cdst[cy] && cdst[cx] ? dst : ed ? edge : cfold[cy] && cfold[cx] ? ff : creal[cy] && creal[cx] ? rr : mix)
+          .push_back(ay * p + ax);
     }
+  dv.n_edge = (int)edge.size();
+  dv.box_edge = edge.empty() ? nullptr : upload<int>(edge.data(), edge.size());
+  dv.class_tri = upload<int>(ctri.data(), ctri.size());
+  dv.edge_tri = tri.empty() ? nullptr : upload<double2>(tri.data(), tri.size());
+  dv.n_dst = (int)dst.size();
+  dv.dst_q = dst.empty() ? 0 : dst_q;
+  dv.box_dst = dst.empty() ? nullptr : upload<int>(dst.data(), dst.size());
+  dv.dst_inv = nullptr;
+  if (!dst.empty()) {
+    // (2/N)^2 / (lambda_my + lambda_mx - k^2) in sine-mode order [my][mx], exact eigenvalues
+    const int N4 = 4 * dst_q, L = N4 - 1;
+    std::vector<double> t((size_t)N4 * N4, 0.0);
+    for (int my = 1; my <= L; ++my)
+      for (int mx = 1; mx <= L; ++mx) {
+        const long double ly = (2.0L - 2.0L * cosl(pi_l * my / N4)) * P->geo.inv_h2;
+        const long double lx = (2.0L - 2.0L * cosl(pi_l * mx / N4)) * P->geo.inv_h2;
+        const long double den = ly + lx - (long double)d->k * d->k;
+        HELM_CHECK(fabsl(den) > 1e-14L * (8.0L * P->geo.inv_h2),
+                   "singular subdomain matrix (lambda_y + lambda_x = k^2)");
+        t[(size_t)(my - 1) * N4 + (mx - 1)] = (double)((2.0L / N4) * (2.0L / N4) / den);
+      }
+    dv.dst_inv = upload<double>(t.data(), t.size());
+  }
   dv.n_ff = (int)ff.size();
   dv.n_rr = (int)rr.size();
   dv.n_mix = (int)mix.size();
@@ -759,7 +885,7 @@ static void finish_desc(helm_plan* P) {
 static void free_plan(helm_plan* P) {
   PlanDev& dv = P->dev;
   void* ptrs[] = {dv.box_start, dv.box_len, dv.box_class, dv.class_len, dv.class_off_V, dv.class_off_lam,
-                  dv.class_V, dv.class_lambda, dv.class_real, dv.class_Vr, dv.box_ff, dv.class_Vf, dv.class_lamf, dv.class_invden, dv.box_rr, dv.box_mix,
+                  dv.class_V, dv.class_lambda, dv.class_real, dv.class_Vr, dv.box_ff, dv.class_Vf, dv.class_lamf, dv.class_invden, dv.box_dst, dv.dst_inv, dv.box_edge, dv.class_tri, dv.edge_tri, dv.box_rr, dv.box_mix,
                   dv.node_first_box, dv.node_mult, dv.node_band, dv.band_node,
                   dv.coarse_scale, dv.twiddle, dv.coarse_lamT, dv.coarse_lamM, dv.t0_band, dv.m0_band, dv.band_piv, dv.band_fac, dv.band_seg, dv.strip_q,
                   dv.cap_left, dv.cap_right, dv.cap_mode, dv.cap_vt, dv.cap_hg,

@@ -229,6 +229,14 @@ struct PlanDev {
   double* class_Vf;    // [n_classes][40][40] folded eigenvectors (even modes | odd modes)
   double* class_lamf;  // [n_classes][40] eigenvalues in the folded mode order (padding 1e30)
   double* class_invden; // [n_classes][n_classes][40][40] 1 / (lamf_y + lamf_x - k^2), padding 0
+  int* box_dst;        // subdomain ids whose two classes are the Dirichlet middle pencil, L = 4 dst_q - 1 (local_dst.cu)
+  int n_dst;
+  int dst_q;
+  double* dst_inv;     // [4 dst_q][4 dst_q] (2/N)^2 / (lam_y[m] + lam_x[n] - k^2), sine-mode order
+  int* box_edge;       // MP-2 subdomain ids with one middle-pencil axis and one Sommerfeld-end axis
+  int n_edge;
+  int* class_tri;      // [n_classes] index into edge_tri of a Sommerfeld-end class, or -1
+  double2* edge_tri;   // [n_tri][2][40][4 dst_q]: Thomas factors l_i, 1/d_i of T_e + (lam_mu - k^2) W_e
   int* box_rr;         // other subdomains whose two classes are real
   int n_rr;
   int* box_mix;        // the other subdomains

@@ -122,4 +122,16 @@ template <typename S>
 void launch_local_dmma(const helm_plan* P, const S* x, const S* base, S* y, S* ovl, const LocalArgs& a, int batch,
                        cudaStream_t st);
 
+// Boxes whose two classes are the Dirichlet middle pencil (exact DST-I eigenvectors) with
+// L = 4Q - 1, Q in {5, 9}: fast sine transforms on the FP64 pipe (local_dst.cu).
+template <typename S>
+void launch_local_dst(const helm_plan* P, const S* x, const S* base, S* y, S* ovl, const LocalArgs& a, int batch,
+                      cudaStream_t st);
+
+// MP-2 edge boxes (one middle axis, one Sommerfeld-end axis): sine transform + tridiagonal
+// solves per sine mode (local_dst.cu).
+template <typename S>
+void launch_local_edge(const helm_plan* P, const S* x, const S* base, S* y, S* ovl, const LocalArgs& a, int batch,
+                       cudaStream_t st);
+
 }  // namespace helm

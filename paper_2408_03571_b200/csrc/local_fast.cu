@@ -219,15 +219,17 @@ bool launch_local_fast(const helm_plan* P, const S* x, const S* base, S* y, S* o
   // The box groups write disjoint nodes / overlap slots, so with a workspace the DFMA boxes
   // run on its side stream beside the tensor-core boxes (at batch 1 they are < 1 wave and
   // would otherwise leave most SMs idle for their whole duration).
-  const bool fork = ws && ws->side && (d.n_rr + d.n_mix) > 0;
+  const bool fork = ws && ws->side && (d.n_rr + d.n_mix + d.n_edge) > 0;
   cudaStream_t sf = fork ? ws->side : st;
   if (fork) {
     HELM_CUDA(cudaEventRecord(ws->fork, st));
     HELM_CUDA(cudaStreamWaitEvent(ws->side, ws->fork, 0));
   }
   fast_launch<S, false>(P, x, base, y, ovl, a, d.box_mix, d.n_mix, batch, sf);
+  launch_local_edge<S>(P, x, base, y, ovl, a, batch, sf);  // edge boxes: sine transform + tridiagonal
   fast_launch<S, true>(P, x, base, y, ovl, a, d.box_rr, d.n_rr, batch, sf);
-  launch_local_dmma<S>(P, x, base, y, ovl, a, batch, st);  // folded real classes: FP64 tensor pipe
+  launch_local_dst<S>(P, x, base, y, ovl, a, batch, st);   // middle-pencil boxes: fast sine transforms
+  launch_local_dmma<S>(P, x, base, y, ovl, a, batch, st);  // other folded real classes: FP64 tensor pipe
   if (fork) {
     HELM_CUDA(cudaEventRecord(ws->join, ws->side));
     HELM_CUDA(cudaStreamWaitEvent(st, ws->join, 0));

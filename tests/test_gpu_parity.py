@@ -376,3 +376,42 @@ def test_reference_gmres_drives_device_preconditioner(name):
     assert abs(rep.iterations - dev.iterations) <= 1
     tol = UNREPRODUCIBLE.get(name, X_TOL)
     assert rel(rep.x, g["gmres_x"]) <= tol
+
+
+@pytest.mark.parametrize("problem,n,k,p,wbs", [("MP2", 65, 10.0, 4, False), ("MP2", 257, 50.0, 8, False),
+                                                ("MP2", 257, 50.0, 8, True), ("MP1", 65, 20.0, 4, False),
+                                                ("MP1", 129, 30.0, 4, True)])
+def test_fast_sine_and_edge_boxes_match_dense_path(monkeypatch, problem, n, k, p, wbs):
+    """The middle-pencil boxes (fast sine transforms, local_dst.cu) and the MP-2 edge boxes (sine
+    transform + one tridiagonal solve per sine mode) against the DMMA / dense box kernels
+    (HELM_DST=0, HELM_EDGE=0) and the CPU oracle: the one-level sum and every preconditioner kind
+    to 1e-12, at batch 1, 3 (an odd tail of the 2-slot CTAs) and 6."""
+    import os
+    import sys
+
+    sys.path.insert(0, os.path.join(os.path.dirname(__file__), "..", "oracle"))
+    import helmdd_oracle as O
+    import paper_2408_03571_b200 as hb
+
+    grid = hb.Grid(n, "dirichlet" if problem == "MP1" else "sommerfeld")
+    prob = hb.assemble(grid, k, problem)
+    dec = hb.extend(hb.partition(grid, p), 2)
+    cs = hb.galerkin(hb.build_hocs(grid, 2), prob.A)
+    oprob, odec, ocs, _ = O.build_shs2(n, k, problem, p, 2)
+    rng = np.random.default_rng(5)
+    shape = (6, prob.A.N)
+    Xn = rng.standard_normal(shape) + (1j * rng.standard_normal(shape) if problem == "MP2" else 0.0)
+    X = torch.from_numpy(Xn).cuda()
+    for kind in ("SHS2", "AS2", "SAS2"):
+        Mf = hb.SchwarzPreconditioner(kind, prob.A, dec, cs, max_batch=6, weights_before_solve=wbs)
+        monkeypatch.setenv("HELM_DST", "0")
+        monkeypatch.setenv("HELM_EDGE", "0")
+        Md = hb.SchwarzPreconditioner(kind, prob.A, dec, cs, max_batch=6, weights_before_solve=wbs)
+        monkeypatch.delenv("HELM_DST")
+        monkeypatch.delenv("HELM_EDGE")
+        for Xb in (X[:1], X[:3], X):
+            yf, yd = Mf(Xb), Md(Xb)
+            assert (torch.linalg.norm(yf - yd) / torch.linalg.norm(yd)).item() <= 1e-12, (kind, Xb.shape[0])
+        oM = O.OSchwarz(kind, oprob.A, odec, ocs, weights_before_solve=wbs)
+        ref = oM(Xn[1])
+        assert rel(Mf(X[1:2])[0].cpu().numpy(), ref) <= 1e-12, kind
