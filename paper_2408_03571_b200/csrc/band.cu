@@ -43,7 +43,12 @@ constexpr size_t band_smem_bytes() {
 
 // NOPIV: no pivot was taken in the factorisation (PlanDev::band_nopiv): pivots are not
 // read and U rows are {1/U_jj, U_j,j+1, U_j,j+2} (UE = 3 instead of 5).
-template <int RB, int NW, int R, int ST, bool NOPIV>
+// VALS: only the strip values of the solution are wanted (the Woodbury / strip-refinement
+// passes): the backward sweep keeps its rows in the stage buffer instead of storing them,
+// and each chunk of R = 8 rows is reduced over the CTA's 32 modes with the strip weights
+// (lane = (row, quarter of the modes), rotated columns: conflict-free 16-byte reads) into
+// part[mode group][row][b*4+i]; `out` is then only the scratch of the eliminated rows.
+template <int RB, int NW, int R, int ST, bool NOPIV, bool VALS>
 __global__ void __launch_bounds__(BW* NW) band_solve_kernel(const double2* __restrict__ in, double2* __restrict__ out,
                                                             const int* __restrict__ piv,
                                                             const double2* __restrict__ L,
@@ -51,7 +56,8 @@ __global__ void __launch_bounds__(BW* NW) band_solve_kernel(const double2* __res
                                                             const double2* __restrict__ corr,
                                                             const double* __restrict__ q,
                                                             const double* __restrict__ sig, int ldc,
-                                                            const double2* __restrict__ add) {
+                                                            const double2* __restrict__ add,
+                                                            double2* __restrict__ part) {
   pdl_wait();  // PDL: the predecessor's writes are visible (no-op without PDL)
   extern __shared__ __align__(16) unsigned char sraw[];
   const int t = threadIdx.x & (BW - 1), w = threadIdx.x / BW;
@@ -197,6 +203,19 @@ __global__ void __launch_bounds__(BW* NW) band_solve_kernel(const double2* __res
   double2 y1[RB], y2[RB], y3[RB], y4[RB];
 #pragma unroll
   for (int r = 0; r < RB; ++r) y1[r] = y2[r] = y3[r] = y4[r] = mk(0.0, 0.0);
+  // VALS: this lane reduces row (t >> 2) of a chunk over the 8 modes p*8 + vcol(i), p = t & 3
+  const int vrow = t >> 2, vp = t & 3;
+  auto vcol = [&](int i) { return vp * 8 + ((i + vp + 4 * (vrow & 1)) & 7); };
+  double qc[VALS ? 8 : 1][4];
+  if constexpr (VALS) {
+    static_assert(R == 8 && BW == 32, "the strip-value reduction maps a lane to (row of 8, quarter of 32 modes)");
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int ac = a0 + vcol(i);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) qc[i][k] = ac < m0 ? q[(size_t)ac * 4 + k] : 0.0;
+    }
+  }
   double2 acur[RB][R], anxt[RB][R];
   auto load_add = [&](int c, double2 (&dst)[RB][R]) {
 #pragma unroll
@@ -215,7 +234,7 @@ __global__ void __launch_bounds__(BW* NW) band_solve_kernel(const double2* __res
     if (c + ST - 1 < nch) issue_bwd(c + ST - 1);
     else cp_commit();
     if (add && c + 1 < nch) load_add(c + 1, anxt);
-    const BS& S = bs[c % ST];
+    BS& S = bs[c % ST];
     const int rows = min(R, m0 - c * R);
 #pragma unroll
     for (int rr = 0; rr < R; ++rr) {
@@ -232,7 +251,9 @@ __global__ void __launch_bounds__(BW* NW) band_solve_kernel(const double2* __res
           v = fms_(S.U[rr][t][UE - 1], y4[r], v);
         }
         v = mul(v, u0);
-        if (va && b0 + r < batch)
+        if constexpr (VALS)
+          S.v[w][r][rr][t] = v;  // the slot just read; the stage is re-issued after the next barrier
+        else if (va && b0 + r < batch)
           out[(size_t)(b0 + r) * N0 + (size_t)j * m0 + a] = add ? ::helm::add(v, acur[r][rr]) : v;
         y4[r] = y3[r];
         y3[r] = y2[r];
@@ -246,25 +267,65 @@ __global__ void __launch_bounds__(BW* NW) band_solve_kernel(const double2* __res
 #pragma unroll
         for (int r = 0; r < RB; ++r) acur[r][rr] = anxt[r][rr];
     }
+    if constexpr (VALS) {
+      __syncwarp();
+#pragma unroll
+      for (int r = 0; r < RB; ++r) {
+        double2 acc[4] = {mk(0.0, 0.0), mk(0.0, 0.0), mk(0.0, 0.0), mk(0.0, 0.0)};
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const double2 x = S.v[w][r][vrow][vcol(i)];
+#pragma unroll
+          for (int k = 0; k < 4; ++k) acc[k] = fma_(qc[i][k], x, acc[k]);
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {  // quarters in the fixed order (p ^ 1) then (p ^ 2)
+          acc[k].x += __shfl_xor_sync(0xffffffffu, acc[k].x, 1);
+          acc[k].y += __shfl_xor_sync(0xffffffffu, acc[k].y, 1);
+          acc[k].x += __shfl_xor_sync(0xffffffffu, acc[k].x, 2);
+          acc[k].y += __shfl_xor_sync(0xffffffffu, acc[k].y, 2);
+        }
+        if (vp == 0 && vrow < rows && b0 + r < batch) {
+          const int j = m0 - 1 - (c * R + vrow);
+          double2* o = part + ((size_t)blockIdx.x * m0 + j) * ldc + (size_t)(b0 + r) * 4;
+#pragma unroll
+          for (int k = 0; k < 4; ++k) o[k] = acc[k];
+        }
+      }
+      __syncwarp();
+    }
   }
   cp_wait<0>();
 }
 
-template <int RB, int NW, int R, int ST, bool NOPIV>
+// Z[e] = (Zadd ? Zadd[e] : 0) + sum_g part[g][e]   (mode groups in order: deterministic)
+__global__ void __launch_bounds__(256) strip_part_sum_kernel(const double2* __restrict__ part,
+                                                             const double2* __restrict__ Zadd,
+                                                             double2* __restrict__ Z, size_t n, int groups) {
+  pdl_wait();  // PDL: the predecessor's writes are visible (no-op without PDL)
+  const size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= n) return;
+  double2 s = Zadd ? Zadd[e] : mk(0.0, 0.0);
+  for (int g = 0; g < groups; ++g) s = ::helm::add(s, part[(size_t)g * n + e]);
+  Z[e] = s;
+}
+
+template <int RB, int NW, int R, int ST, bool NOPIV, bool VALS = false>
 static void band_launch_k(const helm_plan* P, const double2* in, double2* out, const double2* corr, int batch,
-                          cudaStream_t st, const double2* add) {
+                          cudaStream_t st, const double2* add, double2* part = nullptr) {
   const PlanDev& d = P->dev;
   constexpr size_t smem = band_smem_bytes<RB, NW, R, ST>();
   static_assert(smem <= 227 * 1024, "band-solve stages exceed shared memory");
   static bool attr = false;
   if (!attr) {
-    HELM_CUDA(cudaFuncSetAttribute(band_solve_kernel<RB, NW, R, ST, NOPIV>,
+    HELM_CUDA(cudaFuncSetAttribute(band_solve_kernel<RB, NW, R, ST, NOPIV, VALS>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr = true;
   }
   dim3 grd((d.m0 + BW - 1) / BW, (batch + RB * NW - 1) / (RB * NW));
-  launch_pdl(band_solve_kernel<RB, NW, R, ST, NOPIV>, grd, BW * NW, smem, st, in, out, d.band_piv, (const double2*)d.band_l, (const double2*)d.band_u, d.m0, batch, corr, d.strip_q,
-      d.coarse_scale, batch * 4, add);
+  launch_pdl(band_solve_kernel<RB, NW, R, ST, NOPIV, VALS>, grd, BW * NW, smem, st, in, out, d.band_piv,
+             (const double2*)d.band_l, (const double2*)d.band_u, d.m0, batch, corr, d.strip_q, d.coarse_scale,
+             batch * 4, add, part);
   HELM_LAUNCH_CHECK();
 }
 
@@ -284,6 +345,26 @@ static int band_seg_max_batch() {
     return e ? std::atoi(e) : 4;
   }();
   return v;
+}
+
+// Strip values only: Z = (Zadd) + S X for the same system (S = the strip weights strip_q);
+// `scratch` [batch][N0] holds the eliminated rows, `part` ceil(m0/32) * m0 * batch * 4 partial sums.
+bool band_vals_usable(const helm_plan* P, int batch) {
+  return !(batch <= band_seg_max_batch() && P->dev.band_seg) && batch > 4;
+}
+void launch_band_vals(const helm_plan* P, const double2* in, double2* scratch, const double2* corr, int batch,
+                      cudaStream_t st, double2* part, const double2* Zadd, double2* Z) {
+  HELM_CHECK(band_vals_usable(P, batch), "band solve: strip-value pass needs the streaming kernel (batch > 4)");
+  HELM_CHECK((const void*)in != (const void*)scratch, "band solve: input and scratch must not alias");
+  HELM_CHECK(in != nullptr || corr != nullptr, "band solve: no right-hand side");
+  if (P->dev.band_nopiv)
+    band_launch_k<1, 8, 8, 3, true, true>(P, in, scratch, corr, batch, st, nullptr, part);
+  else
+    band_launch_k<1, 8, 8, 3, false, true>(P, in, scratch, corr, batch, st, nullptr, part);
+  const size_t n = (size_t)P->dev.m0 * batch * 4;
+  launch_pdl(strip_part_sum_kernel, (unsigned)((n + 255) / 256), 256, 0, st, (const double2*)part, Zadd, Z, n,
+             (P->dev.m0 + BW - 1) / BW);
+  HELM_LAUNCH_CHECK();
 }
 
 void launch_band_solve(const helm_plan* P, const double2* in, double2* out, const double2* corr, int batch,

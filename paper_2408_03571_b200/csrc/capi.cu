@@ -961,6 +961,8 @@ int helm_workspace_create(const helm_plan* P, int32_t max_batch, helm_workspace*
     for (int s = 0; s < 7; ++s)
       if (P->dev.n_strip)
         HELM_CUDA(cudaMalloc(&w->strip[s], (size_t)(s == 3 ? 8 : 1) * P->dev.m0 * B * P->dev.n_strip * e));
+    if (P->dev.n_strip && max_batch > 4)
+      HELM_CUDA(cudaMalloc(&w->strip_part, (size_t)((P->dev.m0 + 31) / 32) * P->dev.m0 * B * P->dev.n_strip * e));
     w->red_bytes = krylov_scratch_bytes(4096);
     HELM_CUDA(cudaMalloc(&w->red, w->red_bytes));
     HELM_CUDA(cudaMemset(w->red, 0, w->red_bytes));  // the CGS2 completion counters start at zero
@@ -983,7 +985,7 @@ int helm_workspace_destroy(helm_workspace* w) {
     if (!w) return;
     basis_free(w);
     void* ptrs[] = {w->z, w->d, w->c, w->g, w->y0, w->r0, w->e0, w->f0, w->ovl, w->red, w->strip[0], w->strip[1],
-                    w->strip[2], w->strip[3], w->strip[4], w->strip[5], w->strip[6]};
+                    w->strip[2], w->strip[3], w->strip[4], w->strip[5], w->strip[6], w->strip_part};
     for (void* q : ptrs)
       if (q) cudaFree(q);
     if (w->pinned) cudaFreeHost(w->pinned);

@@ -701,6 +701,14 @@ __global__ void __launch_bounds__(256) a0_residual_kernel(const S* __restrict__ 
 // ----------------------------------------------------------------------------
 // composition
 // ----------------------------------------------------------------------------
+// HELM_STRIP_FIRST=0 keeps the round-1 pass order (full pass, Woodbury pass, refinement pass)
+static bool strip_first() {
+  static const bool v = [] {
+    const char* e = std::getenv("HELM_STRIP_FIRST");
+    return !(e && e[0] == '0');
+  }();
+  return v;
+}
 // One fast solve: out = A0^{-1} in  (in, out distinct from ws->g / ws->f0)
 template <typename S>
 static void fast_solve(const helm_plan* P, helm_workspace* ws, const S* in, S* out, int batch, cudaStream_t st,
@@ -718,20 +726,11 @@ static void fast_solve(const helm_plan* P, helm_workspace* ws, const S* in, S* o
     launch_xform<S>(P, T1, out, nullptr, false, batch, st, accumulate);
   } else {
     launch_xform<S>(P, in, T1, d.coarse_scale, false, batch, st);
-    launch_band_solve(P, T1, T2, nullptr, batch, st);
     S* Z = (S*)ws->strip[0];
     S* Ch = (S*)ws->strip[1];
     S* Cs = (S*)ws->strip[2];
-    strip_reduce<S>(T2, d.strip_q, Z, d.m0, batch, st);
     S* part = (S*)ws->strip[3];
     S* Zf = (S*)ws->strip[6];
-    strip_gemm_fold((const double2*)d.cap_left, Z, Ch, true, (const double2*)d.cap_mode, nullptr, d.m0, batch, Zf,
-                    part, st);
-    strip_gemm_fold((const double2*)d.cap_right, Ch, Cs, false, nullptr, nullptr, d.m0, batch, Zf, part, st);
-    launch_band_solve(P, T1, T2, Cs, batch, st);
-    // strip refinement: rho = cS - C_U y_S from this pass's strip values (exact), the
-    // correction W = H G rho - rho from the eigen-space operators (only ~1e-12 accurate,
-    // enough for a correction of a ~1e-12 quantity), then Y^ += B^{-1}(-ext(W)).
     S* T3 = (S*)ws->e0;
     S* R = (S*)ws->strip[4];
     S* W = (S*)ws->strip[5];
@@ -740,6 +739,42 @@ static void fast_solve(const helm_plan* P, helm_workspace* ws, const S* in, S* o
       cp.lm[i] = d.strip_lm[i];
       cp.lk[i] = sub(d.strip_lt[i], scale(d.strip_lm[i], P->geo.k2));
     }
+    const size_t ns = (size_t)d.m0 * batch * 4;
+    if (strip_first() && ws->strip_part && band_vals_usable(P, batch)) {
+      // Strip-first order (batch > 4): the strip correction is settled by passes that keep only
+      // the strip values (no solution rows written, no separate strip sweep), then ONE full
+      // pass forms Y^ = B^{-1}(F^ - ext(cS)).  By linearity this is the sequence below
+      // (Y^ = B^{-1}F^ - B^{-1}ext(cS), strip values Z + Z') with 2 + strip_refine passes.
+      S* Zp = (S*)ws->strip_part;
+      S* Zt = (S*)ws->strip[6];  // Zf is free between the strip GEMMs
+      launch_band_vals(P, T1, T2, nullptr, batch, st, Zp, nullptr, Z);  // Z = S B^{-1} F^
+      strip_gemm_fold((const double2*)d.cap_left, Z, Ch, true, (const double2*)d.cap_mode, nullptr, d.m0, batch, Zf,
+                      part, st);
+      strip_gemm_fold((const double2*)d.cap_right, Ch, Cs, false, nullptr, nullptr, d.m0, batch, Zf, part, st);
+      for (int it = 0; it < d.strip_refine; ++it) {
+        launch_band_vals(P, nullptr, T2, Cs, batch, st, Zp, Z, Zt);  // Zt = Z + S B^{-1}(-ext(cS))
+        launch_pdl(strip_rho_kernel, (d.m0 * batch + 255) / 256, 256, 0, st, Cs, Zt, R, (const double2*)d.t0_band,
+                   (const double2*)d.m0_band, cp, d.m0, batch);
+        HELM_LAUNCH_CHECK();
+        strip_gemm_fold((const double2*)d.cap_vt, R, Ch, true, (const double2*)d.cap_hg, nullptr, d.m0, batch, Zf,
+                        part, st);
+        strip_gemm_fold((const double2*)d.cap_right, Ch, W, false, nullptr, R, d.m0, batch, Zf, part, st);
+        launch_pdl(strip_axpy_kernel, (unsigned)((ns + 255) / 256), 256, 0, st, Cs, W, ns);
+        HELM_LAUNCH_CHECK();
+      }
+      launch_band_solve(P, T1, T2, Cs, batch, st);
+      launch_xform<S>(P, T2, out, nullptr, false, batch, st, accumulate);
+      return;
+    }
+    launch_band_solve(P, T1, T2, nullptr, batch, st);
+    strip_reduce<S>(T2, d.strip_q, Z, d.m0, batch, st);
+    strip_gemm_fold((const double2*)d.cap_left, Z, Ch, true, (const double2*)d.cap_mode, nullptr, d.m0, batch, Zf,
+                    part, st);
+    strip_gemm_fold((const double2*)d.cap_right, Ch, Cs, false, nullptr, nullptr, d.m0, batch, Zf, part, st);
+    launch_band_solve(P, T1, T2, Cs, batch, st);
+    // strip refinement: rho = cS - C_U y_S from this pass's strip values (exact), the
+    // correction W = H G rho - rho from the eigen-space operators (only ~1e-12 accurate,
+    // enough for a correction of a ~1e-12 quantity), then Y^ += B^{-1}(-ext(W)).
     for (int it = 0; it < d.strip_refine; ++it) {
       strip_reduce<S>(T2, d.strip_q, Z, d.m0, batch, st);
       launch_pdl(strip_rho_kernel, (d.m0 * batch + 255) / 256, 256, 0, st, Cs, Z, R, (const double2*)d.t0_band,
@@ -750,7 +785,6 @@ static void fast_solve(const helm_plan* P, helm_workspace* ws, const S* in, S* o
       strip_gemm_fold((const double2*)d.cap_right, Ch, W, false, nullptr, R, d.m0, batch, Zf, part, st);
       launch_band_solve(P, nullptr, T3, W, batch, st, T2);  // T3 = T2 + B^{-1}(-ext(W))
       if (it + 1 < d.strip_refine) {
-        const size_t ns = (size_t)d.m0 * batch * 4;
         launch_pdl(strip_axpy_kernel, (unsigned)((ns + 255) / 256), 256, 0, st, Cs, W, ns);
         HELM_LAUNCH_CHECK();
       }

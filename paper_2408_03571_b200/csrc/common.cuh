@@ -372,6 +372,7 @@ struct helm_workspace {
   void* f0;       // [B][N0]
   void* ovl;      // overlap scratch [B][6][nbands][nu]
   void* strip[7]; // coarse Woodbury scratch [m0][B * n_strip]: Z, C^, C_S, split-K partials (x8), rho, W, Zf
+  void* strip_part;  // strip-value partial sums of the band passes [ceil(m0/32)][m0][B * n_strip] (batch > 4)
   void* red;      // reduction scratch (doubles)
   size_t red_bytes;
   void* pinned;   // small pinned host buffer for scalar read-back

@@ -35,6 +35,10 @@ void band_seg_launch(const helm_plan* P, const double2* in, double2* out, const 
 void launch_band_solve(const helm_plan* P, const double2* in, double2* out, const double2* corr, int batch,
                        cudaStream_t st, const double2* add = nullptr);
 
+bool band_vals_usable(const helm_plan* P, int batch);
+void launch_band_vals(const helm_plan* P, const double2* in, double2* scratch, const double2* corr, int batch,
+                      cudaStream_t st, double2* part, const double2* Zadd, double2* Z);
+
 // composite operators (capi.cu)
 template <typename S> void op_apply_A(const helm_plan* P, const S* x, S* y, int batch, cudaStream_t st);
 template <typename S>

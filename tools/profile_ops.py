@@ -34,13 +34,14 @@ def main():
     ap.add_argument("--only", default="", help="comma-separated op names to time (default: all)")
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--batches", default="1,32")
+    ap.add_argument("--setup", default="native", help="native | host (host: no cuSOLVER kernels, quick under ncu)")
     a = ap.parse_args()
     t = time.time()
     grid = hb.Grid(a.n, "sommerfeld")
     prob = hb.assemble(grid, a.k, "MP2")
     dec = hb.extend(hb.partition(grid, a.p), 2)
     cs = hb.galerkin(hb.build_hocs(grid, 2), prob.A)
-    M = hb.SchwarzPreconditioner("SHS2", prob.A, dec, cs, max_batch=a.batch)
+    M = hb.SchwarzPreconditioner("SHS2", prob.A, dec, cs, max_batch=a.batch, setup=a.setup)
     print(f"setup {time.time() - t:.1f}s", flush=True)
     N, N0 = M.N, M.N0
     p, lib = M.plan, M.plan.lib
