@@ -357,7 +357,9 @@ void launch_band_vals(const helm_plan* P, const double2* in, double2* scratch, c
   HELM_CHECK(band_vals_usable(P, batch), "band solve: strip-value pass needs the streaming kernel (batch > 4)");
   HELM_CHECK((const void*)in != (const void*)scratch, "band solve: input and scratch must not alias");
   HELM_CHECK(in != nullptr || corr != nullptr, "band solve: no right-hand side");
-  if (P->dev.band_nopiv)
+  if (band_tma_usable(P))
+    band_tma_launch(P, in, scratch, corr, batch, st, nullptr, part);
+  else if (P->dev.band_nopiv)
     band_launch_k<1, 8, 8, 3, true, true>(P, in, scratch, corr, batch, st, nullptr, part);
   else
     band_launch_k<1, 8, 8, 3, false, true>(P, in, scratch, corr, batch, st, nullptr, part);
@@ -379,6 +381,8 @@ void launch_band_solve(const helm_plan* P, const double2* in, double2* out, cons
     band_launch<1, 1, 8, 4>(P, in, out, corr, batch, st, add);  // latency-bound recurrence
   else if (batch <= 4)
     band_launch<2, 2, 8, 3>(P, in, out, corr, batch, st, add);
+  else if (band_tma_usable(P))
+    band_tma_launch(P, in, out, corr, batch, st, add, nullptr);  // the same CTA shape, TMA-staged (band_tma.cu)
   else  // 8 warps (8 right-hand sides) share each factor read; 4-16 per CTA and 4-8 rows per
         // stage were measured slower
     band_launch<1, 8, 8, 3>(P, in, out, corr, batch, st, add);

@@ -35,6 +35,9 @@ void band_seg_launch(const helm_plan* P, const double2* in, double2* out, const 
 void launch_band_solve(const helm_plan* P, const double2* in, double2* out, const double2* corr, int batch,
                        cudaStream_t st, const double2* add = nullptr);
 
+bool band_tma_usable(const helm_plan* P);
+void band_tma_launch(const helm_plan* P, const double2* in, double2* out, const double2* corr, int batch,
+                     cudaStream_t st, const double2* add, double2* part);
 bool band_vals_usable(const helm_plan* P, int batch);
 void launch_band_vals(const helm_plan* P, const double2* in, double2* scratch, const double2* corr, int batch,
                       cudaStream_t st, double2* part, const double2* Zadd, double2* Z);

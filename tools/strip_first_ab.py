@@ -36,7 +36,7 @@ def child(tag):
     pl, lib = M.plan, M.plan.lib
     st = torch.cuda.current_stream().cuda_stream
     g = torch.Generator(device="cuda").manual_seed(11)
-    for B in (32, 8):
+    for B in (32, 13, 8):
         C = torch.randn(B, M.N0, dtype=torch.complex128, device="cuda", generator=g)
         Y = torch.empty_like(C)
         X = torch.randn(B, M.N, dtype=torch.complex128, device="cuda", generator=g)
@@ -58,5 +58,7 @@ if __name__ == "__main__":
     if len(sys.argv) > 1:
         child(sys.argv[1])
     else:
+        # default: pass order A/B; "tma": the TMA-staged band kernel against the cp.async one
+        var = "HELM_BAND_TMA" if os.environ.get("AB") == "tma" else "HELM_STRIP_FIRST"
         for tag, v in (("old", "0"), ("new", "1")):
-            subprocess.run([sys.executable, __file__, tag], env=dict(os.environ, HELM_STRIP_FIRST=v), check=False)
+            subprocess.run([sys.executable, __file__, tag], env=dict(os.environ, **{var: v}), check=False, timeout=400)
