@@ -167,7 +167,9 @@ __global__ void __launch_bounds__(TBW* TNW) band_tma_kernel(const double2* __res
     const BandTmaStage& S = stg[c % TST];
     facL = reinterpret_cast<const double2(*)[TBW][2]>(&S.fac[0][0][0]);
     const int rows = min(TR, m0 - c * TR);
-    for (int rr = 0; rr < rows; ++rr) {
+#pragma unroll
+    for (int rr = 0; rr < TR; ++rr) {
+      if (rr >= rows) break;
       const int j = c * TR + rr;
       const double2 l0 = facL[rr][t][0], l1 = facL[rr][t][1];
       const double2 x0 = r0v;

@@ -281,6 +281,82 @@ template <typename S> struct BoxOut {
       else ob[meta[3 * DML + r] + meta[6 * DML + q]] = acc;
     }
   }
+  // Column-mapped forms for the fast-sine kernel: thread = (row group rg of NG, column q), so the
+  // column terms (parity, taps, bounds, scatter offsets) are computed once per thread and the
+  // loops carry only row terms (uniform across a warp's columns).  Same values and fma order as
+  // init_rx / put (bitwise); the element-mapped forms cost ~90 / ~80 instructions per node in
+  // index arithmetic (42 % of the kernel's instructions, profiles/top_kernel_local_dst_kernel_r02_v4.txt).
+  template <int NG> __device__ void init_rx_cols(const S* __restrict__ base, int b0, int nslot, int rg, int j) const {
+    const int tx = x0 + j - a.off;
+    const bool ex = (tx & 1) == 0;
+    const int Vc = ex ? tx / 2 - 1 : (tx - 1) >> 1;
+    const double w0 = ex ? 0.125 : 0.5, w1 = ex ? 0.75 : 0.5, w2 = ex ? 0.125 : 0.0;
+    bool okv[3];
+#pragma unroll
+    for (int t = 0; t < 3; ++t) okv[t] = Vc + t >= 0 && Vc + t < a.m0;
+    const size_t bs = base_stride(a);
+    // NIT rows per thread in batches of HB: a batch's 3 HB loads are all in flight before the
+    // first is used (the prologue has registers to spare; one row at a time left the
+    // L2 latency of every row exposed: 21 % of the kernel's stall samples)
+    constexpr int HB = 6;
+    const int total = nslot * WIN;
+    for (int i0 = 0; rg + i0 * NG < total; i0 += HB) {
+      S c[HB][3];
+      int su[HB];
+#pragma unroll
+      for (int i = 0; i < HB; ++i) {
+        const int idx = rg + (i0 + i) * NG;
+        const int sl = idx / WIN, u = idx - sl * WIN;
+        su[i] = idx < total ? sl * rxs + u * Lx : -1;
+        const int U = Uby + u;
+        const bool okU = idx < total && U >= 0 && U < a.m0;
+        const S* bb = base + (size_t)(b0 + (okU ? sl : 0)) * bs + (size_t)(okU ? U : 0) * a.m0 + Vc;
+#pragma unroll
+        for (int t = 0; t < 3; ++t) c[i][t] = (okU && okv[t]) ? __ldg(bb + t) : Sc<S>::zero();
+      }
+#pragma unroll
+      for (int i = 0; i < HB; ++i) {
+        S row = Sc<S>::zero();
+        row = fma_(w0, c[i][0], row);
+        row = fma_(w1, c[i][1], row);
+        row = fma_(w2, c[i][2], row);
+        if (su[i] >= 0) rx[su[i] + j] = row;
+      }
+    }
+  }
+  struct ColTerms {
+    int mx, c5, c6;
+  };
+  __device__ __forceinline__ ColTerms col_terms(int q) const {
+    return ColTerms{meta[DML + q], meta[5 * DML + q], meta[6 * DML + q]};
+  }
+  __device__ __forceinline__ void put_col(const S* __restrict__ base, S* __restrict__ y, S* __restrict__ ovl,
+                                          bool cbase, int sl, int b, int r, int q, const ColTerms& ct, S acc) const {
+    const int nu = a.nu;
+    const size_t N = (size_t)nu * nu;
+    // branch-free: a warp's columns mix interior and overlap nodes in every row, so the two
+    // store paths of put() both ran for nearly every warp (divergence doubled the epilogue);
+    // here every lane forms both addresses and one predicated value and stores once
+    const int my = meta[r], mm = my * ct.mx;
+    const bool interior = mm == 1;
+    if (a.weighted && !a.wbs) acc = scale(acc, interior ? 1.0 : (mm == 2 ? 0.5 : 0.25));  // x * 1.0 == x
+    const int pidx = meta[4 * DML + r] + x0 + q;
+    S bv = Sc<S>::zero();
+    if (cbase) {
+      const int code = meta[7 * DML + r];
+      const bool ey = code & 1;
+      const S* tp = rx + (size_t)sl * rxs + (code >> 1) + q;
+      bv = fma_(ey ? 0.125 : 0.5, tp[0], bv);
+      bv = fma_(ey ? 0.75 : 0.5, tp[Lx], bv);
+      bv = fma_(ey ? 0.125 : 0.0, tp[2 * Lx], bv);
+    } else if (base && interior) {
+      bv = base[(size_t)b * N + pidx];
+    }
+    const S val = (base && interior) ? add(bv, acc) : acc;
+    const int oo = my == 2 ? meta[2 * DML + r] + ct.c5 : meta[3 * DML + r] + ct.c6;
+    S* dst = interior ? y + (size_t)b * N + pidx : ovl + (size_t)b * 6 * a.nbands * nu + oo;
+    *dst = val;
+  }
   // weights-before-solve factor of node (r, q)
   __device__ __forceinline__ double wbs_factor(int r, int q) const {
     return 1.0 / (a.node_mult[y0 + r] * a.node_mult[x0 + q]);
@@ -330,7 +406,10 @@ __global__ void __launch_bounds__(DstGeo<Sc<S>::cplx ? 2 : 1, Q>::NTH, 3)
     cp_commit();
   }
   io.init_meta(NTH);
-  if (cbase) io.init_rx(base, b0, nslot, NTH);  // behind the box load
+  // prologue / epilogue thread map: NG row groups x L columns (NG * L <= NTH)
+  constexpr int NG = NTH / L;
+  const int cq = threadIdx.x % L, crg = threadIdx.x / L;
+  if (cbase && crg < NG) io.template init_rx_cols<NG>(base, b0, nslot, crg, cq);  // behind the box load
   if (tma.on) {
     __syncthreads();  // the barrier is initialised before any thread waits on it
     mbar_wait_(&box_bar, 0);
@@ -381,14 +460,21 @@ __global__ void __launch_bounds__(DstGeo<Sc<S>::cplx ? 2 : 1, Q>::NTH, 3)
     for (int j = 0; j < L; ++j) Xs[l * RS + NP * j + part] = v[j];
   }
   __syncthreads();
-  // ---- epilogue
-  for (int e = threadIdx.x; e < nslot * L * L; e += NTH) {
-    const int sl = e / (L * L), r = (e / L) % L, q = e % L;
-    const double* Xe = X(sl);
-    S acc;
-    if constexpr (NP == 2) acc = *reinterpret_cast<const double2*>(&Xe[r * RS + 2 * q]);
-    else acc = Xe[r * RS + q];
-    io.put(base, y, ovl, cbase, sl, b0 + sl, r, q, acc);
+  // ---- epilogue (thread = (row group, column): column terms in registers)
+  if (crg < NG) {
+    const typename BoxOut<S>::ColTerms ct = io.col_terms(cq);
+    int sl = 0, r = crg;
+    for (int idx = crg; idx < nslot * L; idx += NG, r += NG) {
+      if (r >= L) {
+        r -= L;
+        ++sl;
+      }
+      const double* Xe = X(sl);
+      S acc;
+      if constexpr (NP == 2) acc = *reinterpret_cast<const double2*>(&Xe[r * RS + 2 * cq]);
+      else acc = Xe[r * RS + cq];
+      io.put_col(base, y, ovl, cbase, sl, b0 + sl, r, cq, ct, acc);
+    }
   }
 }
 
