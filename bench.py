@@ -99,31 +99,47 @@ class ClockSampler:
 # --------------------------------------------------------------------------------------------
 # algorithmic work per vector
 # --------------------------------------------------------------------------------------------
-def work_model(N, N0, m0, s, boxes_1d, real_class_1d, n, refine=1):
+def dst_flops(L):
+    """Real flops of one fast sine transform of a length-L real vector as local_dst.cu runs it
+    (L = 4Q - 1, Q odd: three even/odd folds and dense blocks of Q and (Q-1)/2), or None."""
+    if (L + 1) % 4 or ((L + 1) // 4) % 2 == 0:
+        return None
+    Q = (L + 1) // 4
+    R = (Q - 1) // 2
+    return 2 * (3 * Q * Q + 2 * R * R) + (8 * Q - 4 + 2 * R)
+
+
+def work_model(N, N0, m0, s, boxes_1d, real_class_1d, n, refine=1, batch=1):
     """Algorithmic bytes / flops per vector for each phase.
 
     boxes_1d: 1-D box lengths; real_class_1d: whether each 1-D box pencil is real
-    (middle class, V real) -- a product with real V costs 2 real flops per complex MAC,
-    complex V 8.  Bytes are the operator's own minimal I/O (inputs read once, output
-    written once, setup factors read once), not the traffic of the chosen multi-pass
-    implementation, so the fractions below are honest headroom.
+    (middle class, V real).  Flops are those of the algorithm the kernels run: boxes with the
+    middle pencil on both axes take four fast sine transforms per line (dst_flops) and the
+    eigenvalue scaling; every other box the four one-sided dense products (2 real flops per
+    complex MAC with real V, 8 with complex V).  Bytes are the operator's own minimal I/O
+    (inputs read once, output written once, plan constants read once PER BATCH), not the
+    traffic of the chosen multi-pass implementation, so the fractions below are honest headroom.
     """
     cplx = s == 16
-    # local FDM: per box, 4 one-sided products: (Ly^2 Lx + Ly Lx^2) MACs twice
+    parts = 2 if cplx else 1
     F_loc = 0
     for Ly, ry in zip(boxes_1d, real_class_1d):
         fy = 2 if (ry or not cplx) else 8
         for Lx, rx in zip(boxes_1d, real_class_1d):
             fx = 2 if (rx or not cplx) else 8
-            F_loc += 2 * (Ly * Ly * Lx * fy + Ly * Lx * Lx * fx)
-    if not cplx:
-        F_loc //= 1  # MP-1: real data and real V: 2 flops per MAC already counted
+            fast = dst_flops(Lx) if (rx and ry and Lx == Ly) else None
+            if fast is not None:  # 4 transforms of `parts * L` lines + the eigenvalue reciprocals
+                F_loc += 4 * parts * Lx * fast + parts * Lx * Ly
+            else:  # 4 one-sided products: (Ly^2 Lx + Ly Lx^2) MACs twice
+                F_loc += 2 * (Ly * Ly * Lx * fy + Ly * Lx * Lx * fx)
     # coarse: (1 + refine) fast solves; per solve 2 length-(n-1) FFTs per row
     # (5 L log2 L real flops each) and the O(m0^2) band / strip work
     L = n - 1
     fft = 2 * m0 * 5 * L * np.log2(L) * (1 if cplx else 0.5)
     F_c = (1 + refine) * (fft + (40 * m0 * m0 if cplx else 0))
-    coarse_bytes = 2 * N0 * s + (7 * m0 * m0 * s + m0 * m0 * 4 if cplx else 0)
+    # Sommerfeld: compact band factors (5 complex per row and mode) and the four folded
+    # Woodbury strip matrices (m0^2 / 2 complex each) are read once per batch
+    coarse_bytes = 2 * N0 * s + ((5 * m0 * m0 * s + 2 * m0 * m0 * s) / batch if cplx else 0)
     return {
         "A x": {"bytes": 2 * N * s, "flops": 0},
         "R0 x": {"bytes": (N + N0) * s, "flops": 0},
@@ -134,13 +150,17 @@ def work_model(N, N0, m0, s, boxes_1d, real_class_1d, n, refine=1):
 
 
 def dram_traffic(phase):
-    """DRAM bytes per batch of the phase's kernels from the committed ncu --set full capture
-    (profiles/dram_traffic_r01.json: dram__bytes_read.sum + dram__bytes_write.sum), or None."""
+    """DRAM bytes per batch of the phase's kernels from the committed ncu launch list
+    (profiles/dram_traffic_r02.json: dram__bytes_read.sum + dram__bytes_write.sum), or None."""
     try:
-        with open(os.path.join(ROOT, "profiles", "dram_traffic_r01.json")) as f:
-            return json.load(f).get(phase)
+        for name in ("dram_traffic_r02.json", "dram_traffic_r01.json"):
+            path = os.path.join(ROOT, "profiles", name)
+            if os.path.exists(path):
+                with open(path) as f:
+                    return json.load(f).get(phase)
     except Exception:
-        return None
+        pass
+    return None
 
 
 def composite_roof(model, bw_gbs, p64_tf):
@@ -227,7 +247,7 @@ def run_ours(a, rank, world, local_rank):
     s = 16
     nu = grid.unknowns_per_dim
     model = work_model(N, N0, m0, s, [L for _, L in dec.boxes],
-                       [not (st0 == 0 or st0 + L == nu) for st0, L in dec.boxes], a.n)
+                       [not (st0 == 0 or st0 + L == nu) for st0, L in dec.boxes], a.n, batch=B)
     comp = {}
     for name, fn in phases.items():
         for _ in range(2):
