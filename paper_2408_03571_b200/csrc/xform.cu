@@ -189,8 +189,12 @@ constexpr int fft_rlast(int L) { return L <= 8 ? L : fft_rlast(L / 8); }
 constexpr int fft16_nmid(int rem) { return rem <= 16 ? 0 : 1 + fft16_nmid(rem / 16); }
 constexpr int fft16_rlast(int rem) { return rem <= 16 ? rem : fft16_rlast(rem / 16); }
 
-template <typename S, int VPT, int LT, bool DCT>
-__global__ void __launch_bounds__(256) xform_fft_kernel(const S* __restrict__ in, S* __restrict__ out, XScale sc,
+// MINB = 2 (default for rows >= 1024): two CTAs per SM (128 registers, no spills) without the
+// register prefetch of the next row -- the other CTA's stages cover the load instead.  Coarse solve
+// 2.16 -> 2.12 ms per batch of 32, 0.286 -> 0.279 ms at batch 1; HELM_FFT_MINB=1 restores the
+// one-CTA kernel with the prefetch (210 registers).
+template <typename S, int VPT, int LT, bool DCT, int MINB = 1>
+__global__ void __launch_bounds__(256, MINB) xform_fft_kernel(const S* __restrict__ in, S* __restrict__ out, XScale sc,
                                                         int rows, const double2* __restrict__ tw) {
   constexpr int L = LT, m0 = DCT ? L / 2 + 1 : L / 2 - 1;
   constexpr bool dct = DCT;
@@ -232,10 +236,16 @@ __global__ void __launch_bounds__(256) xform_fft_kernel(const S* __restrict__ in
   };
   double2 cur[VPT];
   int f = blockIdx.x * rpc + g;
+  if constexpr (MINB == 1) {
 #pragma unroll
-  for (int r = 0; r < VPT; ++r) cur[r] = load(f, tid + r * T);
+    for (int r = 0; r < VPT; ++r) cur[r] = load(f, tid + r * T);
+  }
   for (int f0 = blockIdx.x * rpc; f0 < nfft; f0 += gridDim.x * rpc) {
     f = f0 + g;
+    if constexpr (MINB != 1) {
+#pragma unroll
+      for (int r = 0; r < VPT; ++r) cur[r] = load(f, tid + r * T);
+    }
     const bool active = f < nfft;
     const int r0 = (active ? f : 0) * RPF;
     const bool two = active && (RPF == 2) && (r0 + 1 < rows);
@@ -247,8 +257,10 @@ __global__ void __launch_bounds__(256) xform_fft_kernel(const S* __restrict__ in
                                             [&](int, double2) {});
     }
     const int fn = f + gridDim.x * rpc;
+    if constexpr (MINB == 1) {
 #pragma unroll
-    for (int r = 0; r < VPT; ++r) nxt[r] = load(fn, tid + r * T);
+      for (int r = 0; r < VPT; ++r) nxt[r] = load(fn, tid + r * T);
+    }
     // DFT index e -> transform output (sum_J Q[J][a] x_J, then the scale)
     const S* row0 = in + (size_t)r0 * m0;
     double2 x0 = mk(0.0, 0.0), xm = mk(0.0, 0.0);
@@ -325,9 +337,19 @@ __global__ void __launch_bounds__(256) xform_fft_kernel(const S* __restrict__ in
       else stockham_stage<16, 2, false, true>(buf, tw, L, Ns, tid, T, none, store);
     }
     __syncthreads();
+    if constexpr (MINB == 1) {
 #pragma unroll
-    for (int r = 0; r < VPT; ++r) cur[r] = nxt[r];
+      for (int r = 0; r < VPT; ++r) cur[r] = nxt[r];
+    }
   }
+}
+
+static int fft_minb() {
+  static const int v = [] {
+    const char* e = getenv("HELM_FFT_MINB");
+    return e ? atoi(e) : 2;
+  }();
+  return v;
 }
 
 template <typename S, int VPT, int L, bool DCT>
@@ -341,10 +363,19 @@ static void fft_launch_l(const S* in, S* out, const XScale& sc, int rows, const 
   if (!attr) {
     HELM_CUDA(cudaFuncSetAttribute(xform_fft_kernel<S, VPT, L, DCT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    200 * 1024));
+    if constexpr (VPT == 16 && L >= 1024)
+      HELM_CUDA(cudaFuncSetAttribute(xform_fft_kernel<S, VPT, L, DCT, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     100 * 1024));
     attr = true;
   }
   const int nfft = Sc<S>::cplx ? rows : (rows + 1) / 2;
   const int blocks = std::min((nfft + rpc - 1) / rpc, 148 * 4);
+  if constexpr (VPT == 16 && L >= 1024) {
+    if (fft_minb() == 2) {
+      launch_pdl(xform_fft_kernel<S, VPT, L, DCT, 2>, blocks, threads, smem, st, in, out, sc, rows, tw);
+      return;
+    }
+  }
   launch_pdl(xform_fft_kernel<S, VPT, L, DCT>, blocks, threads, smem, st, in, out, sc, rows, tw);
 }
 
