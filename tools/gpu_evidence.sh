@@ -1,5 +1,6 @@
-# Round-2 evidence: smoke, pytest -m gpu, bench (driver flags), reference arm, launch lists (batch 32 / 1),
-# ncu --set full of the top kernel, SASS instruction mix of the library.
+# Round evidence: smoke, pytest -m gpu, bench (driver flags), reference arm, then the launch lists (batch 32 / 1)
+# and ncu --set full captures of the top kernels (tools/gpu_lists.sh: host setup, so the profiled process
+# launches only this library's kernels).
 mkdir -p gpurun_out
 TAG=${TAG:-r02}
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,clocks_event_reasons.active --format=csv > gpurun_out/smi_$TAG.txt
@@ -8,9 +9,4 @@ timeout 1800 python -m pytest tests -m gpu -q -s > gpurun_out/pytest_gpu_$TAG.tx
 tail -1 gpurun_out/pytest_gpu_$TAG.txt
 timeout 900 python bench.py --steps 20 --warmup 5 > gpurun_out/bench_$TAG.log 2>&1; echo bench=$?
 if [ "${REF:-1}" = "1" ]; then timeout 1200 python bench.py --impl reference --steps 20 --warmup 5 > gpurun_out/bench_ref_$TAG.log 2>&1; echo ref=$?; fi
-CMD="python tools/profile_ops.py --gmres 0 --only M^-1 --reps 1 --batches 32"
-$CMD > /dev/null 2>&1
-ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file gpurun_out/launches_M_$TAG.csv $CMD > /dev/null 2>&1; echo ncu32=$?
-CMD1="python tools/profile_ops.py --gmres 0 --only M^-1 --reps 1 --batches 1"
-ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file gpurun_out/launches_M_b1_$TAG.csv $CMD1 > /dev/null 2>&1; echo ncu1=$?
-ncu --set full --clock-control none --import-source on -k regex:local_fdm_dmma -s 1 -c 1 -o gpurun_out/top_kernel_$TAG $CMD > /dev/null 2>&1; echo ncufull=$?
+KERNELS="${KERNELS:-local_dst_kernel band_tma_kernel xform_fft_kernel}" bash tools/gpu_lists.sh
