@@ -161,8 +161,9 @@ template <int NP, int Q> struct DstGeo {
 };
 
 struct TmaDst {
-  CUtensorMap map;  // dims {2 nu, nu, batch} doubles, box {2 L, L, 1}
-  int on;
+  CUtensorMap map;   // dims {2 nu, nu, batch} doubles, box {2 L, L, 1}
+  CUtensorMap cmap;  // coarse base: dims {2 m0, m0, batch} doubles, box {2 WIN, WIN, 1} (con != 0)
+  int on, con;
 };
 
 __device__ __forceinline__ void mbar_init_(uint64_t* bar, unsigned count) {
@@ -324,6 +325,37 @@ template <typename S> struct BoxOut {
       }
     }
   }
+  // The same x pass from the box's raw coarse window staged in shared memory (WIN x WIN, dense,
+  // zero outside the coarse grid: the tensor copy's out-of-bounds fill) at `raw`, which lies inside
+  // slot sl's own rx region: every tap of the thread's rows is read into registers before the
+  // barrier, the rows are written after it.  Called by all threads of the CTA (it synchronises).
+  template <int NG, int NR> __device__ void rx_from_window(const S* raw, int sl, int rg, int j, bool part) const {
+    const int tx = x0 + j - a.off;
+    const bool ex = (tx & 1) == 0;
+    const int V0 = (ex ? tx / 2 - 1 : (tx - 1) >> 1) - window_base(x0, a.off);
+    const double w0 = ex ? 0.125 : 0.5, w1 = ex ? 0.75 : 0.5, w2 = ex ? 0.125 : 0.0;
+    S c[NR][3];
+    if (part) {
+#pragma unroll
+      for (int i = 0; i < NR; ++i) {
+        const int u = rg + i * NG;
+#pragma unroll
+        for (int t = 0; t < 3; ++t) c[i][t] = u < WIN ? raw[u * WIN + V0 + t] : Sc<S>::zero();
+      }
+    }
+    __syncthreads();
+    if (part) {
+#pragma unroll
+      for (int i = 0; i < NR; ++i) {
+        const int u = rg + i * NG;
+        S row = Sc<S>::zero();
+        row = fma_(w0, c[i][0], row);
+        row = fma_(w1, c[i][1], row);
+        row = fma_(w2, c[i][2], row);
+        if (u < WIN) rx[(size_t)sl * rxs + u * Lx + j] = row;
+      }
+    }
+  }
   struct ColTerms {
     int mx, c5, c6;
   };
@@ -377,6 +409,14 @@ __global__ void __launch_bounds__(DstGeo<Sc<S>::cplx ? 2 : 1, Q>::NTH, 3)
   const bool cbase = base && a.coarse_base;
   int* meta = reinterpret_cast<int*>(smem_raw + (size_t)NB * G::XB + (cbase ? (size_t)NB * G::RXB : 0));
   S* rx = reinterpret_cast<S*>(smem_raw + (size_t)NB * G::XB);
+  // coarse-base windows by tensor copy: the raw WIN x WIN window of slot s is staged at the first
+  // 128-byte boundary inside the slot's own rx region (it must fit there: L >= WIN)
+  constexpr bool CWIN_FITS = NP == 2 && L >= WIN + 1;
+  const bool cwin = CWIN_FITS && cbase && tma.on && tma.con;
+  auto raw_win = [&](int s) {
+    const size_t off = ((size_t)s * WIN * L * sizeof(S) + 127) & ~(size_t)127;
+    return reinterpret_cast<S*>(smem_raw + (size_t)NB * G::XB + off);
+  };
 
   const int sid = boxes[blockIdx.x];
   const int ay = sid / a.p, ax = sid % a.p;
@@ -393,8 +433,12 @@ __global__ void __launch_bounds__(DstGeo<Sc<S>::cplx ? 2 : 1, Q>::NTH, 3)
     if (threadIdx.x == 0) {
       mbar_init_(&box_bar, 1);
       asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-      mbar_expect_tx_(&box_bar, (unsigned)(nslot * L * RS * sizeof(double)));
+      mbar_expect_tx_(&box_bar, (unsigned)(nslot * L * RS * sizeof(double)) +
+                                    (cwin ? (unsigned)(nslot * WIN * WIN * sizeof(S)) : 0u));
       for (int s = 0; s < nslot; ++s) tma_load_3d_(X(s), &tma.map, NP * x0, y0, b0 + s, &box_bar);
+      if (cwin)  // the raw coarse windows ride on the same barrier, into their slots' rx regions
+        for (int s = 0; s < nslot; ++s)
+          tma_load_3d_(raw_win(s), &tma.cmap, NP * window_base(x0, a.off), window_base(y0, a.off), b0 + s, &box_bar);
     }
   } else {
     for (int e = threadIdx.x; e < nslot * L * L; e += NTH) {
@@ -409,7 +453,7 @@ __global__ void __launch_bounds__(DstGeo<Sc<S>::cplx ? 2 : 1, Q>::NTH, 3)
   // prologue / epilogue thread map: NG row groups x L columns (NG * L <= NTH)
   constexpr int NG = NTH / L;
   const int cq = threadIdx.x % L, crg = threadIdx.x / L;
-  if (cbase && crg < NG) io.template init_rx_cols<NG>(base, b0, nslot, crg, cq);  // behind the box load
+  if (cbase && !cwin && crg < NG) io.template init_rx_cols<NG>(base, b0, nslot, crg, cq);  // behind the box load
   if (tma.on) {
     __syncthreads();  // the barrier is initialised before any thread waits on it
     mbar_wait_(&box_bar, 0);
@@ -417,6 +461,10 @@ __global__ void __launch_bounds__(DstGeo<Sc<S>::cplx ? 2 : 1, Q>::NTH, 3)
     cp_wait<0>();
   }
   __syncthreads();
+  if (cwin) {  // x pass of R0^T c from the staged windows (no global latency in the prologue)
+    constexpr int NR = (WIN + NG - 1) / NG;
+    for (int sl = 0; sl < nslot; ++sl) io.template rx_from_window<NG, NR>(raw_win(sl), sl, crg, cq, crg < NG);
+  }
 
   // vector of this thread in a pass: slot s, line (row or column) l, part (re / im)
   const int t = threadIdx.x;
@@ -600,6 +648,14 @@ static bool tma_on_dst() {  // HELM_TMA=0: cp.async box loads (A/B)
   return on;
 }
 
+static bool tma_window_on() {  // HELM_TMA_WINDOW=0: the coarse window by per-thread loads (A/B)
+  static const bool on = [] {
+    const char* e = getenv("HELM_TMA_WINDOW");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 template <typename S, int Q>
 static void dst_launch(const helm_plan* P, const S* x, const S* base, S* y, S* ovl, const LocalArgs& a, int batch,
                        cudaStream_t st) {
@@ -627,6 +683,17 @@ static void dst_launch(const helm_plan* P, const S* x, const S* base, S* y, S* o
                                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     HELM_CHECK(r == CUDA_SUCCESS, "cuTensorMapEncodeTiled failed for the fast-sine box load");
     tma.on = 1;
+    if (cbase && G::L >= WIN + 1 && tma_window_on()) {
+      const cuuint64_t cdims[3] = {(cuuint64_t)2 * a.m0, (cuuint64_t)a.m0, (cuuint64_t)batch};
+      const cuuint64_t cstrides[2] = {(cuuint64_t)a.m0 * 16, (cuuint64_t)a.m0 * a.m0 * 16};
+      const cuuint32_t cbox[3] = {(cuuint32_t)(2 * WIN), (cuuint32_t)WIN, 1};
+      const CUresult rc = encode_tiled_dst()(&tma.cmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<S*>(base),
+                                             cdims, cstrides, cbox, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                             CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      HELM_CHECK(rc == CUDA_SUCCESS, "cuTensorMapEncodeTiled failed for the coarse window load");
+      tma.con = 1;
+    }
   }
   dim3 grd(d.n_dst, (batch + G::NB - 1) / G::NB);
   launch_pdl(local_dst_kernel<S, Q>, grd, G::NTH, smem, st, x, base, y, ovl, (const int*)d.box_dst,
