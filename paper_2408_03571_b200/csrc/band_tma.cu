@@ -167,15 +167,17 @@ __global__ void __launch_bounds__(TBW* TNW) band_tma_kernel(const double2* __res
     const BandTmaStage& S = stg[c % TST];
     facL = reinterpret_cast<const double2(*)[TBW][2]>(&S.fac[0][0][0]);
     const int rows = min(TR, m0 - c * TR);
+    // all TR rows unconditionally (no early exit: the chunk's shared-memory reads can then be
+    // hoisted ahead of the recurrence); rows past the end of the last chunk compute on stale
+    // stage data, are never stored and feed nothing (the sweep ends there)
 #pragma unroll
     for (int rr = 0; rr < TR; ++rr) {
-      if (rr >= rows) break;
       const int j = c * TR + rr;
       const double2 l0 = facL[rr][t][0], l1 = facL[rr][t][1];
       const double2 x0 = r0v;
       const double2 x1 = fms_(l0, x0, r1v);
       const double2 x2 = fms_(l1, x0, r2v);
-      if (va && vb) zcol[(size_t)j * m0] = x0;
+      if (va && vb && rr < rows) zcol[(size_t)j * m0] = x0;
       double2 nx = mk(0.0, 0.0);
       if (j + 3 < m0) {  // rows past the end: the stage slot was not filled
         if (in) nx = S.vec[w][rr][t];
@@ -239,8 +241,7 @@ __global__ void __launch_bounds__(TBW* TNW) band_tma_kernel(const double2* __res
     BandTmaStage& S = stg[qn % TST];
     const int rows = min(TR, m0 - c * TR);
 #pragma unroll
-    for (int rr = 0; rr < TR; ++rr) {
-      if (rr >= rows) break;
+    for (int rr = 0; rr < TR; ++rr) {  // no early exit, as in the forward sweep
       const int j = m0 - 1 - (c * TR + rr);
       const int sl = TR - 1 - rr;  // slot of row j in the ascending box
       const double2 u0 = S.fac[sl][t][0], u1 = S.fac[sl][t][1], u2 = S.fac[sl][t][2];
@@ -250,7 +251,7 @@ __global__ void __launch_bounds__(TBW* TNW) band_tma_kernel(const double2* __res
       v = mul(v, u0);
       if constexpr (VALS)
         S.vec[w][sl][t] = v;  // the slot just read; the stage is refilled after the barrier below
-      else if (va && vb)
+      else if (va && vb && rr < rows)
         out[(size_t)b * N0 + (size_t)j * m0 + a] = add ? ::helm::add(v, acur[rr]) : v;
       y2 = y1;
       y1 = v;
