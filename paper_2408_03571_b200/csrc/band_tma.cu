@@ -38,8 +38,9 @@ struct __align__(128) BandTmaStage {
 static_assert(sizeof(BandTmaStage) % 128 == 0, "stages are TMA destinations");
 
 struct BandTmaMaps {
-  CUtensorMap in;   // [batch][m0][2 m0] doubles: right-hand sides (unused when in == null)
-  CUtensorMap z;    // the same view of `out` (the eliminated rows, read back by the backward sweep)
+  CUtensorMap in;    // [batch][m0][2 m0] doubles: right-hand sides (unused when in == null)
+  CUtensorMap z;     // the same view of `out` (the eliminated rows, read back by the backward sweep)
+  CUtensorMap corr;  // [m0][8 batch] doubles: strip correction rows (unused when corr == null)
 };
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
@@ -63,6 +64,13 @@ __device__ __forceinline__ void tb_bulk(void* dst, const void* src, unsigned byt
                    smem_u32(dst)),
                "l"(src), "r"(bytes), "r"(smem_u32(bar))
                : "memory");
+}
+__device__ __forceinline__ void tb_tensor2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::
+          "r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
 }
 __device__ __forceinline__ void tb_tensor3d(void* dst, const CUtensorMap* map, int c0, int c1, int c2,
                                             uint64_t* bar) {
@@ -125,17 +133,14 @@ __global__ void __launch_bounds__(TBW* TNW) band_tma_kernel(const double2* __res
     BandTmaStage& S = stg[c % TST];
     uint64_t* bar = &full[c % TST];
     const int j0 = c * TR, nr = min(TR, m0 - j0);
-    const int r0 = j0 + 3, ncr = max(0, min(TR, m0 - r0));
+    const int r0 = j0 + 3;
     unsigned bytes = (unsigned)nr * TBW * 2 * sizeof(double2);
     if (in) bytes += sizeof(S.vec);
-    if (corr) bytes += (unsigned)ncr * nb * 4 * sizeof(double2);
+    if (corr) bytes += sizeof(S.corr);
     tb_expect(bar, bytes);
     tb_bulk(&S.fac[0][0][0], L + 2 * (fbase + (size_t)j0 * TBW), (unsigned)nr * TBW * 2 * sizeof(double2), bar);
     if (in) tb_tensor3d(&S.vec[0][0][0], &maps.in, 2 * a0, r0, bg, bar);
-    if (corr)
-      for (int rr = 0; rr < ncr; ++rr)
-        tb_bulk(&S.corr[rr][0][0], corr + (size_t)(r0 + rr) * ldc + (size_t)bg * 4, (unsigned)nb * 4 * sizeof(double2),
-                bar);
+    if (corr) tb_tensor2d(&S.corr[0][0][0], &maps.corr, 8 * bg, r0, bar);  // rows / right-hand sides past the end: zeros
   };
   if (threadIdx.x == 0)
     for (int c = 0; c < TST && c < nch; ++c) issue_fwd(c);
@@ -188,7 +193,8 @@ __global__ void __launch_bounds__(TBW* TNW) band_tma_kernel(const double2* __res
       r2v = nx;
     }
     __syncthreads();  // every warp is done with the stage
-    if (threadIdx.x == 0 && c + TST < nch) issue_fwd(c + TST);
+    // the refill is issued by a different warp each chunk, so no warp is the straggler every time
+    if (threadIdx.x == ((c & (TNW - 1)) << 5) && c + TST < nch) issue_fwd(c + TST);
   }
   // the backward sweep reads the eliminated rows back through the TMA unit (async proxy)
   __threadfence();
@@ -287,7 +293,7 @@ __global__ void __launch_bounds__(TBW* TNW) band_tma_kernel(const double2* __res
       asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
     }
     __syncthreads();
-    if (threadIdx.x == 0 && c + TST < nch) issue_bwd(c + TST);
+    if (threadIdx.x == ((c & (TNW - 1)) << 5) && c + TST < nch) issue_bwd(c + TST);
   }
 }
 
@@ -335,6 +341,19 @@ void band_tma_launch(const helm_plan* P, const double2* in, double2* out, const 
   BandTmaMaps maps;
   std::memset(&maps, 0, sizeof(maps));
   make_map(&maps.z, out, d.m0, batch);
+  if (corr) {
+    const cuuint64_t dims[2] = {(cuuint64_t)8 * batch, (cuuint64_t)d.m0};
+    const cuuint64_t strides[1] = {(cuuint64_t)batch * 4 * 16};
+    const cuuint32_t box[2] = {8 * TNW, TR};
+    const cuuint32_t es[2] = {1, 1};
+    const CUresult r = encode_tiled_band()(&maps.corr, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double2*>(corr),
+                                           dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                           CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    HELM_CHECK(r == CUDA_SUCCESS, "cuTensorMapEncodeTiled failed for the strip correction");
+  } else {
+    maps.corr = maps.z;
+  }
   if (in) make_map(&maps.in, in, d.m0, batch);
   else maps.in = maps.z;
   dim3 grd((d.m0 + TBW - 1) / TBW, (batch + TNW - 1) / TNW);
