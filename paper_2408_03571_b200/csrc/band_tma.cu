@@ -51,6 +51,9 @@ __device__ __forceinline__ void tb_expect(uint64_t* bar, unsigned bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
                : "memory");
 }
+__device__ __forceinline__ void tb_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
 __device__ __forceinline__ void tb_wait(uint64_t* bar, unsigned parity) {
   asm volatile(
       "{\n .reg .pred p;\n TB_WAIT:\n"
@@ -83,7 +86,7 @@ __device__ __forceinline__ void tb_tensor3d(void* dst, const CUtensorMap* map, i
 
 // VALS / part / add / corr / in: as band_solve_kernel.
 template <bool VALS>
-__global__ void __launch_bounds__(TBW* TNW) band_tma_kernel(const double2* __restrict__ in, double2* __restrict__ out,
+__global__ void __launch_bounds__(TBW*(TNW + 1)) band_tma_kernel(const double2* __restrict__ in, double2* __restrict__ out,
                                                             const double2* __restrict__ L,
                                                             const double2* __restrict__ U, int m0, int batch,
                                                             const double2* __restrict__ corr,
@@ -95,7 +98,7 @@ __global__ void __launch_bounds__(TBW* TNW) band_tma_kernel(const double2* __res
   pdl_wait();  // PDL: the predecessor's writes are visible (no-op without PDL)
   extern __shared__ __align__(128) unsigned char sraw[];
   BandTmaStage* stg = reinterpret_cast<BandTmaStage*>(sraw);
-  __shared__ __align__(8) uint64_t full[TST];
+  __shared__ __align__(8) uint64_t full[TST], empty[TST];
   const int t = threadIdx.x & (TBW - 1), w = threadIdx.x / TBW;
   const int a0 = blockIdx.x * TBW, a = a0 + t;
   const bool va = a < m0;
@@ -120,7 +123,10 @@ __global__ void __launch_bounds__(TBW* TNW) band_tma_kernel(const double2* __res
   };
   if (threadIdx.x == 0) {
 #pragma unroll
-    for (int s = 0; s < TST; ++s) tb_init(&full[s], 1);
+    for (int s = 0; s < TST; ++s) {
+      tb_init(&full[s], 1);
+      tb_init(&empty[s], TNW);  // one arrival per consumer warp
+    }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
@@ -142,8 +148,35 @@ __global__ void __launch_bounds__(TBW* TNW) band_tma_kernel(const double2* __res
     if (in) tb_tensor3d(&S.vec[0][0][0], &maps.in, 2 * a0, r0, bg, bar);
     if (corr) tb_tensor2d(&S.corr[0][0][0], &maps.corr, 8 * bg, r0, bar);  // rows / right-hand sides past the end: zeros
   };
-  if (threadIdx.x == 0)
-    for (int c = 0; c < TST && c < nch; ++c) issue_fwd(c);
+  // chunk c: rows j = m0-1-(8c+rr), i.e. the ascending range [jlo, jlo+8), jlo = m0 - 8(c+1)
+  // (negative at the last chunk: the tensor load zero-fills, the factor copy skips them)
+  auto issue_bwd = [&](int c) {  // thread 0
+    const int qn = nch + c;
+    BandTmaStage& S = stg[qn % TST];
+    uint64_t* bar = &full[qn % TST];
+    const int jlo = m0 - TR * (c + 1);
+    const int skip = jlo < 0 ? -jlo : 0, nr = TR - skip;
+    const unsigned fb = (unsigned)nr * TBW * 3 * sizeof(double2);
+    tb_expect(bar, fb + (unsigned)sizeof(S.vec));
+    tb_bulk(&S.fac[skip][0][0], U + 3 * (fbase + (size_t)(jlo + skip) * TBW), fb, bar);
+    tb_tensor3d(&S.vec[0][0][0], &maps.z, 2 * a0, jlo, bg, bar);
+  };
+  // ---- producer warp (warp TNW): refills a stage as soon as the eight consumer warps have
+  // released it (empty barrier), so the consumers never meet at a CTA barrier inside a sweep
+  if (w == TNW) {
+    for (int qn = 0; qn < 2 * nch; ++qn) {
+      if (qn == nch) {  // the eliminated rows are complete and fenced before the TMA unit reads them
+        __syncthreads();
+      }
+      if (t == 0) {
+        const int use = qn / TST;
+        if (use > 0) tb_wait(&empty[qn % TST], (unsigned)(use - 1) & 1u);
+        if (qn < nch) issue_fwd(qn);
+        else issue_bwd(qn - nch);
+      }
+    }
+    return;
+  }
   double2 r0v, r1v, r2v;
   {
     const bool ok = va && vb;
@@ -192,9 +225,8 @@ __global__ void __launch_bounds__(TBW* TNW) band_tma_kernel(const double2* __res
       r1v = x2;
       r2v = nx;
     }
-    __syncthreads();  // every warp is done with the stage
-    // the refill is issued by a different warp each chunk, so no warp is the straggler every time
-    if (threadIdx.x == ((c & (TNW - 1)) << 5) && c + TST < nch) issue_fwd(c + TST);
+    __syncwarp();
+    if (t == 0) tb_arrive(&empty[c % TST]);  // this warp is done with the stage
   }
   // the backward sweep reads the eliminated rows back through the TMA unit (async proxy)
   __threadfence();
@@ -202,21 +234,6 @@ __global__ void __launch_bounds__(TBW* TNW) band_tma_kernel(const double2* __res
   __syncthreads();
 
   // ---------------- backward substitution ----------------
-  // chunk c: rows j = m0-1-(8c+rr), i.e. the ascending range [jlo, jlo+8), jlo = m0 - 8(c+1)
-  // (negative at the last chunk: the tensor load zero-fills, the factor copy skips them)
-  auto issue_bwd = [&](int c) {  // thread 0
-    const int qn = nch + c;
-    BandTmaStage& S = stg[qn % TST];
-    uint64_t* bar = &full[qn % TST];
-    const int jlo = m0 - TR * (c + 1);
-    const int skip = jlo < 0 ? -jlo : 0, nr = TR - skip;
-    const unsigned fb = (unsigned)nr * TBW * 3 * sizeof(double2);
-    tb_expect(bar, fb + (unsigned)sizeof(S.vec));
-    tb_bulk(&S.fac[skip][0][0], U + 3 * (fbase + (size_t)(jlo + skip) * TBW), fb, bar);
-    tb_tensor3d(&S.vec[0][0][0], &maps.z, 2 * a0, jlo, bg, bar);
-  };
-  if (threadIdx.x == 0)
-    for (int c = 0; c < TST && c < nch; ++c) issue_bwd(c);
   double2 y1 = mk(0.0, 0.0), y2 = mk(0.0, 0.0);
   // VALS: this lane reduces row (t >> 2) of a chunk over the 8 modes p*8 + vcol(i), p = t & 3
   const int vrow = t >> 2, vp = t & 3;
@@ -292,8 +309,8 @@ __global__ void __launch_bounds__(TBW* TNW) band_tma_kernel(const double2* __res
       // the generic-proxy writes above precede the TMA refill of this stage
       asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
     }
-    __syncthreads();
-    if (threadIdx.x == ((c & (TNW - 1)) << 5) && c + TST < nch) issue_bwd(c + TST);
+    __syncwarp();
+    if (t == 0) tb_arrive(&empty[qn % TST]);
   }
 }
 
@@ -358,10 +375,10 @@ void band_tma_launch(const helm_plan* P, const double2* in, double2* out, const 
   else maps.in = maps.z;
   dim3 grd((d.m0 + TBW - 1) / TBW, (batch + TNW - 1) / TNW);
   if (part)
-    launch_pdl(band_tma_kernel<true>, grd, TBW * TNW, smem, st, in, out, (const double2*)d.band_l,
+    launch_pdl(band_tma_kernel<true>, grd, TBW * (TNW + 1), smem, st, in, out, (const double2*)d.band_l,
                (const double2*)d.band_u, d.m0, batch, corr, d.strip_q, d.coarse_scale, batch * 4, add, part, maps);
   else
-    launch_pdl(band_tma_kernel<false>, grd, TBW * TNW, smem, st, in, out, (const double2*)d.band_l,
+    launch_pdl(band_tma_kernel<false>, grd, TBW * (TNW + 1), smem, st, in, out, (const double2*)d.band_l,
                (const double2*)d.band_u, d.m0, batch, corr, d.strip_q, d.coarse_scale, batch * 4, add, part, maps);
   HELM_LAUNCH_CHECK();
 }
