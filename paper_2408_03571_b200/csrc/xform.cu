@@ -210,6 +210,41 @@ __global__ void __launch_bounds__(256, MINB) xform_fft_kernel(const S* __restric
   const int nfft = (rows + RPF - 1) / RPF;
   constexpr int K = L / 2;
   constexpr int nst = fft_nst(L), rlast = fft_rlast(L);
+  // STAGED (MINB = 2, complex rows): the CTA's next rows (contiguous in memory) arrive by one
+  // cp.async.bulk into a raw-row buffer behind the FFT buffers while the current rows are in
+  // their shared-memory stages; the symmetric extension is then read from shared memory (each
+  // element fetched from HBM once instead of twice, no global-load latency in the loop)
+  constexpr bool STAGED = MINB != 1 && Sc<S>::cplx;
+  double2* rawrows = reinterpret_cast<double2*>(sraw) + (size_t)rpc * (VPT == 16 ? padded_len16(L) : padded_len(L));
+  __shared__ __align__(8) unsigned long long rawbar;
+  auto raw_issue = [&](int fb) {  // thread 0: rows fb .. fb + rpc - 1 (clamped to nfft)
+    const int nv = min(rpc, nfft - fb);
+    if (nv <= 0) return;
+    const unsigned bytes = (unsigned)nv * m0 * (unsigned)sizeof(double2);
+    const unsigned bar = (unsigned)__cvta_generic_to_shared(&rawbar);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                     (unsigned)__cvta_generic_to_shared(rawrows)),
+                 "l"(reinterpret_cast<const double2*>(in) + (size_t)fb * m0), "r"(bytes), "r"(bar)
+                 : "memory");
+  };
+  auto raw_wait = [&](unsigned parity) {
+    asm volatile(
+        "{\n .reg .pred p;\n FFT_RAW_WAIT:\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra FFT_RAW_WAIT;\n}\n" ::"r"((unsigned)__cvta_generic_to_shared(&rawbar)),
+        "r"(parity)
+        : "memory");
+  };
+  if constexpr (STAGED) {
+    if (threadIdx.x == 0) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"((unsigned)__cvta_generic_to_shared(&rawbar))
+                   : "memory");
+      asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+      raw_issue(blockIdx.x * rpc);
+    }
+    __syncthreads();
+  }
   // symmetric extension G(j) of FFT f (two real rows packed as re/im)
   auto load = [&](int f, int j) -> double2 {
     if (f >= nfft) return mk(0.0, 0.0);
@@ -227,7 +262,10 @@ __global__ void __launch_bounds__(256, MINB) xform_fft_kernel(const S* __restric
       J = L - j - 1;
       sg = -1.0;
     }
-    if constexpr (Sc<S>::cplx) {
+    if constexpr (STAGED) {
+      const double2 x = rawrows[(size_t)g * m0 + J];
+      return mk(sg * x.x, sg * x.y);
+    } else if constexpr (Sc<S>::cplx) {
       const double2 x = row0[J];
       return mk(sg * x.x, sg * x.y);
     } else {
@@ -242,7 +280,15 @@ __global__ void __launch_bounds__(256, MINB) xform_fft_kernel(const S* __restric
   }
   for (int f0 = blockIdx.x * rpc; f0 < nfft; f0 += gridDim.x * rpc) {
     f = f0 + g;
+    double2 x0s = mk(0.0, 0.0), xms = mk(0.0, 0.0);
     if constexpr (MINB != 1) {
+      if constexpr (STAGED) {
+        raw_wait((unsigned)((f0 - blockIdx.x * rpc) / (gridDim.x * rpc)) & 1u);
+        if (f < nfft) {
+          x0s = rawrows[(size_t)g * m0];
+          xms = rawrows[(size_t)g * m0 + m0 - 1];
+        }
+      }
 #pragma unroll
       for (int r = 0; r < VPT; ++r) cur[r] = load(f, tid + r * T);
     }
@@ -257,6 +303,9 @@ __global__ void __launch_bounds__(256, MINB) xform_fft_kernel(const S* __restric
                                             [&](int, double2) {});
     }
     const int fn = f + gridDim.x * rpc;
+    if constexpr (STAGED) {  // stage 1 ended with a CTA barrier: every thread has read its raw values
+      if (threadIdx.x == 0) raw_issue(f0 + gridDim.x * rpc);
+    }
     if constexpr (MINB == 1) {
 #pragma unroll
       for (int r = 0; r < VPT; ++r) nxt[r] = load(fn, tid + r * T);
@@ -265,7 +314,10 @@ __global__ void __launch_bounds__(256, MINB) xform_fft_kernel(const S* __restric
     const S* row0 = in + (size_t)r0 * m0;
     double2 x0 = mk(0.0, 0.0), xm = mk(0.0, 0.0);
     if (dct && active) {
-      if constexpr (Sc<S>::cplx) {
+      if constexpr (STAGED) {
+        x0 = x0s;
+        xm = xms;
+      } else if constexpr (Sc<S>::cplx) {
         x0 = row0[0];
         xm = row0[m0 - 1];
       } else {
@@ -357,7 +409,10 @@ static void fft_launch_l(const S* in, S* out, const XScale& sc, int rows, const 
   constexpr int T = L / VPT;
   const int threads = std::max(T, std::min(256, std::max(32, L)));
   const int rpc = threads / T;
-  const size_t smem = (size_t)(rpc * (VPT == 16 ? padded_len16(L) : padded_len(L))) * sizeof(double2);
+  size_t smem = (size_t)(rpc * (VPT == 16 ? padded_len16(L) : padded_len(L))) * sizeof(double2);
+  constexpr int m0c = DCT ? L / 2 + 1 : L / 2 - 1;
+  const bool staged = VPT == 16 && L >= 1024 && Sc<S>::cplx && fft_minb() == 2;
+  if (staged) smem += (size_t)rpc * m0c * sizeof(double2);  // the raw-row buffer of the staged kernel
   HELM_CHECK(smem <= 200 * 1024 && threads <= 256, "coarse FFT row too long");
   static bool attr = false;
   if (!attr) {
@@ -365,7 +420,7 @@ static void fft_launch_l(const S* in, S* out, const XScale& sc, int rows, const 
                                    200 * 1024));
     if constexpr (VPT == 16 && L >= 1024)
       HELM_CUDA(cudaFuncSetAttribute(xform_fft_kernel<S, VPT, L, DCT, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     100 * 1024));
+                                     110 * 1024));
     attr = true;
   }
   const int nfft = Sc<S>::cplx ? rows : (rows + 1) / 2;
