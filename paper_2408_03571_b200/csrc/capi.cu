@@ -476,7 +476,9 @@ static void gmres_multi_impl(const helm_plan* P, helm_workspace* ws, const S* B,
 // ---------------------------------------------------------------------------
 static void build_plan(const helm_desc* d, helm_plan* P) {
   HELM_CHECK(d != nullptr, "null descriptor");
-  HELM_CHECK(d->n >= 5 && (d->n % 2) == 1, "n must be odd and >= 5");
+  // MP-1 needs odd n (discretization.py:172-173); MP-2 takes any n (discretization.py:183-188), the
+  // coarse ratio must then divide n - 1 (checked below), which excludes ratio 2 for even n
+  HELM_CHECK(d->n >= 5 && ((d->n % 2) == 1 || d->bc == HELM_SOMMERFELD), "n must be >= 5, and odd for MP-1");
   HELM_CHECK(d->bc == HELM_DIRICHLET || d->bc == HELM_SOMMERFELD, "unknown boundary condition");
   HELM_CHECK(d->is_complex == (d->bc == HELM_SOMMERFELD ? 1 : 0),
              "MP-1 (Dirichlet) plans are fp64, MP-2 (Sommerfeld) plans complex128");

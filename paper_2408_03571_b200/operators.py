@@ -182,8 +182,10 @@ def assemble(grid: Grid, k: float, problem: str) -> HelmholtzProblem:
     expected = "dirichlet" if problem == "MP1" else "sommerfeld"
     if grid.bc != expected:
         raise ValueError(f"{problem} requires a {expected} grid, got {grid.bc!r}")
-    if grid.n % 2 == 0:
-        raise ValueError("the GPU path needs odd n (H = 2h coarse grid, centre node source)")
+    # MP-2 accepts even n as the reference does (discretization.py:183-188: the load sits at the node
+    # nearest the centre); the coarse spaces then need a ratio that divides n - 1 (coarse.py:78-79)
+    if problem == "MP1" and grid.n % 2 == 0:
+        raise ValueError("MP1 needs odd n so the source at (1/2, 1/2) is a grid node")
     A = HelmholtzOperator(grid, k, problem)
     f = np.zeros(grid.num_unknowns, dtype=A.dtype)
     c = (grid.n - 1) // 2

@@ -24,6 +24,8 @@ CASES = [  # problem, n, k, coarse kind, ratio
     ("MP1", 97, 5.0, "HOCS", 16),
     ("MP2", 129, 30.0, "HOCS", 8),
     ("MP2", 61, 12.0, "FOCS", 3),
+    ("MP2", 64, 12.0, "FOCS", 3),  # even n (MP-2 only, discretization.py:183-188): ratios dividing n - 1
+    ("MP2", 46, 8.0, "FOCS", 5),
 ]
 
 

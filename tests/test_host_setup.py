@@ -275,3 +275,19 @@ def test_harness_config_mirror(tmp_path):
         Hh.emit_csv([], tmp_path / "e.csv")
     with pytest.raises(Hh.ConfigError):
         Hh.run_experiment(t1, backend="cpu")
+
+
+def test_even_n_follows_the_reference():
+    """discretization.py:172-173, 183-188: MP-1 needs odd n (same message), MP-2 takes even n with
+    the load at the node nearest the centre; coarse.py:78-79: the ratio must divide n - 1."""
+    import paper_2408_03571_b200 as hb
+
+    with pytest.raises(ValueError, match="MP1 needs odd n"):
+        hb.assemble(hb.Grid(46, "dirichlet"), 8.0, "MP1")
+    grid = hb.Grid(64, "sommerfeld")
+    prob = hb.assemble(grid, 12.0, "MP2")
+    c = (64 - 1) // 2
+    assert prob.f[grid.unknown_index(c, c)] == 1.0 / grid.h**2 and np.count_nonzero(prob.f) == 1
+    with pytest.raises(ValueError, match="does not divide"):
+        hb.build_hocs(grid, 2)
+    assert hb.build_focs(grid, 3).ratio == 3
